@@ -1,0 +1,379 @@
+"""Pins of the oracle against what the paper and the mathematics fix.
+
+Each test names the passage (PAPER.md line P:n) or the mathematical fact that
+pins the oracle function it exercises.  These run without a GPU.
+"""
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import discretization as D
+from oracle import mgrit as M
+from oracle import psi as P
+from oracle import theory as T
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- stencils
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_upwind_order_conditions(p):
+    """U_p is a p-th order approximation of d/dx: exact rational moments
+    sum_d w_d d^q / den = [q == 1] for q = 0..p, and failing at q = p+1."""
+    w, den = D.UPWIND[p]
+    for q in range(p + 1):
+        mom = sum(Fraction(wd) * Fraction(d) ** q for d, wd in w.items()) / den
+        assert mom == (1 if q == 1 else 0), (p, q, mom)
+    mom = sum(Fraction(wd) * Fraction(d) ** (p + 1) for d, wd in w.items()) / den
+    assert mom != 0
+    # odd orders: one-point upwind bias, even orders: two-point bias
+    assert (-min(w)) - max(w) == (1 if p % 2 == 1 else 2)
+    assert len(w) == p + 1
+
+
+# ---------------------------------------------------------------- tableaux
+def _exp_taylor(z, n):
+    return sum(z ** k / math.factorial(k) for k in range(n + 1))
+
+
+ZS = np.array([0.3 + 0.1j, -0.7 + 0.4j, -1.2 - 0.9j, 0.05j, -2.5 + 0.2j])
+
+
+@pytest.mark.parametrize("name,closed", [
+    ("erk1", lambda z: 1 + z),
+    ("erk2", lambda z: _exp_taylor(z, 2)),
+    ("erk3_ssp", lambda z: _exp_taylor(z, 3)),
+    ("erk3_kutta", lambda z: _exp_taylor(z, 3)),
+    ("erk4", lambda z: _exp_taylor(z, 4)),
+    # Butcher's 6-stage 5th-order method: b^T A^5 1 = 1/1280 (R7)
+    ("erk5", lambda z: _exp_taylor(z, 5) + z ** 6 / 1280.0),
+    ("sdirk1", lambda z: 1.0 / (1.0 - z)),
+])
+def test_stability_function_closed_form(name, closed):
+    """R(z) of each tableau (Lemma 1; tableaux)."""
+    R = D.stability_function(D.tableau(name), ZS)
+    np.testing.assert_allclose(R, closed(ZS), rtol=1e-14, atol=1e-15)
+
+
+def test_sdirk2_sdirk3_closed_forms():
+    """SDIRK2: R = (1 + (1-2g) z)/(1-g z)^2, g = 1 - sqrt(2)/2 (L-stable).
+    SDIRK3: R = (1 + (1-3z)x + (1/2-3z+3z^2)x^2)/(1-zeta x)^3 with zeta the root of
+    x^3 - 3x^2 + 3/2 x - 1/6."""
+    g = 1 - np.sqrt(2) / 2
+    np.testing.assert_allclose(D.stability_function(D.tableau("sdirk2"), ZS),
+                               (1 + (1 - 2 * g) * ZS) / (1 - g * ZS) ** 2, rtol=1e-14)
+    zeta = D.sdirk3_constants()[0]
+    assert abs(zeta ** 3 - 3 * zeta ** 2 + 1.5 * zeta - 1 / 6) < 1e-16
+    Pz = 1 + (1 - 3 * zeta) * ZS + (0.5 - 3 * zeta + 3 * zeta ** 2) * ZS ** 2
+    np.testing.assert_allclose(D.stability_function(D.tableau("sdirk3"), ZS),
+                               Pz / (1 - zeta * ZS) ** 3, rtol=1e-13)
+
+
+def test_sdirk4_order_and_lstability():
+    """SDIRK4 (Hairer-Wanner (6.16)): order 4 and L-stable."""
+    tab = D.tableau("sdirk4")
+    for z in [1e-2, 2e-2]:
+        err = D.stability_function(tab, np.array([z]))[0] - np.exp(z)
+        assert abs(err) < 5 * abs(z) ** 5
+    assert abs(D.stability_function(tab, np.array([-1e9]))[0]) < 1e-7
+    np.testing.assert_allclose(np.sum(np.array(tab.A), axis=1), tab.c, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", ["erk1", "erk2", "erk3_ssp", "erk3_kutta", "erk4", "erk5",
+                                  "sdirk1", "sdirk2", "sdirk3", "sdirk4"])
+def test_tableau_consistency(name):
+    tab = D.tableau(name)
+    assert abs(sum(tab.b) - 1.0) < 1e-14
+    np.testing.assert_allclose(np.sum(np.array(tab.A), axis=1), tab.c, atol=2e-15)
+    A = np.array(tab.A)
+    if tab.implicit:
+        assert np.allclose(np.diag(A), A[0, 0]) and np.allclose(np.triu(A, 1), 0)
+    else:
+        assert np.allclose(np.triu(A), 0)
+
+
+# ---------------------------------------------------------------- Phi
+SCHEMES = [(1, "erk1", 0.85), (2, "erk2", 0.425), (3, "erk3_ssp", 0.85), (3, "erk3_kutta", 0.85),
+           (4, "erk4", 0.85), (5, "erk5", 0.85), (1, "sdirk1", 4.0), (2, "sdirk2", 4.0),
+           (3, "sdirk3", 4.0), (4, "sdirk4", 4.0)]
+
+
+@pytest.mark.parametrize("order,tab,c", SCHEMES)
+def test_phi_on_fourier_modes(order, tab, c):
+    """Phi = R(dt L) on every grid mode (Lemma 1, Corollary 1 P:154):
+    the stage-form step applied to cos/sin(theta_k i) equals Re/Im of
+    R(lambda_k) e^{i theta_k i}, with lambda_k the Fourier symbol of Z."""
+    nx = 64
+    phi = D.make_phi(order, tab, c, nx)
+    i = np.arange(nx)
+    for k in [0, 1, 5, nx // 2 - 1, nx // 2]:
+        th = 2 * np.pi * k / nx
+        lam = D.stability_function(D.tableau(tab), np.array([D.stencil_symbol(phi.z, th)]))[0]
+        ref = lam * np.exp(1j * th * i)
+        np.testing.assert_allclose(phi(np.cos(th * i)), ref.real, atol=2e-14)
+        np.testing.assert_allclose(phi(np.sin(th * i)), ref.imag, atol=2e-14)
+
+
+def test_erk1_u1_cfl1_exact_shift():
+    """U1 + forward Euler at CFL 1 is the exact grid shift, bitwise."""
+    u = W.guess_rows(11, 64, np.array([3]))[0]
+    phi = D.make_phi(1, "erk1", 1.0, 64)
+    assert np.array_equal(phi(u), np.roll(u, 1))
+    U = D.sequential(phi, u, 64)
+    assert np.array_equal(U[64], u)
+
+
+@pytest.mark.parametrize("order,tab,c", SCHEMES)
+def test_constant_preservation(order, tab, c):
+    phi = D.make_phi(order, tab, c, 32)
+    np.testing.assert_allclose(phi(np.ones(32)), 1.0, atol=4e-15)
+
+
+def test_sdirk_stage_solve_residual():
+    """The implicit stage solve satisfies (I - zeta Z) y = b."""
+    phi = D.make_phi(3, "sdirk3", 4.0, 128)
+    zeta = D.sdirk3_constants()[0]
+    b = W.guess_rows(5, 128, np.array([0]))[0]
+    y = D.solve_circulant(b, phi._mcols[0])
+    res = y - zeta * D.apply_stencil(y, phi.z) - b
+    assert np.max(np.abs(res)) < 1e-13
+
+
+def _golden_cfl():
+    rows = []
+    for line in open(os.path.join(GOLDEN, "cfl_limits.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        s, tab, p, cmax = line.split()
+        rows.append((tab, int(p), float(cmax)))
+    return rows
+
+
+@pytest.mark.parametrize("tab,p,cmax", _golden_cfl())
+def test_cfl_limits_table1(tab, p, cmax):
+    """Table 1.  ERK5+U5 reproduces the printed 1.96583 only with a
+    |R| <= 1 + 1e-6 tolerance (R7)."""
+    excess = 1e-6 if p == 5 else 1e-13
+    c = D.cfl_limit(p, tab, ntheta=4001, tol=1e-7, excess=excess)
+    assert abs(c - cmax) < 2e-5, (tab, c, cmax)
+
+
+def test_sequential_equals_dense_spacetime_solve():
+    """Sequential stepping solves the block lower-bidiagonal space-time system."""
+    nx, nt = 16, 24
+    for order, tab, c in [(3, "erk3_ssp", 0.85), (3, "sdirk3", 4.0), (5, "erk5", 0.85)]:
+        phi = D.make_phi(order, tab, c, nx)
+        Phi = D.dense_matrix(phi, nx)
+        u0 = W.u0_fourier(nx, 1)
+        N = (nt + 1) * nx
+        A = np.eye(N)
+        for n in range(nt):
+            A[(n + 1) * nx:(n + 2) * nx, n * nx:(n + 1) * nx] = -Phi
+        rhs = np.zeros(N)
+        rhs[:nx] = u0
+        ref = np.linalg.solve(A, rhs).reshape(nt + 1, nx)
+        np.testing.assert_allclose(D.sequential(phi, u0, nt), ref, atol=1e-13)
+
+
+# ---------------------------------------------------------------- MGRIT
+def _setup(order, tab, c, nx, nt, seed=2, lo=-1.0):
+    phi = D.make_phi(order, tab, c, nx)
+    u0 = W.u0_fourier(nx, 1)
+    U = W.initial_iterate(seed, nx, nt, u0, lo)
+    dx = 2.0 / nx
+    return phi, U, dx, c * dx
+
+
+@pytest.mark.parametrize("order,tab,c,m,relax", [
+    (1, "erk1", 0.85, 2, "F"), (1, "erk1", 0.85, 4, "FCF"), (3, "erk3_kutta", 0.85, 4, "FCF"),
+    (3, "erk3_ssp", 0.85, 8, "F"), (5, "erk5", 0.85, 8, "FCF"), (3, "sdirk3", 4.0, 4, "FCF")])
+def test_ideal_psi_converges_in_one_iteration(order, tab, c, m, relax):
+    """Psi_ideal = Phi^m reaches the exact solution in a single iteration."""
+    nx, nt = 32, 128
+    phi, U, dx, dt = _setup(order, tab, c, nx, nt)
+    rep = M.solve(U, [phi, D.PowerPhi(phi, m)], m, dx, dt, relax, 1e-10, 5)
+    assert rep.iterations == 1 and rep.converged, rep.history
+    S = D.sequential(phi, U[0], nt)
+    assert np.max(np.abs(U - S)) < 1e-13
+
+
+@pytest.mark.parametrize("order,tab,c,m,relax", [
+    (1, "erk1", 0.85, 2, "F"), (1, "erk1", 0.85, 2, "FCF"), (3, "erk3_ssp", 0.85, 4, "F"),
+    (3, "erk3_ssp", 0.85, 4, "FCF"), (5, "erk5", 0.85, 8, "FCF")])
+def test_finite_termination(order, tab, c, m, relax):
+    """MGRIT reaches the exact discrete solution after nt/(2m) FCF (nt/m F) iterations
+    for any coarse operator: here Psi = 0.5 I."""
+    nx, nt = 16, 64
+    phi, U, dx, dt = _setup(order, tab, c, nx, nt)
+    psi = D.StencilPhi({0: 0.5}, nx)
+    kmax = nt // (2 * m) if relax == "FCF" else nt // m
+    for _ in range(kmax - 1):
+        M.vcycle(0, U, None, [phi, psi], m, relax)
+    S = D.sequential(phi, U[0], nt)
+    assert np.max(np.abs(U - S)) > 1e-6          # not yet exact one iteration earlier
+    M.vcycle(0, U, None, [phi, psi], m, relax)
+    # exact in exact arithmetic; in fp64 up to the rounding of the corrections
+    assert np.max(np.abs(U - S)) < 1e-13 * np.max(np.abs(S))
+
+
+def test_residual_of_sequential_solution_is_zero():
+    phi, U, dx, dt = _setup(3, "erk3_ssp", 0.85, 32, 64)
+    S = D.sequential(phi, U[0], 64)
+    assert M.residual_norm(S, phi, dx, dt) == 0.0
+
+
+def test_initial_row_pinned():
+    """Row 0 equals u0 bitwise after any number of iterations."""
+    phi, U, dx, dt = _setup(3, "erk3_ssp", 0.85, 32, 128)
+    u0 = U[0].copy()
+    psi = D.StencilPhi({-3: 0.1, -2: 0.4, -1: 0.4, 0: 0.1}, 32)
+    M.solve(U, [phi, psi], 4, dx, dt, "FCF", 1e-10, 3)
+    assert np.array_equal(U[0], u0)
+
+
+def test_iteration_count_independent_of_u0():
+    """Linear problem: iteration count depends on the initial error, not u0 (§4.5)."""
+    nx, nt, m = 64, 256, 4
+    phi = D.make_phi(3, "erk3_ssp", 0.85, nx)
+    fit = P.fit_hierarchy(phi, nx, m, 0.85, (9,))[0]
+    psi = D.StencilPhi(fit.stencil, nx)
+    ks = []
+    for u0 in (W.u0_fourier(nx, 1), W.u0_sin4(nx)):
+        U = W.initial_iterate(2, nx, nt, u0)
+        E0 = U - D.sequential(phi, u0, nt)               # same initial error both times
+        U = D.sequential(phi, u0, nt) + E0
+        U[0] = u0
+        ks.append(M.solve(U, [phi, psi], m, 2 / nx, 0.85 * 2 / nx, "FCF", 1e-10, 30).iterations)
+    assert ks[0] == ks[1]
+
+
+def test_multilevel_ideal_hierarchy_one_iteration():
+    """Ideal operators on every level make each coarse problem exact."""
+    nx, nt, m = 16, 256, 4
+    phi, U, dx, dt = _setup(3, "erk3_ssp", 0.85, nx, nt)
+    phis = [phi, D.PowerPhi(phi, m), D.PowerPhi(phi, m * m), D.PowerPhi(phi, m ** 3)]
+    rep = M.solve(U, phis, m, dx, dt, "FCF", 1e-10, 4)
+    assert rep.iterations == 1
+
+
+# ---------------------------------------------------------------- paper tables
+def _golden_iters():
+    rows = []
+    for line in open(os.path.join(GOLDEN, "iteration_tables.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        src, tab, p, nx, nt, m, kind, relax, k = line.split()
+        rows.append((src, tab, int(p), int(nx), int(nt), int(m), kind, relax, int(k)))
+    return rows
+
+
+@pytest.mark.parametrize("row", _golden_iters(), ids=lambda r: f"{r[0]}-{r[1]}-m{r[5]}")
+def test_paper_iteration_tables(row):
+    """tab:examples_IRK_redisc and tab:LSQlin_ERK under the
+    readings R1-Q1 (norm), R2 (counting), R3 (U[0,1) guess).  The paper's RNG stream
+    is unknown, so +-1 iteration is allowed (R16)."""
+    src, tab, p, nx, nt, m, kind, relax, kref = row
+    c = 4.0 if tab.startswith("sdirk") else 0.85
+    phi, U, dx, dt = _setup(p, tab, c, nx, nt, seed=0, lo=0.0)
+    U[0] = W.u0_sin4(nx)
+    if kind == "redisc":
+        psi = D.make_phi(p, tab, P.redisc_cfl(c, m), nx)
+    else:
+        # window of the nnz(Phi)+m/4 largest... : contiguous window of width
+        # 2,3,4 for m = 2,4,8 centred on -mc (R8)
+        nu = {2: 2, 4: 3, 8: 4}[m]
+        fit = P.fit_hierarchy(phi, nx, m, c, (nu,))[0]
+        assert fit.accepted
+        psi = D.StencilPhi(fit.stencil, nx)
+    rep = M.solve(U, [phi, psi], m, dx, dt, relax, 1e-10, 80)
+    assert rep.converged
+    assert abs(rep.iterations - kref) <= 1, (rep.iterations, kref, rep.history[-3:])
+
+
+# ---------------------------------------------------------------- Psi fit
+def test_lsq_unit_weight_is_truncation():
+    """Remark 1: W = I gives psi = R phi~^m (truncation of Phi^m)."""
+    nx, m = 128, 4
+    phi = D.make_phi(3, "erk3_ssp", 0.85, nx)
+    col = P.ideal_first_column(phi, nx, m)
+    offs = list(range(-9, 2))
+    res = P.lsq_psi(col, None, offs, w=np.ones(nx))
+    np.testing.assert_allclose(res.coeffs, [col[(-d) % nx] for d in offs], atol=1e-14)
+
+
+def test_lsq_full_pattern_recovers_ideal():
+    nx, m = 32, 2
+    phi = D.make_phi(3, "erk3_ssp", 0.85, nx)
+    col = P.ideal_first_column(phi, nx, m)
+    lam = P.eigenvalues(phi(np.eye(nx)[0]))
+    offs = list(range(-nx // 2 + 1, nx // 2 + 1))
+    res = P.lsq_psi(col, lam, offs)
+    np.testing.assert_allclose(res.coeffs, [col[(-d) % nx] for d in offs], atol=1e-10)
+
+
+@pytest.mark.parametrize("tab,p,m,nu", [("erk3_kutta", 3, 4, 9), ("erk5", 5, 8, 15),
+                                        ("erk1", 1, 4, 3), ("erk3_ssp", 3, 16, 13)])
+def test_lsq_solution_real(tab, p, m, nu):
+    """Lemma 3: the LSQ solution is real; characteristic windows are
+    never flagged."""
+    nx = 256
+    phi = D.make_phi(p, tab, 0.85, nx)
+    fit = P.fit_hierarchy(phi, nx, m, 0.85, (nu,))[0]
+    assert fit.imag_residue < 1e-8 and fit.accepted
+    mu = D.stencil_symbol(fit.stencil, 2 * np.pi * np.arange(nx) / nx)
+    assert np.max(np.abs(mu)) < 1 + 1e-6
+
+
+def test_threshold_pattern_sdirk3_cfg4():
+    """eta = 0.01 thresholding of Phi^4 for SDIRK3+U3, c = 4: a contiguous
+    window around the characteristic departure point (about -4m)."""
+    nx = 1024
+    phi = D.make_phi(3, "sdirk3", 4.0, nx)
+    col = P.ideal_first_column(phi, nx, 4)
+    offs = P.threshold_pattern(col, 0.01)
+    assert offs[0] <= -20 and offs[-1] >= -8 and 20 <= len(offs) <= 40
+
+
+# ---------------------------------------------------------------- theory
+def test_bound_dominates_dense_propagator():
+    """eq. (Dobrev_bounds) P:283-293 bounds the exact two-level FCF error propagator
+    of each Fourier mode, and is tight up to O(m/nt)."""
+    rng = np.random.default_rng(0)
+    gaps = []
+    for _ in range(12):
+        lam = 0.95 * rng.uniform(0.3, 1.0) * np.exp(1j * rng.uniform(0, np.pi))
+        m = int(rng.choice([2, 4]))
+        mu = lam ** m * (1 + 0.05 * (rng.uniform() - 0.5)) * np.exp(0.05j * rng.uniform())
+        if abs(mu) >= 0.99:
+            continue
+        g = []
+        for nt in (16 * m, 64 * m):
+            E = T.scalar_two_level_error_matrix(lam, mu, m, nt, "FCF")
+            nE = np.linalg.norm(E, 2)
+            b = T.fcf_bound(lam, mu, m, nt)
+            assert nE <= b * (1 + 1e-10) + 1e-14
+            g.append((b - nE) / b)
+        gaps.append(g)
+    assert np.mean([g[1] <= g[0] + 1e-12 for g in gaps]) >= 0.9
+    assert T.fcf_bound(0.7, 0.7 ** 4, 4, 64) < 1e-15
+    assert np.linalg.norm(T.scalar_two_level_error_matrix(0.7, 0.7 ** 4, 4, 64), 2) < 1e-14
+
+
+# ---------------------------------------------------------------- inputs
+def test_splitmix64_reference_values():
+    """Counter-based generator (R4): SplitMix64 reference outputs for
+    the state sequence starting at 0 (Vigna's splitmix64.c)."""
+    z = W.splitmix64(np.array([0, 0x9E3779B97F4A7C15], dtype=np.uint64))
+    assert int(z[0]) == 0xE220A8397B1DCDAF
+    assert int(z[1]) == 0x6E789E6AA1B965F4
+
+
+def test_uniform_ranges():
+    v = W.guess_rows(7, 4096, np.arange(3), lo=-1.0)
+    assert v.min() >= -1 and v.max() < 1 and abs(v.mean()) < 0.03
+    v = W.guess_rows(7, 4096, np.arange(3), lo=0.0)
+    assert v.min() >= 0 and v.max() < 1
