@@ -1,0 +1,190 @@
+/*
+ * mgrit.h — C ABI of the B200 MGRIT/Parareal library (libmgrit.so) for the periodic
+ * 1D constant-coefficient linear advection equation u_t + alpha u_x = 0.
+ *
+ * Paper: De Sterck, Falgout, Friedhoff, Krzysik, MacLachlan, "Optimizing MGRIT and
+ * Parareal coarse-grid operators for linear advection", arXiv:1910.03726.
+ * "P:n" = line n of PAPER.md; "S:n" = line n of SPEC.md.
+ *
+ * Conventions (apply to every entry point)
+ *  - All floating point is IEEE fp64.  Space-time arrays are row-major [t][x]: row n
+ *    (time t^n = n dt) holds nx contiguous doubles, x_i = -1 + i*2/nx (periodic).
+ *  - "_dev" pointers are CUDA device pointers, "_host" pointers host pointers.
+ *  - Ownership: the caller owns ALL device memory (the workspace, the guess, outputs)
+ *    and the CUDA stream.  The library never calls cudaMalloc/cudaFree; it carves the
+ *    caller's workspace.  Host arrays passed to mgrit_setup are copied.
+ *  - Every call is asynchronous on the context's stream except those that return host
+ *    values (mgrit_residual with norm_host, mgrit_solve, mgrit_profile_read), which
+ *    synchronise the stream.
+ *  - Errors: a negative mgrit_status; mgrit_last_error(ctx) gives a message.
+ *  - Stencil index convention: a circulant operator A is a stencil {d: a_d} with
+ *    (A u)_i = sum_d a_d u_{(i+d) mod nx}.
+ */
+#ifndef MGRIT_H
+#define MGRIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGRIT_MAX_LEVELS 8
+#define MGRIT_MAX_PSI_TAPS 64
+
+typedef enum {
+  MGRIT_OK = 0,
+  MGRIT_EINVAL = -1,      /* invalid argument (sizes, divisibility, pointers) */
+  MGRIT_ENOMEM = -2,      /* workspace too small */
+  MGRIT_ECUDA = -3,       /* CUDA launch/runtime error */
+  MGRIT_ENONFINITE = -4,  /* residual became NaN/Inf; history filled up to that point */
+  MGRIT_EUNSUPPORTED = -5 /* valid but not implemented combination */
+} mgrit_status;
+
+/* Runge-Kutta tableaux of Appendix A.  Order p pairs RK_p with U_p. */
+typedef enum {
+  MGRIT_TAB_ERK1 = 0,       /* Euler */
+  MGRIT_TAB_ERK2 = 1,       /* SSP RK2 */
+  MGRIT_TAB_ERK3_SSP = 2,   /* SSP RK3 */
+  MGRIT_TAB_ERK3_KUTTA = 3, /* Kutta RK3 (BASELINE.json cfg2) */
+  MGRIT_TAB_ERK4 = 4,       /* classical RK4 */
+  MGRIT_TAB_ERK5 = 5,       /* Butcher (236a) */
+  MGRIT_TAB_SDIRK1 = 6,     /* backward Euler */
+  MGRIT_TAB_SDIRK2 = 7,
+  MGRIT_TAB_SDIRK3 = 8,     /* P:999, zeta = 0.43586652150845899942 */
+  MGRIT_TAB_SDIRK4 = 9      /* Hairer-Wanner (6.16) */
+} mgrit_tableau;
+
+typedef enum { MGRIT_RELAX_F = 0, MGRIT_RELAX_C = 1, MGRIT_RELAX_FCF = 2 } mgrit_relax_kind;
+
+/* Coarse-grid time stepper Psi. */
+typedef enum {
+  MGRIT_PSI_STENCIL = 0, /* sparse circulant, e.g. the LSQ fit of eq. (LSQ_1D_problem) */
+  MGRIT_PSI_IDEAL = 1,   /* Psi = Phi^m */
+  MGRIT_PSI_REDISC = 2   /* Phi rediscretised with time step m dt, i.e. CFL redisc_cfl */
+} mgrit_psi_kind;
+
+typedef struct {
+  int kind;              /* mgrit_psi_kind */
+  int nnz;               /* STENCIL: number of taps (1..MGRIT_MAX_PSI_TAPS) */
+  const int *offsets;    /* STENCIL: host, nnz strictly increasing offsets d */
+  const double *coeffs;  /* STENCIL: host, nnz coefficients psi_d */
+  double redisc_cfl;     /* REDISC: CFL number of the coarse operator (m*c) */
+} mgrit_psi;
+
+typedef struct mgrit_ctx mgrit_ctx;
+
+/*
+ * Workspace size (bytes) for a problem; see mgrit_setup for the arguments.
+ * Returns 0 for invalid sizes.
+ */
+size_t mgrit_workspace_bytes(int nx, int nt, int m, int levels);
+
+/*
+ * mgrit_setup — create a solver context (north_star: mgrit_setup(nx, nt, m, alpha, CFL,
+ * scheme, levels, psi_coeffs)).
+ *   nx, nt      spatial points (periodic) and time steps; nt % m^(levels-1) == 0.
+ *   m           coarsening factor (>= 2) on every level.
+ *   alpha, cfl  wave speed (> 0) and CFL number c = alpha dt/dx; dx = 2/nx.
+ *   order       p of the upwind stencil U_p, 1..5.
+ *   tableau     mgrit_tableau; explicit tableaux need ERK, implicit SDIRK.
+ *   levels      2 = two-level MGRIT/Parareal; > 2 = multilevel V-cycle.
+ *   psi         host array of levels-1 coarse operators Psi_2..Psi_L (copied).  IDEAL and
+ *               REDISC are only valid for levels == 2.
+ *   relax       production relaxation of mgrit_solve: MGRIT_RELAX_F (Parareal) or
+ *               MGRIT_RELAX_FCF.
+ *   workspace_dev / workspace_bytes   caller-owned device memory, >= mgrit_workspace_bytes.
+ *   stream      cudaStream_t (NULL = legacy default stream).
+ * Errors: EINVAL (sizes, divisibility, tableau/order mismatch, nx too small for a stencil),
+ *         ENOMEM (workspace), EUNSUPPORTED.
+ */
+int mgrit_setup(mgrit_ctx **ctx, int nx, int nt, int m, double alpha, double cfl, int order,
+                int tableau, int levels, const mgrit_psi *psi, int relax,
+                void *workspace_dev, size_t workspace_bytes, void *stream);
+
+void mgrit_destroy(mgrit_ctx *ctx);
+const char *mgrit_last_error(const mgrit_ctx *ctx);
+
+/*
+ * The library's fp64 coefficients (host-only, no GPU needed): z_d of Z = dt L
+ * (z_d = (-c w_d)/den, R3), the tableau (A row-major s x s, b), and, for a
+ * STENCIL Psi of level l, its dense contiguous window.  Sizes: z[8], A[36], b[6].
+ */
+int mgrit_get_coefficients(const mgrit_ctx *ctx, int *s, int *z_lo, int *z_n, double *z,
+                           double *A, double *b);
+
+/*
+ * Same coefficients without a context (host-only): U_p stencil at CFL `cfl` and the
+ * tableau `tableau`.  Returns EINVAL for unknown ids.
+ */
+int mgrit_scheme_coefficients(int order, int tableau, double cfl, int *s, int *z_lo, int *z_n,
+                              double *z, double *A, double *b);
+
+/*
+ * mgrit_set_guess — register the initial space-time iterate: a FULL
+ * (nt+1) x nx device array whose row 0 is u0.  It is read, never written; the caller
+ * keeps it alive while solving.
+ */
+int mgrit_set_guess(mgrit_ctx *ctx, const double *guess_dev);
+
+/*
+ * FULL-state primitives on a caller-owned (nt+1) x nx device array U_dev (level 0 only),
+ * in place.  Row 0 is never written.
+ *   mgrit_relax:        kind F: U[jm+i] = Phi U[jm+i-1], i = 1..m-1;  C: U[(j+1)m] =
+ *                       Phi U[(j+1)m-1];  FCF: F then C then F.
+ *   mgrit_residual:     norm_host (nullable) = sqrt(dx dt sum_{n>=1} |Phi U[n-1] - U[n]|^2)
+ *                       over ALL rows (R1); r_dev (nullable, (nt/m+1) x nx)
+ *                       receives the C-point residuals r_j = Phi U[jm-1] - U[jm], r_0 = 0.
+ *   mgrit_coarse_solve: two-level coarse-grid correction: C-point residuals, sequential
+ *                       coarse solve e_j = Psi e_{j-1} + r_j, e_0 = 0 (eq. 3),
+ *                       U[jm] += e_j, then F-relaxation ("ideal interpolation").
+ */
+int mgrit_relax(mgrit_ctx *ctx, int level, int kind, double *U_dev);
+int mgrit_residual(mgrit_ctx *ctx, int level, const double *U_dev, double *norm_host,
+                   double *r_dev);
+int mgrit_coarse_solve(mgrit_ctx *ctx, int level, double *U_dev);
+
+/*
+ * mgrit_solve — MGRIT iterations from the registered guess until ||r^(k)|| < tol or
+ * k == max_iter (R2, R15).  Production engine: C-point storage, fused
+ * relax+residual+restriction sweeps, sequential (or V-cycle) coarse solve.
+ *   out_dev       nullable; FULL (nt+1) x nx solution (F-points materialised by an
+ *                 F-relaxation from the final C-points).
+ *   iters         iterations performed K.
+ *   hist_host     nullable, >= max_iter+1 doubles: ||r^(0)|| .. ||r^(K)||.
+ *   converged     1 if ||r^(K)|| < tol.
+ *   crows_hist_dev  nullable, max_iter x (nt/m+1) x nx: C-rows after every iteration.
+ * Returns MGRIT_ENONFINITE if the residual became NaN/Inf (history filled so far).
+ */
+int mgrit_solve(mgrit_ctx *ctx, double tol, int max_iter, double *out_dev, int *iters,
+                double *hist_host, int *converged, double *crows_hist_dev);
+
+/* C-rows (nt/m+1) x nx of the current iterate after mgrit_solve. */
+int mgrit_get_crows(mgrit_ctx *ctx, double *out_dev);
+
+/*
+ * Input generation (not part of the method; R4): fills rows [row0, row0+rows)
+ * of an iterate with the counter-based SplitMix64 uniform variates of (seed, n*nx+i);
+ * lo_kind 0: U[-1,1), 1: U[0,1).  If u0_dev is non-NULL and row0 == 0, row 0 := u0.
+ */
+int mgrit_fill_guess(double *dst_dev, long long row0, long long rows, int nx, uint64_t seed,
+                     int lo_kind, const double *u0_dev, void *stream);
+
+/*
+ * Profiling (bench.py): when enabled, every kernel launch is bracketed by CUDA events on
+ * the launching stream; mgrit_profile_read returns, per kernel class, the number of
+ * launches and the summed device milliseconds since the last reset.
+ * Classes: 0 fine sweep, 1 coarse-level sweeps, 2 coarse/sequential solves,
+ *          3 interpolation/materialisation, 4 residual, 5 reductions/other.
+ */
+#define MGRIT_PROF_CLASSES 6
+int mgrit_profile_enable(mgrit_ctx *ctx, int on);
+int mgrit_profile_read(mgrit_ctx *ctx, long long *launches, double *ms);
+/* Total kernel launches since setup (or the last profile reset). */
+long long mgrit_launch_count(const mgrit_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGRIT_H */

@@ -1,0 +1,261 @@
+"""Thin ctypes binding of libmgrit.so (include/mgrit.h).  Argument marshalling only:
+every step of the MGRIT path runs in the library's sm_100a kernels.  PyTorch provides
+device memory (the workspace, the guess, outputs) and the CUDA stream.
+
+The binding fails loudly when the library is missing: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmgrit.so")
+
+TABLEAU = {"erk1": 0, "erk2": 1, "erk3_ssp": 2, "erk3_kutta": 3, "erk4": 4, "erk5": 5,
+           "sdirk1": 6, "sdirk2": 7, "sdirk3": 8, "sdirk4": 9}
+RELAX = {"F": 0, "C": 1, "FCF": 2}
+PSI_KIND = {"stencil": 0, "ideal": 1, "redisc": 2}
+STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENONFINITE", -5: "EUNSUPPORTED"}
+PROF_CLASSES = ("fine_sweep", "level_sweep", "coarse_solve", "interp", "residual", "other")
+MAX_LEVELS = 8
+
+
+class MgritError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Psi(C.Structure):
+    _fields_ = [("kind", C.c_int), ("nnz", C.c_int), ("offsets", C.POINTER(C.c_int)),
+                ("coeffs", C.POINTER(C.c_double)), ("redisc_cfl", C.c_double)]
+
+
+_lib = None
+
+# (name, restype, argtypes) of every entry point declared in include/mgrit.h
+_SIGS = [
+    ("mgrit_workspace_bytes", C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    ("mgrit_setup", C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_double,
+                              C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(_Psi), C.c_int,
+                              C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("mgrit_destroy", None, [C.c_void_p]),
+    ("mgrit_last_error", C.c_char_p, [C.c_void_p]),
+    ("mgrit_get_coefficients", C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                         C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("mgrit_scheme_coefficients", C.c_int, [C.c_int, C.c_int, C.c_double, C.POINTER(C.c_int),
+                                            C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                            C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                            C.POINTER(C.c_double)]),
+    ("mgrit_set_guess", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("mgrit_relax", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    ("mgrit_residual", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_double),
+                                 C.c_void_p]),
+    ("mgrit_coarse_solve", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    ("mgrit_solve", C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.POINTER(C.c_int),
+                              C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p]),
+    ("mgrit_get_crows", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("mgrit_fill_guess", C.c_int, [C.c_void_p, C.c_longlong, C.c_longlong, C.c_int,
+                                   C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
+    ("mgrit_profile_enable", C.c_int, [C.c_void_p, C.c_int]),
+    ("mgrit_profile_read", C.c_int, [C.c_void_p, C.POINTER(C.c_longlong),
+                                     C.POINTER(C.c_double)]),
+    ("mgrit_launch_count", C.c_longlong, [C.c_void_p]),
+]
+
+
+def lib():
+    """Load libmgrit.so (built by paper_1910_03726_b200/build.py); raise if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1910_03726_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in _SIGS:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> List[str]:
+    return [s[0] for s in _SIGS]
+
+
+def _dptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    import torch
+    assert isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 \
+        and t.is_contiguous(), "expected a contiguous CUDA float64 tensor"
+    return t.data_ptr()
+
+
+def scheme_coefficients(order: int, tableau: str, cfl: float):
+    """Host-only: the library's z_d (d = z_lo..) and Butcher (A, b)."""
+    s, zlo, zn = C.c_int(), C.c_int(), C.c_int()
+    z = (C.c_double * 8)()
+    A = (C.c_double * 36)()
+    b = (C.c_double * 6)()
+    st = lib().mgrit_scheme_coefficients(order, TABLEAU[tableau], cfl, C.byref(s), C.byref(zlo),
+                                         C.byref(zn), z, A, b)
+    if st:
+        raise MgritError(st, "mgrit_scheme_coefficients")
+    S = s.value
+    zd = {zlo.value + k: z[k] for k in range(zn.value)}
+    Am = np.array(A[:]).reshape(6, 6)[:S, :S].copy()
+    return zd, Am, np.array(b[:S])
+
+
+def fill_guess(dst, seed: int, lo: float = -1.0, u0=None, row0: int = 0, stream=None):
+    """Fill a (rows, nx) CUDA float64 tensor with the counter-based guess (R4)."""
+    import torch
+    rows, nx = dst.shape
+    st = lib().mgrit_fill_guess(_dptr(dst), row0, rows, nx, seed, 0 if lo == -1.0 else 1,
+                                _dptr(u0), C.c_void_p(_stream(stream)))
+    if st:
+        raise MgritError(st, "mgrit_fill_guess")
+    return dst
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class MGRIT:
+    """One problem (nx, nt, m, scheme, Psi hierarchy) bound to a CUDA stream.
+
+    psi: list of levels-1 dicts: {"kind": "stencil", "offsets": [...], "coeffs": [...]},
+    {"kind": "ideal"} or {"kind": "redisc", "cfl": c'}.
+    """
+
+    def __init__(self, nx: int, nt: int, m: int, alpha: float, cfl: float, order: int,
+                 tableau: str, levels: int, psi: Sequence[Dict], relax: str = "FCF",
+                 stream=None, device: str = "cuda"):
+        import torch
+        self.nx, self.nt, self.m, self.levels = nx, nt, m, levels
+        self.alpha, self.cfl, self.order, self.tableau = alpha, cfl, order, tableau
+        self.relax = relax
+        self.dx = 2.0 / nx
+        self.dt = cfl * self.dx / alpha
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        nbytes = lib().mgrit_workspace_bytes(nx, nt, m, levels)
+        if nbytes == 0:
+            raise MgritError(-1, f"invalid sizes nx={nx} nt={nt} m={m} levels={levels}")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        arr = (_Psi * max(1, levels - 1))()
+        self._keep = []
+        for l, p in enumerate(psi):
+            kind = PSI_KIND[p["kind"]]
+            arr[l].kind = kind
+            if kind == 0:
+                offs = (C.c_int * len(p["offsets"]))(*[int(o) for o in p["offsets"]])
+                cof = (C.c_double * len(p["coeffs"]))(*[float(c) for c in p["coeffs"]])
+                self._keep += [offs, cof]
+                arr[l].nnz = len(p["offsets"])
+                arr[l].offsets = C.cast(offs, C.POINTER(C.c_int))
+                arr[l].coeffs = C.cast(cof, C.POINTER(C.c_double))
+            arr[l].redisc_cfl = float(p.get("cfl", 0.0))
+        ctx = C.c_void_p()
+        st = lib().mgrit_setup(C.byref(ctx), nx, nt, m, alpha, cfl, order, TABLEAU[tableau],
+                               levels, arr, RELAX[relax], self.workspace.data_ptr(), nbytes,
+                               C.c_void_p(self.stream.cuda_stream))
+        if st:
+            raise MgritError(st, "mgrit_setup failed (see stderr)")
+        self.ctx = ctx
+        self.guess = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None):
+                lib().mgrit_destroy(self.ctx)
+                self.ctx = None
+        except Exception:
+            pass
+
+    def _check(self, st, what):
+        if st:
+            msg = lib().mgrit_last_error(self.ctx)
+            raise MgritError(st, f"{what}: {msg.decode() if msg else ''}")
+
+    # ---- FULL-state primitives -----------------------------------------------
+    def relax_full(self, U, kind: str = "FCF"):
+        self._check(lib().mgrit_relax(self.ctx, 0, RELAX[kind], _dptr(U)), "mgrit_relax")
+
+    def residual_full(self, U, want_r: bool = False):
+        import torch
+        norm = C.c_double()
+        r = torch.empty((self.nt // self.m + 1, self.nx), dtype=torch.float64,
+                        device=U.device) if want_r else None
+        self._check(lib().mgrit_residual(self.ctx, 0, _dptr(U), C.byref(norm), _dptr(r)),
+                    "mgrit_residual")
+        return (norm.value, r) if want_r else norm.value
+
+    def coarse_solve_full(self, U):
+        self._check(lib().mgrit_coarse_solve(self.ctx, 0, _dptr(U)), "mgrit_coarse_solve")
+
+    # ---- production solve -------------------------------------------------------
+    def set_guess(self, guess):
+        assert tuple(guess.shape) == (self.nt + 1, self.nx)
+        self.guess = guess
+        self._check(lib().mgrit_set_guess(self.ctx, _dptr(guess)), "mgrit_set_guess")
+
+    def solve(self, tol: float = 1e-10, max_iter: int = 64, out=None, keep_crows: bool = False):
+        import torch
+        iters, conv = C.c_int(), C.c_int()
+        hist = (C.c_double * (max_iter + 1))()
+        crows = None
+        if keep_crows:
+            crows = torch.empty((max(1, max_iter), self.nt // self.m + 1, self.nx),
+                                dtype=torch.float64, device=self.guess.device)
+        st = lib().mgrit_solve(self.ctx, tol, max_iter, _dptr(out), C.byref(iters), hist,
+                               C.byref(conv), _dptr(crows))
+        k = iters.value
+        res = {"iterations": k, "history": list(hist[:k + 1]), "converged": bool(conv.value),
+               "status": st}
+        if keep_crows:
+            res["crows"] = crows[:k]
+        if st and st != -4:
+            self._check(st, "mgrit_solve")
+        return res
+
+    def crows(self):
+        import torch
+        out = torch.empty((self.nt // self.m + 1, self.nx), dtype=torch.float64,
+                          device=self.guess.device)
+        self._check(lib().mgrit_get_crows(self.ctx, _dptr(out)), "mgrit_get_crows")
+        return out
+
+    def coefficients(self):
+        s, zlo, zn = C.c_int(), C.c_int(), C.c_int()
+        z = (C.c_double * 8)()
+        A = (C.c_double * 36)()
+        b = (C.c_double * 6)()
+        self._check(lib().mgrit_get_coefficients(self.ctx, C.byref(s), C.byref(zlo), C.byref(zn),
+                                                 z, A, b), "coefficients")
+        S = s.value
+        return ({zlo.value + k: z[k] for k in range(zn.value)},
+                np.array(A[:]).reshape(6, 6)[:S, :S].copy(), np.array(b[:S]))
+
+    # ---- profiling --------------------------------------------------------------
+    def profile(self, on: bool = True):
+        self._check(lib().mgrit_profile_enable(self.ctx, 1 if on else 0), "profile_enable")
+
+    def profile_read(self):
+        n = (C.c_longlong * 6)()
+        ms = (C.c_double * 6)()
+        self._check(lib().mgrit_profile_read(self.ctx, n, ms), "profile_read")
+        return {k: (n[i], ms[i]) for i, k in enumerate(PROF_CLASSES)}
+
+    def launch_count(self) -> int:
+        return lib().mgrit_launch_count(self.ctx)

@@ -1,0 +1,394 @@
+// coarse.cu — coarse-grid kernels.
+//
+// Stencil coarse operators Psi are applied in *shifted* coordinates: with
+// contiguous offsets o0..o0+nu-1, a CTA's window origin moves by -o0 per step
+// and its valid length shrinks by nu-1 from the right, so the characteristic
+// shift (up to ~870 points on cfg5's coarsest level) costs no halo.
+//
+//  * psi_coarse_kernel: sequential solve x_n = Psi x_{n-1} + g_n over a block of
+//    steps, out_n = v_n + x_n (coarse error equation eq. (3) P:210 fused with the
+//    C-point correction P:212).  Trapezoid tiles: each CTA recomputes the
+//    dependency cone of its slice, so a launch needs no inter-CTA communication.
+//  * psi_sweep_kernel: FCF relaxation + residual + injection of V-cycle level l>=2
+//    (P:618-624), and its interpolation (correction fused into level l-1's C-rows).
+//  * rk_coarse_kernel: IDEAL (Phi^m) / REDISC Psi in Runge-Kutta form.
+#include "kernels.h"
+
+namespace mg {
+
+constexpr int PSI_EXT = MAX_PSI + 8;  // shared-memory tail for wrap/overrun reads
+
+__device__ __forceinline__ int wrapi(long long g, int nx) {
+  long long r = g % nx;
+  return (int)(r < 0 ? r + nx : r);
+}
+
+// x'[p] = sum_q psi_q s[base + p + q]  (s holds the current state, unpadded).
+template <int P>
+__device__ __forceinline__ void psi_apply(const double *__restrict__ s, int base,
+                                          const PsiOp &op, double (&out)[P]) {
+  double w[P + 3];
+#pragma unroll
+  for (int r = 0; r < P + 3; ++r) w[r] = s[pidx<P>(base + r)];
+#pragma unroll
+  for (int p = 0; p < P; ++p) out[p] = 0.0;
+  const int nu4 = (op.nu + 3) & ~3;
+#pragma unroll 1
+  for (int q0 = 0; q0 < nu4; q0 += 4) {
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const double c = op.psi[q0 + qq];
+#pragma unroll
+      for (int p = 0; p < P; ++p) out[p] = fma(c, w[p + qq], out[p]);
+    }
+#pragma unroll
+    for (int r = 0; r + 4 < P + 3; ++r) w[r] = w[r + 4];
+#pragma unroll
+    for (int r = P - 1; r < P + 3; ++r) w[r] = s[pidx<P>(base + q0 + 4 + r)];
+  }
+}
+
+// Write the state into s (padded layout) plus the periodic tail: logical
+// s[W + e] = s[e mod W] for e < PSI_EXT.
+template <int NT, int P>
+__device__ __forceinline__ void psi_put(double *s, const double (&x)[P]) {
+  constexpr int W = NT * P;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int l = t * P + p;
+    s[t * Pad<P>::SP + p] = x[p];
+    for (int e = l; e < PSI_EXT; e += W) s[pidx<P>(W + e)] = x[p];
+  }
+}
+
+// Shared-memory sizes (doubles) of the padded buffers.
+template <int NT, int P> struct PsiSmem {
+  static constexpr int SP = Pad<P>::SP;
+  static constexpr int X = (NT + PSI_EXT / P + 2) * SP;  // state + tail
+  static constexpr int G = NT * SP;                      // g window / staging
+  static constexpr int TOTAL = X + 2 * G;
+};
+
+// --------------------------------------------------------------------------
+template <int NT, int P>
+__global__ void __launch_bounds__(NT) psi_coarse_kernel(const __grid_constant__ CoarseArgs a) {
+  constexpr int W = NT * P;
+  extern __shared__ double smem[];
+  constexpr int SP = Pad<P>::SP;
+  double *sx = smem;                           // state + periodic tail (padded)
+  double *sg = sx + PsiSmem<NT, P>::X;         // g window (padded)
+  double *so = sg + PsiSmem<NT, P>::G;         // output staging (padded)
+  const int nx = a.nx, tid = threadIdx.x;
+  const int tile = blockIdx.x;
+  const int abeg = (int)(((long long)tile * nx) / a.ntiles);
+  const int T = (int)(((long long)(tile + 1) * nx) / a.ntiles) - abeg;
+  const int N = a.nsteps, o0 = a.op.o0;
+  // origin of step i: S_i = abeg + (N - i) * o0  (mod nx); S_N = abeg
+  double x[P];
+  {
+    const int S0 = wrapi((long long)abeg + (long long)N * o0, nx);
+    if (a.state_in) {
+      for (int q = tid; q < W; q += NT) {
+        int g = S0 + q;
+        if (g >= nx) g -= nx;
+        sx[pidx<P>(q)] = a.state_in[g];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int p = 0; p < P; ++p) x[p] = sx[tid * SP + p];
+    } else {
+#pragma unroll
+      for (int p = 0; p < P; ++p) x[p] = 0.0;
+    }
+  }
+#pragma unroll 1
+  for (int i = 1; i <= N; ++i) {
+    const long long n = a.n0 + i;
+    const int Si = wrapi((long long)abeg + (long long)(N - i) * o0, nx);
+    __syncthreads();
+    psi_put<NT, P>(sx, x);
+    const double *grow = a.g.base + (a.g.off + n * a.g.stride) * (long long)nx;
+    for (int q = tid; q < W; q += NT) {
+      int g = Si + q;
+      if (g >= nx) g -= nx;
+      sg[pidx<P>(q)] = __ldg(grow + g);
+    }
+    __syncthreads();
+    double y[P];
+    psi_apply<P>(sx, tid * P, a.op, y);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      x[p] = y[p] + sg[tid * SP + p];
+      so[tid * SP + p] = x[p];
+    }
+    __syncthreads();
+    double *orow = const_cast<double *>(a.out.base) + (a.out.off + n * a.out.stride) * (long long)nx;
+    const double *vrow = a.v.base ? a.v.base + (a.v.off + n * a.v.stride) * (long long)nx : nullptr;
+    for (int q = tid; q < T; q += NT) {
+      int g = Si + q;
+      if (g >= nx) g -= nx;
+      orow[g] = vrow ? vrow[g] + so[pidx<P>(q)] : so[pidx<P>(q)];
+    }
+  }
+  if (a.state_out) {
+    // S_N = abeg: the owned slice [abeg, abeg+T) is so[0..T)
+    for (int q = tid; q < T; q += NT) a.state_out[abeg + q] = so[pidx<P>(q)];
+  }
+}
+
+// --------------------------------------------------------------------------
+template <int NT, int P>
+__global__ void __launch_bounds__(NT) psi_sweep_kernel(const __grid_constant__ PsiSweepArgs a) {
+  constexpr int W = NT * P;
+  extern __shared__ double smem[];
+  constexpr int SP = Pad<P>::SP;
+  double *sx = smem;
+  double *sg = sx + PsiSmem<NT, P>::X;
+  double *so = sg + PsiSmem<NT, P>::G;
+  const int nx = a.nx, tid = threadIdx.x, m = a.m;
+  const int item = blockIdx.x / a.ntiles;
+  const int tile = blockIdx.x - item * a.ntiles;
+  const int abeg = (int)(((long long)tile * nx) / a.ntiles);
+  const int T = (int)(((long long)(tile + 1) * nx) / a.ntiles) - abeg;
+  const int o0 = a.op.o0;
+  const bool p2 = !a.interp && item < a.p2_items;
+  // total steps in this CTA and the origin of step i: S_i = abeg + (N - i) o0
+  const int N = a.interp ? (m - 1) : (p2 ? 2 * m : m);
+  auto origin = [&](int i) { return wrapi((long long)abeg + (long long)(N - i) * o0, nx); };
+  auto rowp = [&](const RowMap &r, long long j) {
+    return r.base + (r.off + j * r.stride) * (long long)nx;
+  };
+  auto load = [&](const double *row, int S, double *s) {
+    for (int q = tid; q < W; q += NT) {
+      int g = S + q;
+      if (g >= nx) g -= nx;
+      s[pidx<P>(q)] = __ldg(row + g);
+    }
+  };
+  // out[S..S+T) = (add ? add : 0) + x   (x staged through so)
+  auto store = [&](double *row, const double *add, int S, const double(&v)[P]) {
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < P; ++p) so[tid * SP + p] = v[p];
+    __syncthreads();
+    for (int q = tid; q < T; q += NT) {
+      int g = S + q;
+      if (g >= nx) g -= nx;
+      row[g] = add ? add[g] + so[pidx<P>(q)] : so[pidx<P>(q)];
+    }
+  };
+
+  double x[P];
+  if (a.u.base) {
+    load(rowp(a.u, item), origin(0), sx);
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = sx[tid * SP + p];
+  } else {
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = 0.0;
+  }
+  const long long grow0 = a.g.off + (long long)item * a.g.stride;   // row jm
+  if (a.interp) {
+    const long long orow0 = a.out2.off + (long long)item * a.out2.stride;
+    const long long vrow0 = a.v2.off + (long long)item * a.v2.stride;
+    store(const_cast<double *>(a.out2.base) + orow0 * nx, a.v2.base ? a.v2.base + vrow0 * nx : nullptr,
+          origin(0), x);
+  }
+  const int n1 = a.interp ? (m - 1) : m;
+#pragma unroll 1
+  for (int i = 1; i <= n1; ++i) {
+    __syncthreads();
+    psi_put<NT, P>(sx, x);
+    load(a.g.base + (grow0 + i) * nx, origin(i), sg);
+    __syncthreads();
+    double y[P];
+    psi_apply<P>(sx, tid * P, a.op, y);
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * SP + p];
+    if (a.interp) {
+      const long long orow = a.out2.off + (long long)item * a.out2.stride + i;
+      const long long vrow = a.v2.off + (long long)item * a.v2.stride + i;
+      store(const_cast<double *>(a.out2.base) + orow * nx, a.v2.base ? a.v2.base + vrow * nx : nullptr,
+            origin(i), x);
+    }
+  }
+  if (a.interp) return;
+  // v_{j+1}
+  store(const_cast<double *>(rowp(a.v, item)), nullptr, origin(m), x);
+  if (!p2) return;
+  if (a.ucmp.base) {
+    __syncthreads();
+    load(rowp(a.ucmp, item), origin(m), sg);
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] -= sg[tid * SP + p];
+  }
+#pragma unroll 1
+  for (int i = m + 1; i <= 2 * m; ++i) {
+    __syncthreads();
+    psi_put<NT, P>(sx, x);
+    __syncthreads();
+    psi_apply<P>(sx, tid * P, a.op, x);
+  }
+  store(const_cast<double *>(rowp(a.r2, item)), nullptr, origin(2 * m), x);
+}
+
+// --------------------------------------------------------------------------
+template <class SC, int NT, int P>
+__global__ void __launch_bounds__(NT) rk_coarse_kernel(const __grid_constant__ RKCoarseArgs a) {
+  extern __shared__ double smem[];
+  double *edge = smem;
+  const int tid = threadIdx.x, nx = a.nx;
+  int phase = 0;
+  double x[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) x[p] = 0.0;
+#pragma unroll 1
+  for (int n = 1; n <= a.nsteps; ++n) {
+#pragma unroll 1
+    for (int r = 0; r < a.q; ++r) erk_step<SC, P, NT>(x, a.co, edge, phase);
+    const double *g = a.g.base + (a.g.off + (long long)n * a.g.stride) * nx;
+    const double *v = a.v.base ? a.v.base + (a.v.off + (long long)n * a.v.stride) * nx : nullptr;
+    double *o = const_cast<double *>(a.out.base) + (a.out.off + (long long)n * a.out.stride) * nx;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int i = tid * P + p;
+      x[p] = x[p] + g[i];
+      o[i] = v ? v[i] + x[p] : x[p];
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) reduce_kernel(const double *__restrict__ p, long long n,
+                                                      double *out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 1024) s += p[i];
+  s = block_sum<1024>(s, red);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_guess_kernel(double *dst, long long row0, long long rows, int nx,
+                                  uint64_t seed, int lo_kind, const double *u0) {
+  const long long total = rows * (long long)nx;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / nx;
+    const int i = (int)(t - r * nx);
+    const long long n = row0 + r;
+    double val;
+    if (n == 0 && u0) {
+      val = u0[i];
+    } else {
+      const uint64_t idx = (uint64_t)n * (uint64_t)nx + (uint64_t)i;
+      const uint64_t k = splitmix64(idx + seed * 0x632BE59BD9B4E019ull) >> 11;
+      val = lo_kind == 0 ? (double)((long long)k - (1ll << 52)) * 0x1p-52
+                         : (double)k * 0x1p-53;
+    }
+    dst[t] = val;
+  }
+}
+
+// --------------------------------------------------------------------------
+#define MG_PSI_CFGS(X) \
+  X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8)
+
+template <int NT, int P>
+static cudaError_t launch_coarse_one(const CoarseArgs &a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * PsiSmem<NT, P>::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(psi_coarse_kernel<NT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  psi_coarse_kernel<NT, P><<<a.ntiles, NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NT, int P>
+static cudaError_t launch_psisweep_one(const PsiSweepArgs &a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * PsiSmem<NT, P>::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(psi_sweep_kernel<NT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  const long long grid = (long long)a.nitems * a.ntiles;
+  if (grid <= 0) return cudaSuccess;
+  psi_sweep_kernel<NT, P><<<(unsigned)grid, NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_psi_coarse(SweepCfg c, const CoarseArgs &a, cudaStream_t s) {
+  if (a.nsteps <= 0) return cudaSuccess;
+#define MG_CASE(NT_, P_) \
+  if (c.nt_threads == NT_ && c.p == P_) return launch_coarse_one<NT_, P_>(a, s);
+  MG_PSI_CFGS(MG_CASE)
+#undef MG_CASE
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_psi_sweep(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s) {
+#define MG_CASE(NT_, P_) \
+  if (c.nt_threads == NT_ && c.p == P_) return launch_psisweep_one<NT_, P_>(a, s);
+  MG_PSI_CFGS(MG_CASE)
+#undef MG_CASE
+  return cudaErrorInvalidConfiguration;
+}
+
+template <class SC>
+static cudaError_t launch_rkc(SweepCfg c, const RKCoarseArgs &a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (2 * (c.nt_threads / 32) * (SC::NL + SC::NR) + 4);
+  if (c.nt_threads == 32 && c.p == 2) {
+    rk_coarse_kernel<SC, 32, 2><<<1, 32, smem, s>>>(a);
+  } else if (c.nt_threads == 32 && c.p == 4) {
+    rk_coarse_kernel<SC, 32, 4><<<1, 32, smem, s>>>(a);
+  } else if (c.nt_threads == 32 && c.p == 8) {
+    rk_coarse_kernel<SC, 32, 8><<<1, 32, smem, s>>>(a);
+  } else if (c.nt_threads == 128 && c.p == 8) {
+    rk_coarse_kernel<SC, 128, 8><<<1, 128, smem, s>>>(a);
+  } else {
+    return cudaErrorInvalidConfiguration;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rk_coarse(int scheme, SweepCfg c, const RKCoarseArgs &a, cudaStream_t s) {
+  switch (scheme) {
+    case 0: return launch_rkc<ERK1U1>(c, a, s);
+    case 1: return launch_rkc<ERK2U2>(c, a, s);
+    case 2: return launch_rkc<ERK3U3>(c, a, s);
+    case 3: return launch_rkc<ERK4U4>(c, a, s);
+    case 4: return launch_rkc<ERK5U5>(c, a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_reduce(const double *partials, long long n, double *out, cudaStream_t s) {
+  reduce_kernel<<<1, 1024, 0, s>>>(partials, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_guess(double *dst, long long row0, long long rows, int nx, uint64_t seed,
+                              int lo_kind, const double *u0, cudaStream_t s) {
+  const long long total = rows * (long long)nx;
+  if (total <= 0) return cudaSuccess;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  fill_guess_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, row0, rows, nx, seed, lo_kind, u0);
+  return cudaGetLastError();
+}
+
+}  // namespace mg

@@ -1,0 +1,176 @@
+// device.cuh — register-tile building blocks of the MGRIT kernels (sm_100a).
+//
+// A CTA of NT threads holds a window of W = NT*P consecutive grid points of one
+// space-time row; thread t owns points [t*P, t*P+P) in registers.  Stencil
+// neighbours across threads come from warp shuffles; across warps from a tiny
+// double-buffered shared-memory edge buffer (one __syncthreads per stage).
+// Wrap-around between the last and the first thread is exact in periodic
+// (whole-row) mode and produces garbage only inside the discarded halo in tile
+// mode.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mg {
+
+constexpr int MAXS = 6;   // max RK stages (ERK5 has 6)
+constexpr int MAXZ = 8;   // max taps of Z = dt*L (U5 has 6)
+constexpr unsigned FULL = 0xffffffffu;
+
+// Runtime fp64 coefficients of one RK step (kernel parameter, constant bank).
+struct RKCoeffs {
+  double z[MAXZ];          // z_d for d = -NL .. NR (index d + NL)
+  double A[MAXS][MAXS];    // Butcher A
+  double b[MAXS];          // Butcher b
+  double mdiag[MAXS];      // SDIRK: a_ii (stage matrix I - a_ii Z)
+};
+
+// Compile-time structure of a scheme: stages, stencil reach, zero pattern.
+template <int S_, int NL_, int NR_, uint64_t AMASK_, unsigned BMASK_, bool IMPL_ = false>
+struct Scheme {
+  static constexpr int S = S_;
+  static constexpr int NL = NL_;   // left reach |d_min| of one Z application
+  static constexpr int NR = NR_;   // right reach d_max
+  static constexpr bool implicit = IMPL_;
+  __host__ __device__ static constexpr bool a_nz(int i, int l) {
+    return (AMASK_ >> (i * MAXS + l)) & 1ull;
+  }
+  __host__ __device__ static constexpr bool b_nz(int i) { return (BMASK_ >> i) & 1u; }
+};
+
+constexpr uint64_t abit(int i, int l) { return 1ull << (i * MAXS + l); }
+
+// ERKp + Up pairs.  Reach of U_p: U1 [-1,0], U2 [-2,0], U3 [-2,1], U4 [-3,1], U5 [-3,2].
+using ERK1U1 = Scheme<1, 1, 0, 0ull, 0x1u>;
+using ERK2U2 = Scheme<2, 2, 0, abit(1, 0), 0x3u>;
+using ERK3U3 = Scheme<3, 2, 1, abit(1, 0) | abit(2, 0) | abit(2, 1), 0x7u>;
+using ERK4U4 = Scheme<4, 3, 1, abit(1, 0) | abit(2, 1) | abit(3, 2), 0xFu>;
+using ERK5U5 = Scheme<6, 3, 2,
+                      abit(1, 0) | abit(2, 0) | abit(2, 1) | abit(3, 2) | abit(4, 0) |
+                          abit(4, 1) | abit(4, 2) | abit(4, 3) | abit(5, 0) | abit(5, 1) |
+                          abit(5, 2) | abit(5, 3) | abit(5, 4),
+                      0x3Du>;  // b2 = 0
+
+template <int N> struct Arr { double v[N > 0 ? N : 1]; };
+
+// ---------------------------------------------------------------------------
+// Halo exchange: L[k] = y of point (t*P - NL + k), R[k] = y of point (t*P + P + k).
+// `edge` holds 2 * NW * (NL+NR) doubles; `phase` toggles the half in use.
+// ---------------------------------------------------------------------------
+template <int NL, int NR, int P, int NT>
+__device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<NR> &R,
+                                         double *edge, int &phase) {
+  constexpr int NW = NT / 32;
+  constexpr int E = NL + NR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NL; ++k) L.v[k] = __shfl_up_sync(FULL, y[P - NL + k], 1);
+#pragma unroll
+  for (int k = 0; k < NR; ++k) R.v[k] = __shfl_down_sync(FULL, y[k], 1);
+  double *buf = edge + phase * (NW * E);
+  if (lane == 31) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) buf[warp * E + k] = y[P - NL + k];
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) buf[warp * E + NL + k] = y[k];
+  }
+  __syncthreads();
+  if (lane == 0) {
+    const int pw = (warp + NW - 1) % NW;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) L.v[k] = buf[pw * E + k];
+  }
+  if (lane == 31) {
+    const int nw = (warp + 1) % NW;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) R.v[k] = buf[nw * E + NL + k];
+  }
+  phase ^= 1;
+}
+
+// k = Z y, (Z y)_i = sum_{d=-NL}^{NR} z_d y_{i+d}, d ascending (oracle order).
+template <int NL, int NR, int P, int NT>
+__device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
+                                        const double *__restrict__ z, double *edge,
+                                        int &phase) {
+  Arr<NL> L;
+  Arr<NR> R;
+  exchange<NL, NR, P, NT>(y, L, R, edge, phase);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    double acc = 0.0;
+#pragma unroll
+    for (int d = -NL; d <= NR; ++d) {
+      const int q = p + d;
+      const double v = (q < 0) ? L.v[(NL + q) < 0 ? 0 : (NL + q)]
+                               : (q >= P ? R.v[(q - P) < NR ? (q - P) : 0] : y[q < P ? q : 0]);
+      acc = (d == -NL) ? z[0] * v : fma(z[d + NL], v, acc);
+    }
+    k[p] = acc;
+  }
+}
+
+// One explicit RK step in stage form (App. A):
+//   k_i = Z(x + sum_{l<i} a_il k_l),  x <- x + sum_i b_i k_i.
+// Partial stage sums are accumulated as soon as k_l is known (same summation
+// order as the oracle: l ascending).
+template <class SC, int P, int NT>
+__device__ __forceinline__ void erk_step(double (&x)[P], const RKCoeffs &c, double *edge,
+                                         int &phase) {
+  constexpr int S = SC::S;
+  double acc[S][P];
+  double out[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    out[p] = x[p];
+#pragma unroll
+    for (int i = 0; i < S; ++i) acc[i][p] = x[p];
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    double k[P];
+    apply_Z<SC::NL, SC::NR, P, NT>(acc[i], k, c.z, edge, phase);
+#pragma unroll
+    for (int l = i + 1; l < S; ++l) {
+      if (SC::a_nz(l, i)) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) acc[l][p] = fma(c.A[l][i], k[p], acc[l][p]);
+      }
+    }
+    if (SC::b_nz(i)) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) out[p] = fma(c.b[i], k[p], out[p]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) x[p] = out[p];
+}
+
+// Padded shared-memory layout of a window: thread t's P points start at t*SP,
+// SP = P rounded up to odd, so a warp reading element k of every thread hits
+// distinct bank pairs (2 wavefronts, the fp64 minimum).
+template <int P> struct Pad { static constexpr int SP = P | 1; };
+template <int P> __device__ __forceinline__ int pidx(int q) {
+  return (q / P) * Pad<P>::SP + (q % P);
+}
+
+// Deterministic block sum (fixed butterfly + fixed warp order).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+  }
+  return s;
+}
+
+}  // namespace mg

@@ -1,0 +1,111 @@
+// kernels.h — host-visible launch interfaces of the MGRIT kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+
+namespace mg {
+
+// Row addressing: row(j) = base + (off + j*stride) * nx.  base == nullptr disables.
+struct RowMap {
+  const double *base;
+  long long off;
+  long long stride;
+};
+
+// ---- RK sweep (fine level, fixed coordinates, halo tiles or whole periodic rows) ----
+struct SweepArgs {
+  int nx;
+  int nitems;      // items (intervals or rows) j = 0..nitems-1
+  int ntiles;      // spatial tiles per item (1 = whole periodic row)
+  int HL;          // left halo (points) of the window in tile mode
+  int nsteps1;     // phase-1 steps of Phi
+  int nsteps2;     // phase-2 steps (applied to delta), 0 = none
+  int p2_items;    // phase 2 only for items j < p2_items
+  int each_first;  // write phase-1 states i = each_first..each_last into `each` rows
+  int each_last;   //   (each_last < each_first: none); i = 0 is the input state
+  long long each_step;  // row(j,i) = each.base + (each.off + j*each.stride + i*each_step)*nx
+  RowMap in;       // input state (base null: zero)
+  RowMap cmp;      // delta = x - cmp (base null: no delta)
+  RowMap endw;     // store the phase-1 result
+  RowMap each;
+  RowMap dstore;   // store delta of item j at row (j+d_phase)/d_every if divisible
+  int d_every, d_phase;
+  RowMap r2;       // phase-2 result
+  double *partials;  // [nitems*ntiles] sum(delta^2) over each tile's own outputs
+  RKCoeffs co;
+};
+
+struct SweepCfg {
+  int nt_threads;  // NT
+  int p;           // points per thread
+};
+
+// scheme: 0 ERK1U1, 1 ERK2U2, 2 ERK3U3, 3 ERK4U4, 4 ERK5U5, 5.. SDIRK
+cudaError_t launch_rk_sweep(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s);
+bool rk_sweep_supported(int scheme, SweepCfg cfg);
+int rk_scheme_reach_left(int scheme);
+int rk_scheme_reach_right(int scheme);
+int rk_scheme_stages(int scheme);
+
+// ---- Stencil (Psi) kernels in shifted coordinates ----
+constexpr int MAX_PSI = 64;
+struct PsiOp {
+  int nu;        // taps, contiguous offsets o0 .. o0+nu-1
+  int o0;
+  double psi[MAX_PSI];
+};
+
+// Sequential (coarsest-level) solve over steps n0+1..n0+nsteps of
+//   x_n = Psi x_{n-1} + g_n,   out_n = v_n + x_n
+// in trapezoid tiles (no inter-CTA communication inside a launch).
+struct CoarseArgs {
+  int nx, ntiles, nsteps;
+  long long n0;
+  RowMap g;        // g row n  (n = n0+i)
+  RowMap v;        // addend row n (base null: 0)
+  RowMap out;      // out row n
+  const double *state_in;  // x_{n0} (nx), null: zero
+  double *state_out;       // x_{n0+nsteps} (nx), null: not stored
+  PsiOp op;
+};
+cudaError_t launch_psi_coarse(SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);
+
+// Level-l (l >= 2) relaxation sweep of the V-cycle with Psi_l and RHS g (u = 0 start):
+//   phase 1: x_i = Psi x_{i-1} + g[jm+i], i=1..m, x_0 = u_j (null: 0) -> v_{j+1}
+//   delta = x_m - u_{j+1} (null: x_m); phase 2: m homogeneous steps -> r_{j+2}.
+// Interp mode: x_0 = u_j, x_i = Psi x_{i-1} + g[jm+i] for i = 1..m-1,
+//   out[jm+i] = v2[jm+i] + x_i for i = 0..m-1.
+struct PsiSweepArgs {
+  int nx, nitems, ntiles, m;
+  int interp;
+  RowMap u;        // level-l C-rows (null: zero)
+  RowMap ucmp;     // u_{j+1} (null: zero)
+  RowMap g;        // level-l rhs rows, row(j) = base + (off + j*stride) and + i
+  RowMap v;        // v_{j+1}
+  RowMap r2;       // r_{j+2}
+  int p2_items;
+  RowMap v2;       // interp: addend rows of level l-1 (row jm+i)
+  RowMap out2;     // interp: output rows of level l-1 (row jm+i)
+  PsiOp op;
+};
+cudaError_t launch_psi_sweep(SweepCfg cfg, const PsiSweepArgs &a, cudaStream_t s);
+
+// RK-form coarse operator (IDEAL = q fine steps, REDISC = one step at CFL m*c),
+// sequential over nsteps, whole periodic row, one CTA.
+struct RKCoarseArgs {
+  int nx, nsteps, q;
+  RowMap g, v, out;
+  RKCoeffs co;
+};
+cudaError_t launch_rk_coarse(int scheme, SweepCfg cfg, const RKCoarseArgs &a, cudaStream_t s);
+
+// Deterministic reduction of partials -> out[0] (single block, fixed order).
+cudaError_t launch_reduce(const double *partials, long long n, double *out, cudaStream_t s);
+
+// Counter-based SplitMix64 uniform generator (R4).
+cudaError_t launch_fill_guess(double *dst, long long row0, long long rows, int nx,
+                              uint64_t seed, int lo_kind, const double *u0, cudaStream_t s);
+
+}  // namespace mg

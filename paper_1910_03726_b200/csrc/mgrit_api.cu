@@ -1,0 +1,931 @@
+// mgrit_api.cu — C ABI (include/mgrit.h): validation, workspace carving, kernel
+// orchestration of the MGRIT iteration.
+//
+// Production iteration:
+//   hist[0] = ||r|| over all rows of the guess (R1)
+//   sweep(u)             : v_{j+1} = Phi^m u_j, delta_{j+1} = v_{j+1} - u_{j+1} (norm),
+//                          r_{j+2} = Phi^m delta_{j+1}              (FCF)
+//   repeat: coarse correction (two-level sequential, or V-cycle)  -> u
+//           sweep(u) -> ||r^(k)|| ; stop when < tol                (R2)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mgrit.h"
+#include "kernels.h"
+
+using namespace mg;
+
+cudaError_t mg_add_rows(double *dst, const double *a, const double *b, int n, cudaStream_t s);
+
+namespace {
+
+// Upwind stencils U1..U5: weights w_d for d = dmin..dmax and den.
+struct Upwind {
+  int dmin, dmax, den;
+  int w[6];
+};
+const Upwind kUpwind[6] = {
+    {0, 0, 1, {0}},
+    {-1, 0, 1, {-1, 1}},                       // U1: u_i - u_{i-1}
+    {-2, 0, 2, {1, -4, 3}},                    // U2: 3u_i - 4u_{i-1} + u_{i-2}
+    {-2, 1, 6, {1, -6, 3, 2}},                 // U3: 2u_{i+1} + 3u_i - 6u_{i-1} + u_{i-2}
+    {-3, 1, 12, {-1, 6, -18, 10, 3}},          // U4
+    {-3, 2, 60, {-2, 15, -60, 20, 30, -3}},    // U5
+};
+
+struct Tab {
+  int s;
+  bool implicit;
+  double A[MAXS][MAXS];
+  double b[MAXS];
+};
+
+// Butcher tableaux (App. A).  Built at run time with plain IEEE
+// operations (host compiled with -ffp-contract=off), R3.
+bool make_tableau(int id, Tab &t) {
+  std::memset(&t, 0, sizeof(t));
+  switch (id) {
+    case MGRIT_TAB_ERK1:
+      t.s = 1; t.b[0] = 1.0; return true;
+    case MGRIT_TAB_ERK2:
+      t.s = 2; t.A[1][0] = 1.0; t.b[0] = 1.0 / 2.0; t.b[1] = 1.0 / 2.0; return true;
+    case MGRIT_TAB_ERK3_SSP:
+      t.s = 3; t.A[1][0] = 1.0; t.A[2][0] = 1.0 / 4.0; t.A[2][1] = 1.0 / 4.0;
+      t.b[0] = 1.0 / 6.0; t.b[1] = 1.0 / 6.0; t.b[2] = 2.0 / 3.0; return true;
+    case MGRIT_TAB_ERK3_KUTTA:
+      t.s = 3; t.A[1][0] = 1.0 / 2.0; t.A[2][0] = -1.0; t.A[2][1] = 2.0;
+      t.b[0] = 1.0 / 6.0; t.b[1] = 2.0 / 3.0; t.b[2] = 1.0 / 6.0; return true;
+    case MGRIT_TAB_ERK4:
+      t.s = 4; t.A[1][0] = 1.0 / 2.0; t.A[2][1] = 1.0 / 2.0; t.A[3][2] = 1.0;
+      t.b[0] = 1.0 / 6.0; t.b[1] = 1.0 / 3.0; t.b[2] = 1.0 / 3.0; t.b[3] = 1.0 / 6.0; return true;
+    case MGRIT_TAB_ERK5:
+      t.s = 6;
+      t.A[1][0] = 1.0 / 4.0;
+      t.A[2][0] = 1.0 / 8.0; t.A[2][1] = 1.0 / 8.0;
+      t.A[3][2] = 1.0 / 2.0;
+      t.A[4][0] = 3.0 / 16.0; t.A[4][1] = -3.0 / 8.0; t.A[4][2] = 3.0 / 8.0; t.A[4][3] = 9.0 / 16.0;
+      t.A[5][0] = -3.0 / 7.0; t.A[5][1] = 8.0 / 7.0; t.A[5][2] = 6.0 / 7.0;
+      t.A[5][3] = -12.0 / 7.0; t.A[5][4] = 8.0 / 7.0;
+      t.b[0] = 7.0 / 90.0; t.b[1] = 0.0; t.b[2] = 32.0 / 90.0; t.b[3] = 12.0 / 90.0;
+      t.b[4] = 32.0 / 90.0; t.b[5] = 7.0 / 90.0;
+      return true;
+    case MGRIT_TAB_SDIRK1:
+      t.s = 1; t.implicit = true; t.A[0][0] = 1.0; t.b[0] = 1.0; return true;
+    case MGRIT_TAB_SDIRK2: {
+      t.s = 2; t.implicit = true;
+      const double g = 1.0 - std::sqrt(2.0) / 2.0, h = std::sqrt(2.0) / 2.0;
+      t.A[0][0] = g; t.A[1][0] = h; t.A[1][1] = g; t.b[0] = h; t.b[1] = g; return true;
+    }
+    case MGRIT_TAB_SDIRK3: {
+      t.s = 3; t.implicit = true;
+      volatile double zeta = 0.43586652150845899942;
+      const double beta = (1.0 - zeta) / 2.0;
+      const double gamma = -1.5 * zeta * zeta + 4.0 * zeta - 0.25;
+      const double eps = 1.5 * zeta * zeta - 5.0 * zeta + 1.25;
+      t.A[0][0] = zeta; t.A[1][0] = beta; t.A[1][1] = zeta;
+      t.A[2][0] = gamma; t.A[2][1] = eps; t.A[2][2] = zeta;
+      t.b[0] = gamma; t.b[1] = eps; t.b[2] = zeta; return true;
+    }
+    case MGRIT_TAB_SDIRK4: {
+      t.s = 5; t.implicit = true;
+      const double A[5][5] = {{1.0 / 4.0, 0, 0, 0, 0},
+                              {1.0 / 2.0, 1.0 / 4.0, 0, 0, 0},
+                              {17.0 / 50.0, -1.0 / 25.0, 1.0 / 4.0, 0, 0},
+                              {371.0 / 1360.0, -137.0 / 2720.0, 15.0 / 544.0, 1.0 / 4.0, 0},
+                              {25.0 / 24.0, -49.0 / 48.0, 125.0 / 16.0, -85.0 / 12.0, 1.0 / 4.0}};
+      for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) t.A[i][j] = A[i][j];
+      for (int j = 0; j < 5; ++j) t.b[j] = A[4][j];
+      return true;
+    }
+  }
+  return false;
+}
+
+// z_d = (-c * w_d) / den, d = dmin..dmax (R3), stored at index d - dmin.
+void make_z(int order, double cfl, double *z, int *zlo, int *zn) {
+  const Upwind &u = kUpwind[order];
+  for (int d = u.dmin; d <= u.dmax; ++d) {
+    const volatile double wd = (double)u.w[d - u.dmin];
+    z[d - u.dmin] = (-cfl * wd) / (double)u.den;
+  }
+  *zlo = u.dmin;
+  *zn = u.dmax - u.dmin + 1;
+}
+
+int scheme_id(int tableau) {
+  switch (tableau) {
+    case MGRIT_TAB_ERK1: return 0;
+    case MGRIT_TAB_ERK2: return 1;
+    case MGRIT_TAB_ERK3_SSP:
+    case MGRIT_TAB_ERK3_KUTTA: return 2;
+    case MGRIT_TAB_ERK4: return 3;
+    case MGRIT_TAB_ERK5: return 4;
+    default: return -1;
+  }
+}
+
+int tableau_order(int tableau) {
+  switch (tableau) {
+    case MGRIT_TAB_ERK1: case MGRIT_TAB_SDIRK1: return 1;
+    case MGRIT_TAB_ERK2: case MGRIT_TAB_SDIRK2: return 2;
+    case MGRIT_TAB_ERK3_SSP: case MGRIT_TAB_ERK3_KUTTA: case MGRIT_TAB_SDIRK3: return 3;
+    case MGRIT_TAB_ERK4: case MGRIT_TAB_SDIRK4: return 4;
+    case MGRIT_TAB_ERK5: return 5;
+  }
+  return -1;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Layout of the workspace (doubles unless noted).
+struct Layout {
+  size_t u0, v0, g[MGRIT_MAX_LEVELS], vl[MGRIT_MAX_LEVELS], ul[MGRIT_MAX_LEVELS];
+  size_t partials, scal, sa, sb, total;
+  long long npart;
+};
+
+bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
+  if (nx < 2 || nt < 1 || m < 2 || levels < 2 || levels > MGRIT_MAX_LEVELS) return false;
+  long long q = 1;
+  for (int l = 0; l < levels - 1; ++l) {
+    q *= m;
+    if (q > nt || nt % q) return false;
+  }
+  size_t off = 0;
+  const size_t row = (size_t)nx * sizeof(double);
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
+  const long long nc0 = nt / m;
+  L.u0 = take((nc0 + 1) * row);
+  L.v0 = take((nc0 + 1) * row);
+  long long ntl = nt;
+  for (int l = 1; l < levels; ++l) {
+    ntl /= m;  // nt at level l
+    L.g[l] = take((ntl + 1) * row);
+    if (l < levels - 1) {
+      L.vl[l] = take((ntl / m + 1) * row);
+      L.ul[l] = take((ntl / m + 1) * row);
+    } else {
+      L.vl[l] = L.ul[l] = 0;
+    }
+  }
+  // partials: largest sweep = all nt rows x up to 64 tiles
+  L.npart = (long long)(nt + 1) * 64;
+  L.partials = take(L.npart * sizeof(double));
+  L.scal = take(64 * sizeof(double));
+  L.sa = take(row);
+  L.sb = take(row);
+  L.total = off;
+  return true;
+}
+
+}  // namespace
+
+struct mgrit_ctx {
+  int nx, nt, m, levels, order, tableau, relax, scheme;
+  bool implicit;
+  double alpha, cfl, dx, dt;
+  cudaStream_t stream;
+  long long ntl[MGRIT_MAX_LEVELS];  // nt at level l
+  int psi_kind;
+  PsiOp op[MGRIT_MAX_LEVELS];       // stencil Psi of level l >= 1
+  double redisc_cfl;
+  RKCoeffs fine, coarse_rk;
+  int coarse_q;
+  int zlo, zn;
+  Tab tab;
+  Layout lay;
+  char *ws;
+  double *u0b, *v0b, *g[MGRIT_MAX_LEVELS], *vl[MGRIT_MAX_LEVELS], *ul[MGRIT_MAX_LEVELS];
+  double *partials, *scal, *sa, *sb;
+  const double *guess;
+  bool have_iterate;   // u0b holds the iterate (after >= 1 iteration)
+  std::string err;
+  // profiling
+  bool prof;
+  std::vector<cudaEvent_t> evpool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  long long prof_launch[MGRIT_PROF_CLASSES];
+  double prof_ms[MGRIT_PROF_CLASSES];
+  long long launches;
+};
+
+namespace {
+
+int fail(mgrit_ctx *c, int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+cudaEvent_t get_event(mgrit_ctx *c) {
+  if (!c->evpool.empty()) {
+    cudaEvent_t e = c->evpool.back();
+    c->evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Run a launch, counting it and (if profiling) bracketing it with events.
+template <class F>
+int run(mgrit_ctx *c, int cls, F &&f) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof) {
+    e0 = get_event(c);
+    e1 = get_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  cudaError_t st = f();
+  if (st != cudaSuccess) return fail(c, MGRIT_ECUDA, "kernel launch failed: %s", cudaGetErrorString(st));
+  c->launches++;
+  if (c->prof) {
+    cudaEventRecord(e1, c->stream);
+    c->pending.push_back({cls, {e0, e1}});
+  }
+  return MGRIT_OK;
+}
+
+void collect(mgrit_ctx *c) {
+  for (auto &p : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(p.second.second);
+    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+    c->prof_ms[p.first] += ms;
+    c->prof_launch[p.first] += 1;
+    c->evpool.push_back(p.second.first);
+    c->evpool.push_back(p.second.second);
+  }
+  c->pending.clear();
+}
+
+// ---- launch configuration of the fine RK sweep --------------------------------
+struct FineCfg {
+  SweepCfg cfg;
+  int ntiles, HL;
+};
+
+// Choose (NT, P, tiles) for a sweep of `steps` total Phi applications per item.
+bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
+  const int nx = c->nx;
+  // periodic whole-row mode: W == nx exactly
+  const int cand[][2] = {{512, 8}, {256, 8}, {128, 8}, {64, 8}, {32, 8}, {32, 4}, {32, 2}};
+  for (auto &cc : cand) {
+    if (cc[0] * cc[1] == nx && rk_sweep_supported(c->scheme, {cc[0], cc[1]})) {
+      f.cfg = {cc[0], cc[1]};
+      f.ntiles = 1;
+      f.HL = 0;
+      return true;
+    }
+  }
+  // tile mode with halos: window W = NT*P >= T + HL + HR
+  const int S = rk_scheme_stages(c->scheme);
+  const int HL = steps * S * rk_scheme_reach_left(c->scheme);
+  const int HR = steps * S * rk_scheme_reach_right(c->scheme);
+  const int tcand[][2] = {{256, 11}, {128, 11}};
+  for (auto &cc : tcand) {
+    const int W = cc[0] * cc[1];
+    if (W > nx) continue;
+    const int Tmax = W - HL - HR;
+    if (Tmax < 64) continue;
+    int ntiles = (nx + Tmax - 1) / Tmax;
+    if ((nx + ntiles - 1) / ntiles > Tmax) ++ntiles;
+    f.cfg = {cc[0], cc[1]};
+    f.ntiles = ntiles;
+    f.HL = HL;
+    return true;
+  }
+  return false;
+}
+
+// ---- launch configuration of the stencil (Psi) kernels -------------------------
+struct PsiCfg {
+  SweepCfg cfg;
+  int ntiles;
+};
+bool choose_psi(int nx, int halo, bool allow_periodic, PsiCfg &f) {
+  const int cand[][2] = {{512, 8}, {256, 8}, {128, 8}, {64, 8}, {32, 8}, {32, 4}, {32, 2}};
+  if (allow_periodic) {
+    for (auto &cc : cand)
+      if (cc[0] * cc[1] == nx) {
+        f.cfg = {cc[0], cc[1]};
+        f.ntiles = 1;
+        return true;
+      }
+  }
+  // tiles: smallest window that leaves >= max(halo, 128) outputs, preferring many tiles
+  const int tc[][2] = {{256, 8}, {512, 8}};
+  for (auto &cc : tc) {
+    const int W = cc[0] * cc[1];
+    const int Tmax = W - halo;
+    if (Tmax < std::min(128, nx) || W > nx) continue;
+    int ntiles = (nx + Tmax - 1) / Tmax;
+    if ((nx + ntiles - 1) / ntiles > Tmax) ++ntiles;
+    f.cfg = {cc[0], cc[1]};
+    f.ntiles = ntiles;
+    return true;
+  }
+  // fall back to periodic whole row if it exists
+  for (auto &cc : cand)
+    if (cc[0] * cc[1] == nx) {
+      f.cfg = {cc[0], cc[1]};
+      f.ntiles = 1;
+      return true;
+    }
+  return false;
+}
+
+RowMap rm(const double *b, long long off, long long stride) { return RowMap{b, off, stride}; }
+const RowMap kNone = {nullptr, 0, 0};
+
+SweepArgs base_sweep(const mgrit_ctx *c) {
+  SweepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nx = c->nx;
+  a.each_first = 1;
+  a.each_last = 0;  // none
+  a.d_every = 1;
+  a.co = c->fine;
+  a.in = a.cmp = a.endw = a.each = a.dstore = a.r2 = kNone;
+  return a;
+}
+
+int sweep(mgrit_ctx *c, int cls, SweepArgs a, int total_steps) {
+  FineCfg f;
+  if (!choose_fine(c, total_steps, f))
+    return fail(c, MGRIT_EUNSUPPORTED, "no fine-sweep configuration for nx=%d", c->nx);
+  a.ntiles = f.ntiles;
+  a.HL = f.HL;
+  if (a.partials && (long long)a.nitems * a.ntiles > c->lay.npart)
+    return fail(c, MGRIT_ENOMEM, "partials buffer too small");
+  return run(c, cls, [&] { return launch_rk_sweep(c->scheme, f.cfg, a, c->stream); });
+}
+
+int reduce_norm(mgrit_ctx *c, long long n, double *norm2_host) {
+  int st = run(c, 5, [&] { return launch_reduce(c->partials, n, c->scal, c->stream); });
+  if (st) return st;
+  if (norm2_host) {
+    cudaError_t e = cudaMemcpyAsync(norm2_host, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(c, MGRIT_ECUDA, "norm readback: %s", cudaGetErrorString(e));
+  }
+  return MGRIT_OK;
+}
+
+// Sequential coarse solve on level l (= levels-1, the coarsest) for steps 1..ntl:
+//   x_n = Psi x_{n-1} + g_n, out_n = v_n + x_n.
+int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
+  const long long N = c->ntl[l];
+  if (c->psi_kind != MGRIT_PSI_STENCIL) {
+    RKCoarseArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.nx = c->nx;
+    a.nsteps = (int)N;
+    a.q = c->coarse_q;
+    a.g = rm(c->g[l], 0, 1);
+    a.v = v;
+    a.out = out;
+    a.co = c->coarse_rk;
+    SweepCfg cfg;
+    if (c->nx == 64) cfg = {32, 2};
+    else if (c->nx == 128) cfg = {32, 4};
+    else if (c->nx == 256) cfg = {32, 8};
+    else if (c->nx == 1024) cfg = {128, 8};
+    else return fail(c, MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,256,1024}");
+    return run(c, 2, [&] { return launch_rk_coarse(c->scheme, cfg, a, c->stream); });
+  }
+  const PsiOp &op = c->op[l];
+  // Short chains (the V-cycle's coarsest level): trapezoid tiles, one launch, no
+  // inter-CTA communication.  Long chains (two-level): one periodic CTA.
+  PsiCfg pc;
+  const long long cone = N * (long long)(op.nu - 1);
+  bool ok = false;
+  if (cone <= 2048 && c->nx >= 2048) ok = choose_psi(c->nx, (int)cone, false, pc);
+  if (!ok) {
+    ok = choose_psi(c->nx, 0, true, pc) && pc.ntiles == 1 &&
+         pc.cfg.nt_threads * pc.cfg.p == c->nx;
+  }
+  if (!ok) return fail(c, MGRIT_EUNSUPPORTED, "no coarse-solve configuration for nx=%d", c->nx);
+  CoarseArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nx = c->nx;
+  a.ntiles = pc.ntiles;
+  a.nsteps = (int)N;
+  a.n0 = 0;
+  a.g = rm(c->g[l], 0, 1);
+  a.v = v;
+  a.out = out;
+  a.state_in = nullptr;
+  a.state_out = nullptr;
+  a.op = op;
+  return run(c, 2, [&] { return launch_psi_coarse(pc.cfg, a, c->stream); });
+}
+
+// Level-l (1 <= l <= levels-2) FCF sweep with RHS g_l, zero initial guess:
+// v_l rows 1..nc, g_{l+1} rows 2..nc.
+int level_sweep(mgrit_ctx *c, int l) {
+  const PsiOp &op = c->op[l];
+  const int m = c->m;
+  const long long nc = c->ntl[l] / m;
+  PsiCfg pc;
+  if (!choose_psi(c->nx, 2 * m * (op.nu - 1), true, pc))
+    return fail(c, MGRIT_EUNSUPPORTED, "no level-sweep configuration");
+  PsiSweepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nx = c->nx;
+  a.nitems = (int)nc;
+  a.ntiles = pc.ntiles;
+  a.m = m;
+  a.interp = 0;
+  a.u = kNone;
+  a.ucmp = kNone;
+  a.g = rm(c->g[l], 0, m);
+  a.v = rm(c->vl[l], 1, 1);
+  a.r2 = rm(c->g[l + 1], 2, 1);
+  a.p2_items = (int)nc - 1;
+  a.v2 = a.out2 = kNone;
+  a.op = op;
+  return run(c, 1, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
+}
+
+// Level-l interpolation: from corrected C-rows u_l, F-relax with g_l and write
+// level l-1's corrected C-rows: out_{l-1}[n] = v_{l-1}[n] + U_l[n], n = 0..nt_l-1.
+int level_interp(mgrit_ctx *c, int l, RowMap v_prev, RowMap out_prev) {
+  const PsiOp &op = c->op[l];
+  const int m = c->m;
+  const long long nc = c->ntl[l] / m;
+  PsiCfg pc;
+  if (!choose_psi(c->nx, (m - 1) * (op.nu - 1), true, pc))
+    return fail(c, MGRIT_EUNSUPPORTED, "no interpolation configuration");
+  PsiSweepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nx = c->nx;
+  a.nitems = (int)nc;
+  a.ntiles = pc.ntiles;
+  a.m = m;
+  a.interp = 1;
+  a.u = rm(c->ul[l], 0, 1);
+  a.ucmp = kNone;
+  a.g = rm(c->g[l], 0, m);
+  a.v = a.r2 = kNone;
+  a.v2 = RowMap{v_prev.base, v_prev.off, v_prev.stride * m};
+  a.out2 = RowMap{out_prev.base, out_prev.off, out_prev.stride * m};
+  a.op = op;
+  int st = run(c, 3, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
+  if (st) return st;
+  // the last point n = nt_l (level l's last C-row): out[nt_l] = v[nt_l] + u_l[nc]
+  const long long ntl = c->ntl[l];
+  double *dst = const_cast<double *>(out_prev.base) +
+                (out_prev.off + ntl * out_prev.stride) * (long long)c->nx;
+  const double *vsrc = v_prev.base + (v_prev.off + ntl * v_prev.stride) * (long long)c->nx;
+  const double *usrc = c->ul[l] + nc * (long long)c->nx;
+  return run(c, 3, [&] { return mg_add_rows(dst, vsrc, usrc, c->nx, c->stream); });
+}
+
+// C-point correction + V-cycle below level 0 after the fine sweep (g_1 = r).
+int coarse_correction(mgrit_ctx *c, RowMap v0map, RowMap out0map) {
+  const int L = c->levels;
+  if (L == 2) return coarse_solve_level(c, 1, rm(v0map.base, v0map.off, v0map.stride),
+                                        rm(out0map.base, out0map.off, out0map.stride));
+  // down: levels 1..L-2 sweeps
+  for (int l = 1; l <= L - 2; ++l) {
+    int st = level_sweep(c, l);
+    if (st) return st;
+  }
+  // coarsest: writes u_{L-2}[n] = v_{L-2}[n] + x_n, n = 1..nt_{L-1}
+  {
+    int st = coarse_solve_level(c, L - 1, rm(c->vl[L - 2], 0, 1), rm(c->ul[L - 2], 0, 1));
+    if (st) return st;
+  }
+  // up: level l interpolation writes level l-1's corrected C-rows
+  for (int l = L - 2; l >= 1; --l) {
+    RowMap vprev = (l == 1) ? v0map : rm(c->vl[l - 1], 0, 1);
+    RowMap oprev = (l == 1) ? out0map : rm(c->ul[l - 1], 0, 1);
+    int st = level_interp(c, l, vprev, oprev);
+    if (st) return st;
+  }
+  return MGRIT_OK;
+}
+
+}  // namespace
+
+__global__ void mg_add_rows_kernel(double *dst, const double *a, const double *b, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = a[i] + b[i];
+}
+cudaError_t mg_add_rows(double *dst, const double *a, const double *b, int n, cudaStream_t s) {
+  mg_add_rows_kernel<<<(n + 255) / 256 < 148 ? (n + 255) / 256 : 148, 256, 0, s>>>(dst, a, b, n);
+  return cudaGetLastError();
+}
+
+// =============================================================================
+extern "C" {
+
+size_t mgrit_workspace_bytes(int nx, int nt, int m, int levels) {
+  Layout L;
+  if (!make_layout(nx, nt, m, levels, L)) return 0;
+  return L.total;
+}
+
+const char *mgrit_last_error(const mgrit_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl, int order,
+                int tableau, int levels, const mgrit_psi *psi, int relax, void *workspace_dev,
+                size_t workspace_bytes, void *stream) {
+  if (!out) return MGRIT_EINVAL;
+  *out = nullptr;
+  mgrit_ctx *c = new mgrit_ctx();
+  c->err.clear();
+  c->nx = nx; c->nt = nt; c->m = m; c->levels = levels; c->order = order;
+  c->tableau = tableau; c->relax = relax; c->alpha = alpha; c->cfl = cfl;
+  c->stream = (cudaStream_t)stream;
+  c->prof = false;
+  c->launches = 0;
+  std::memset(c->prof_launch, 0, sizeof(c->prof_launch));
+  std::memset(c->prof_ms, 0, sizeof(c->prof_ms));
+  auto bad = [&](int code, const char *msg) {
+    fprintf(stderr, "mgrit_setup: %s\n", msg);
+    delete c;
+    return code;
+  };
+  if (!(alpha > 0)) return bad(MGRIT_EINVAL, "alpha must be > 0");
+  if (!(cfl > 0)) return bad(MGRIT_EINVAL, "cfl must be > 0");
+  if (order < 1 || order > 5) return bad(MGRIT_EINVAL, "order must be 1..5");
+  if (tableau_order(tableau) != order) return bad(MGRIT_EINVAL, "tableau order != stencil order");
+  if (relax != MGRIT_RELAX_F && relax != MGRIT_RELAX_FCF) return bad(MGRIT_EINVAL, "relax must be F or FCF");
+  if (!make_tableau(tableau, c->tab)) return bad(MGRIT_EINVAL, "unknown tableau");
+  c->implicit = c->tab.implicit;
+  c->scheme = scheme_id(tableau);
+  if (c->implicit || c->scheme < 0) return bad(MGRIT_EUNSUPPORTED, "SDIRK fine propagators are not built yet");
+  if (!make_layout(nx, nt, m, levels, c->lay)) return bad(MGRIT_EINVAL, "invalid nx/nt/m/levels (nt % m^(levels-1) != 0?)");
+  if (workspace_bytes < c->lay.total || !workspace_dev) return bad(MGRIT_ENOMEM, "workspace too small");
+  const Upwind &up = kUpwind[order];
+  if (nx < 4 * (up.dmax - up.dmin + 1)) return bad(MGRIT_EINVAL, "nx too small for the stencil");
+  if (!psi) return bad(MGRIT_EINVAL, "psi is NULL");
+  c->dx = 2.0 / nx;
+  c->dt = cfl * c->dx / alpha;
+  c->ntl[0] = nt;
+  for (int l = 1; l < levels; ++l) c->ntl[l] = c->ntl[l - 1] / m;
+  // fine coefficients
+  std::memset(&c->fine, 0, sizeof(c->fine));
+  make_z(order, cfl, c->fine.z, &c->zlo, &c->zn);
+  for (int i = 0; i < MAXS; ++i) {
+    c->fine.b[i] = c->tab.b[i];
+    c->fine.mdiag[i] = c->tab.A[i][i];
+    for (int j = 0; j < MAXS; ++j) c->fine.A[i][j] = c->tab.A[i][j];
+  }
+  // coarse operators
+  c->psi_kind = psi[0].kind;
+  for (int l = 1; l < levels; ++l) {
+    const mgrit_psi &p = psi[l - 1];
+    if (p.kind != c->psi_kind) return bad(MGRIT_EINVAL, "mixed Psi kinds across levels");
+    if (p.kind == MGRIT_PSI_STENCIL) {
+      if (p.nnz < 1 || p.nnz > MGRIT_MAX_PSI_TAPS || !p.offsets || !p.coeffs)
+        return bad(MGRIT_EINVAL, "bad stencil Psi");
+      const int o0 = p.offsets[0], o1 = p.offsets[p.nnz - 1];
+      const int nu = o1 - o0 + 1;
+      if (nu > MAX_PSI || nu > nx / 2) return bad(MGRIT_EINVAL, "Psi stencil too wide");
+      PsiOp &op = c->op[l];
+      std::memset(&op, 0, sizeof(op));
+      op.nu = nu;
+      op.o0 = o0;
+      for (int k = 0; k < p.nnz; ++k) {
+        if (k > 0 && p.offsets[k] <= p.offsets[k - 1]) return bad(MGRIT_EINVAL, "Psi offsets must increase");
+        op.psi[p.offsets[k] - o0] = p.coeffs[k];
+      }
+    } else {
+      if (levels != 2) return bad(MGRIT_EINVAL, "IDEAL/REDISC Psi only for two levels");
+      std::memset(&c->coarse_rk, 0, sizeof(c->coarse_rk));
+      c->coarse_rk = c->fine;
+      if (p.kind == MGRIT_PSI_IDEAL) {
+        c->coarse_q = m;
+      } else if (p.kind == MGRIT_PSI_REDISC) {
+        int zlo, zn;
+        make_z(order, p.redisc_cfl, c->coarse_rk.z, &zlo, &zn);
+        c->coarse_q = 1;
+        c->redisc_cfl = p.redisc_cfl;
+      } else {
+        return bad(MGRIT_EINVAL, "unknown Psi kind");
+      }
+    }
+  }
+  // carve the workspace
+  c->ws = (char *)workspace_dev;
+  c->u0b = (double *)(c->ws + c->lay.u0);
+  c->v0b = (double *)(c->ws + c->lay.v0);
+  for (int l = 1; l < levels; ++l) {
+    c->g[l] = (double *)(c->ws + c->lay.g[l]);
+    c->vl[l] = (l < levels - 1) ? (double *)(c->ws + c->lay.vl[l]) : nullptr;
+    c->ul[l] = (l < levels - 1) ? (double *)(c->ws + c->lay.ul[l]) : nullptr;
+  }
+  c->partials = (double *)(c->ws + c->lay.partials);
+  c->scal = (double *)(c->ws + c->lay.scal);
+  c->sa = (double *)(c->ws + c->lay.sa);
+  c->sb = (double *)(c->ws + c->lay.sb);
+  c->guess = nullptr;
+  c->have_iterate = false;
+  // constant rows: g_l rows 0 and 1 (r_1 = 0), coarse v_l/u_l row 0
+  const size_t row = (size_t)nx * sizeof(double);
+  for (int l = 1; l < levels; ++l) {
+    cudaMemsetAsync(c->g[l], 0, 2 * row, c->stream);
+    if (l < levels - 1) {
+      cudaMemsetAsync(c->vl[l], 0, row, c->stream);
+      cudaMemsetAsync(c->ul[l], 0, row, c->stream);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return bad(MGRIT_ECUDA, cudaGetErrorString(e));
+  *out = c;
+  return MGRIT_OK;
+}
+
+void mgrit_destroy(mgrit_ctx *c) {
+  if (!c) return;
+  for (auto &p : c->pending) {
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  delete c;
+}
+
+int mgrit_get_coefficients(const mgrit_ctx *c, int *s, int *z_lo, int *z_n, double *z, double *A,
+                           double *b) {
+  if (!c) return MGRIT_EINVAL;
+  if (s) *s = c->tab.s;
+  if (z_lo) *z_lo = c->zlo;
+  if (z_n) *z_n = c->zn;
+  if (z) for (int k = 0; k < c->zn; ++k) z[k] = c->fine.z[k];
+  if (A) for (int i = 0; i < MAXS; ++i) for (int j = 0; j < MAXS; ++j) A[i * MAXS + j] = c->tab.A[i][j];
+  if (b) for (int i = 0; i < MAXS; ++i) b[i] = c->tab.b[i];
+  return MGRIT_OK;
+}
+
+int mgrit_scheme_coefficients(int order, int tableau, double cfl, int *s, int *z_lo, int *z_n,
+                              double *z, double *A, double *b) {
+  Tab t;
+  if (order < 1 || order > 5 || tableau_order(tableau) != order || !make_tableau(tableau, t))
+    return MGRIT_EINVAL;
+  double zz[MAXZ] = {0};
+  int lo, n;
+  make_z(order, cfl, zz, &lo, &n);
+  if (s) *s = t.s;
+  if (z_lo) *z_lo = lo;
+  if (z_n) *z_n = n;
+  if (z) for (int k = 0; k < n; ++k) z[k] = zz[k];
+  if (A) for (int i = 0; i < MAXS; ++i) for (int j = 0; j < MAXS; ++j) A[i * MAXS + j] = t.A[i][j];
+  if (b) for (int i = 0; i < MAXS; ++i) b[i] = t.b[i];
+  return MGRIT_OK;
+}
+
+int mgrit_set_guess(mgrit_ctx *c, const double *guess_dev) {
+  if (!c || !guess_dev) return MGRIT_EINVAL;
+  c->guess = guess_dev;
+  c->have_iterate = false;
+  return MGRIT_OK;
+}
+
+int mgrit_relax(mgrit_ctx *c, int level, int kind, double *U) {
+  if (!c || !U) return MGRIT_EINVAL;
+  if (level != 0) return fail(c, MGRIT_EUNSUPPORTED, "FULL primitives are level 0 only");
+  const int m = c->m;
+  const long long nc = c->nt / m;
+  auto frelax = [&]() {
+    SweepArgs a = base_sweep(c);
+    a.nitems = (int)nc;
+    a.nsteps1 = m - 1;
+    a.in = rm(U, 0, m);
+    a.each = rm(U, 0, m);
+    a.each_step = 1;
+    a.each_first = 1;
+    a.each_last = m - 1;
+    return sweep(c, 0, a, m - 1);
+  };
+  auto crelax = [&]() {
+    SweepArgs a = base_sweep(c);
+    a.nitems = (int)nc;
+    a.nsteps1 = 1;
+    a.in = rm(U, m - 1, m);
+    a.endw = rm(U, m, m);
+    return sweep(c, 0, a, 1);
+  };
+  int st = MGRIT_OK;
+  if (kind == MGRIT_RELAX_F) st = frelax();
+  else if (kind == MGRIT_RELAX_C) st = crelax();
+  else if (kind == MGRIT_RELAX_FCF) {
+    st = frelax();
+    if (!st) st = crelax();
+    if (!st) st = frelax();
+  } else st = fail(c, MGRIT_EINVAL, "relax kind");
+  return st;
+}
+
+int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, double *r_dev) {
+  if (!c || !U) return MGRIT_EINVAL;
+  if (level != 0) return fail(c, MGRIT_EUNSUPPORTED, "FULL primitives are level 0 only");
+  SweepArgs a = base_sweep(c);
+  a.nitems = c->nt;
+  a.nsteps1 = 1;
+  a.in = rm(U, 0, 1);
+  a.cmp = rm(U, 1, 1);
+  a.partials = c->partials;
+  if (r_dev) {
+    cudaMemsetAsync(r_dev, 0, (size_t)c->nx * sizeof(double), c->stream);
+    a.dstore = rm(r_dev, 0, 1);
+    a.d_every = c->m;
+    a.d_phase = 1;
+  }
+  int st = sweep(c, 4, a, 1);
+  if (st) return st;
+  FineCfg f;
+  choose_fine(c, 1, f);
+  double n2 = 0;
+  st = reduce_norm(c, (long long)c->nt * f.ntiles, norm_host ? &n2 : nullptr);
+  if (st) return st;
+  if (norm_host) *norm_host = std::sqrt(c->dx * c->dt * n2);
+  return MGRIT_OK;
+}
+
+int mgrit_coarse_solve(mgrit_ctx *c, int level, double *U) {
+  if (!c || !U) return MGRIT_EINVAL;
+  if (level != 0 || c->levels != 2)
+    return fail(c, MGRIT_EUNSUPPORTED, "FULL coarse_solve is two-level, level 0 only");
+  const int m = c->m;
+  const long long nc = c->nt / m;
+  // r_j = Phi U[jm-1] - U[jm], j = 1..nc  -> g_1 rows 1..nc
+  SweepArgs a = base_sweep(c);
+  a.nitems = (int)nc;
+  a.nsteps1 = 1;
+  a.in = rm(U, m - 1, m);
+  a.cmp = rm(U, m, m);
+  a.dstore = rm(c->g[1], 1, 1);
+  int st = sweep(c, 4, a, 1);
+  if (st) return st;
+  // e_j = Psi e_{j-1} + r_j ; U[jm] += e_j
+  st = coarse_solve_level(c, 1, rm(U, 0, m), rm(U, 0, m));
+  if (st) return st;
+  // ideal interpolation: F-relaxation
+  return mgrit_relax(c, 0, MGRIT_RELAX_F, U);
+}
+
+int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *iters,
+                double *hist, int *converged, double *crows_hist) {
+  if (!c) return MGRIT_EINVAL;
+  if (!c->guess) return fail(c, MGRIT_EINVAL, "mgrit_set_guess first");
+  if (max_iter < 0) return fail(c, MGRIT_EINVAL, "max_iter < 0");
+  const int m = c->m, nx = c->nx;
+  const long long nc = c->nt / m;
+  const size_t row = (size_t)nx * sizeof(double);
+  const bool fcf = c->relax == MGRIT_RELAX_FCF;
+  int st;
+  // row 0 of the C-row buffers = u0
+  cudaMemcpyAsync(c->u0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemcpyAsync(c->v0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream);
+  // hist[0]: all-row residual of the guess
+  double r0;
+  st = mgrit_residual(c, 0, c->guess, &r0, nullptr);
+  if (st) return st;
+  if (hist) hist[0] = r0;
+  if (!fcf)  // Parareal: the coarse correction updates the C-rows in place (v = u)
+    cudaMemcpy2DAsync(c->u0b, row, c->guess, row * m, row, nc + 1, cudaMemcpyDeviceToDevice,
+                      c->stream);
+  int k = 0;
+  bool conv = r0 < tol;
+  bool nonfinite = !std::isfinite(r0);
+  c->have_iterate = false;
+  FineCfg f;
+  if (!choose_fine(c, fcf ? 2 * m : m, f)) return fail(c, MGRIT_EUNSUPPORTED, "no sweep cfg");
+  auto do_sweep = [&](bool first, bool want_norm) -> int {
+    SweepArgs a = base_sweep(c);
+    a.nitems = (int)nc;
+    a.nsteps1 = m;
+    if (first && fcf) {
+      a.in = rm(c->guess, 0, m);
+      a.cmp = rm(c->guess, m, m);
+    } else {
+      a.in = rm(c->u0b, 0, 1);
+      a.cmp = rm(c->u0b, 1, 1);
+    }
+    a.partials = want_norm ? c->partials : nullptr;
+    if (fcf) {
+      a.endw = rm(c->v0b, 1, 1);
+      a.nsteps2 = m;
+      a.p2_items = (int)nc - 1;
+      a.r2 = rm(c->g[1], 2, 1);
+    } else {
+      a.dstore = rm(c->g[1], 1, 1);
+      a.d_every = 1;
+      a.d_phase = 0;
+    }
+    if (!want_norm && !fcf) a.partials = nullptr;
+    return sweep(c, 0, a, fcf ? 2 * m : m);
+  };
+  if (!conv && !nonfinite && max_iter > 0) {
+    st = do_sweep(true, false);
+    if (st) return st;
+    while (true) {
+      // coarse-grid correction -> u0b
+      RowMap vmap = fcf ? rm(c->v0b, 0, 1) : rm(c->u0b, 0, 1);
+      st = coarse_correction(c, vmap, rm(c->u0b, 0, 1));
+      if (st) return st;
+      c->have_iterate = true;
+      ++k;
+      if (crows_hist)
+        cudaMemcpyAsync(crows_hist + (size_t)(k - 1) * (nc + 1) * nx, c->u0b, (nc + 1) * row,
+                        cudaMemcpyDeviceToDevice, c->stream);
+      // residual of iterate k (computed by the next sweep)
+      st = do_sweep(false, true);
+      if (st) return st;
+      double n2;
+      st = reduce_norm(c, nc * f.ntiles, &n2);
+      if (st) return st;
+      const double rk = std::sqrt(c->dx * c->dt * n2);
+      if (hist) hist[k] = rk;
+      if (!std::isfinite(rk)) { nonfinite = true; break; }
+      if (rk < tol) { conv = true; break; }
+      if (k >= max_iter) break;
+    }
+  }
+  if (iters) *iters = k;
+  if (converged) *converged = conv ? 1 : 0;
+  if (out_dev) {
+    if (!c->have_iterate) {
+      cudaMemcpyAsync(out_dev, c->guess, (size_t)(c->nt + 1) * row, cudaMemcpyDeviceToDevice, c->stream);
+    } else {
+      SweepArgs a = base_sweep(c);
+      a.nitems = (int)nc;
+      a.nsteps1 = m - 1;
+      a.in = rm(c->u0b, 0, 1);
+      a.each = rm(out_dev, 0, m);
+      a.each_step = 1;
+      a.each_first = 0;
+      a.each_last = m - 1;
+      st = sweep(c, 3, a, m - 1);
+      if (st) return st;
+      cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->u0b + (size_t)nc * nx, row,
+                      cudaMemcpyDeviceToDevice, c->stream);
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return fail(c, MGRIT_ECUDA, "solve: %s", cudaGetErrorString(e));
+  if (c->prof) collect(c);
+  if (nonfinite) return fail(c, MGRIT_ENONFINITE, "residual became non-finite at iteration %d", k);
+  return MGRIT_OK;
+}
+
+int mgrit_get_crows(mgrit_ctx *c, double *out_dev) {
+  if (!c || !out_dev) return MGRIT_EINVAL;
+  const long long nc = c->nt / c->m;
+  const size_t row = (size_t)c->nx * sizeof(double);
+  if (c->have_iterate)
+    cudaMemcpyAsync(out_dev, c->u0b, (nc + 1) * row, cudaMemcpyDeviceToDevice, c->stream);
+  else
+    cudaMemcpy2DAsync(out_dev, row, c->guess, row * c->m, row, nc + 1, cudaMemcpyDeviceToDevice, c->stream);
+  return MGRIT_OK;
+}
+
+int mgrit_fill_guess(double *dst, long long row0, long long rows, int nx, uint64_t seed, int lo_kind,
+                     const double *u0, void *stream) {
+  if (!dst || nx < 1 || rows < 0 || (lo_kind != 0 && lo_kind != 1)) return MGRIT_EINVAL;
+  cudaError_t e = launch_fill_guess(dst, row0, rows, nx, seed, lo_kind, u0, (cudaStream_t)stream);
+  return e == cudaSuccess ? MGRIT_OK : MGRIT_ECUDA;
+}
+
+int mgrit_profile_enable(mgrit_ctx *c, int on) {
+  if (!c) return MGRIT_EINVAL;
+  cudaStreamSynchronize(c->stream);
+  collect(c);
+  c->prof = on != 0;
+  std::memset(c->prof_launch, 0, sizeof(c->prof_launch));
+  std::memset(c->prof_ms, 0, sizeof(c->prof_ms));
+  c->launches = 0;
+  return MGRIT_OK;
+}
+
+int mgrit_profile_read(mgrit_ctx *c, long long *launches, double *ms) {
+  if (!c) return MGRIT_EINVAL;
+  cudaStreamSynchronize(c->stream);
+  collect(c);
+  for (int i = 0; i < MGRIT_PROF_CLASSES; ++i) {
+    if (launches) launches[i] = c->prof_launch[i];
+    if (ms) ms[i] = c->prof_ms[i];
+  }
+  return MGRIT_OK;
+}
+
+long long mgrit_launch_count(const mgrit_ctx *c) { return c ? c->launches : -1; }
+
+}  // extern "C"

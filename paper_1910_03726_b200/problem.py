@@ -1,0 +1,39 @@
+"""Bind a BASELINE.json workload (workloads/) to the library: Psi inputs, solver, guess."""
+from __future__ import annotations
+
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from . import binding, psi as psimod
+
+
+def psi_inputs(w) -> List[Dict]:
+    """Coarse operators of a workload as library inputs (host LSQ fit)."""
+    if w.psi_kind == "ideal":
+        return [{"kind": "ideal"}]
+    if w.psi_kind == "redisc":
+        return [{"kind": "redisc", "cfl": w.redisc_cfl}]
+    return psimod.hierarchy(w.order, w.tableau, w.cfl, w.nx, w.m, w.levels,
+                            w.psi_widths, w.psi_eta)
+
+
+def make_solver(w, psi: Optional[List[Dict]] = None, stream=None) -> binding.MGRIT:
+    return binding.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels,
+                         psi if psi is not None else psi_inputs(w), w.relax, stream=stream)
+
+
+def device_guess(w, device="cuda"):
+    """The workload's initial iterate generated on the device (R4)."""
+    import torch
+    u0 = torch.from_numpy(w.u0()).to(device)
+    g = torch.empty((w.nt + 1, w.nx), dtype=torch.float64, device=device)
+    binding.fill_guess(g, w.guess_seed, w.guess_lo, u0=u0)
+    return g
+
+
+def dof_updates(w, iterations: int) -> int:
+    """Fine space-time DOF updates of a solve: 2*nt*nx per FCF iteration,
+    nt*nx per F iteration."""
+    per = 2 if w.relax == "FCF" else 1
+    return per * w.nt * w.nx * iterations

@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element,
+on the same seeded inputs and the same Psi coefficients (R18 tolerances).
+
+Every solve compares: identical iteration counts (R16), residual histories, the
+C-rows after every iteration and the final FULL solution.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import discretization as D
+from oracle import mgrit as M
+from oracle import psi as OP
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1910_03726_b200 import binding
+    binding.lib()
+    return binding
+
+
+def _oracle_psi(w, phi):
+    """Psi inputs computed by the ORACLE's fit; both sides consume the same data."""
+    if w.psi_kind == "ideal":
+        return [{"kind": "ideal"}], [D.PowerPhi(phi, w.m)]
+    if w.psi_kind == "redisc":
+        return ([{"kind": "redisc", "cfl": w.redisc_cfl}],
+                [D.make_phi(w.order, w.tableau, w.redisc_cfl, w.nx)])
+    fits = OP.fit_hierarchy(phi, w.nx, w.m, w.cfl, w.psi_widths[: w.levels - 1], w.psi_eta)
+    lib = [{"kind": "stencil", "offsets": f.offsets, "coeffs": list(f.coeffs)} for f in fits]
+    return lib, [D.StencilPhi(f.stencil, w.nx) for f in fits]
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def _hist_ok(hg, ho, w, umax):
+    T = w.nt * w.dt
+    floor = 1e-15 * math.sqrt(2 * T) * umax
+    for k, (a, b) in enumerate(zip(hg, ho)):
+        assert abs(a - b) <= REL * abs(b) + floor, (k, a, b)
+
+
+def _tie(h, tol):
+    return abs(h - tol) / tol < 1e-6
+
+
+# ------------------------------------------------------------------ inputs
+def test_fill_guess_bitexact():
+    B = _cuda()
+    nx, nt = 384, 37
+    u0 = W.u0_fourier(nx, 3)
+    for lo in (-1.0, 0.0):
+        ref = W.initial_iterate(11, nx, nt, u0, lo)
+        g = torch.empty((nt + 1, nx), dtype=torch.float64, device="cuda")
+        B.fill_guess(g, 11, lo, u0=torch.from_numpy(u0).cuda())
+        assert np.array_equal(g.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ primitives
+PRIM = [  # (order, tableau, cfl, nx, nt, m)
+    (1, "erk1", 0.85, 64, 64, 2),
+    (2, "erk2", 0.425, 128, 48, 4),
+    (3, "erk3_kutta", 0.85, 1024, 64, 4),
+    (3, "erk3_ssp", 0.85, 16384, 32, 4),     # cfg5 width: halo tiles (NT=256, P=11)
+    (3, "erk3_ssp", 0.85, 6007, 24, 4),      # ragged tiles, odd nx
+    (4, "erk4", 0.85, 256, 32, 4),
+    (5, "erk5", 0.85, 4096, 32, 8),          # cfg3 width: whole periodic rows
+    (5, "erk5", 0.85, 12000, 16, 8),         # ERK5 tile mode
+]
+
+
+@pytest.mark.parametrize("order,tab,cfl,nx,nt,m", PRIM)
+def test_relax_primitives(order, tab, cfl, nx, nt, m):
+    """F-, C- and FCF-relaxation on the FULL state vs the oracle."""
+    B = _cuda()
+    phi = D.make_phi(order, tab, cfl, nx)
+    U0 = W.initial_iterate(5, nx, nt, W.u0_fourier(nx, 1))
+    s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2,
+                [{"kind": "stencil", "offsets": [-1, 0], "coeffs": [0.5, 0.5]}], "FCF")
+    for kind in ("F", "C", "FCF"):
+        Uo = U0.copy()
+        if kind in ("F", "FCF"):
+            M.f_relax(Uo, phi, m)
+        if kind in ("C", "FCF"):
+            M.c_relax(Uo, phi, m)
+        if kind == "FCF":
+            M.f_relax(Uo, phi, m)
+        Ug = torch.from_numpy(U0).cuda()
+        s.relax_full(Ug, kind)
+        Ug = Ug.cpu().numpy()
+        assert np.array_equal(Ug[0], U0[0])
+        assert _rel(Ug, Uo) <= REL, (kind, _rel(Ug, Uo))
+
+
+@pytest.mark.parametrize("order,tab,cfl,nx,nt,m", PRIM[:6])
+def test_residual_primitive(order, tab, cfl, nx, nt, m):
+    """All-row residual norm (R1) and C-point residuals."""
+    B = _cuda()
+    phi = D.make_phi(order, tab, cfl, nx)
+    U = W.initial_iterate(6, nx, nt, W.u0_fourier(nx, 1))
+    dx, dt = 2.0 / nx, cfl * 2.0 / nx
+    s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2,
+                [{"kind": "stencil", "offsets": [0], "coeffs": [0.5]}], "FCF")
+    ng, rg = s.residual_full(torch.from_numpy(U).cuda(), want_r=True)
+    no = M.residual_norm(U, phi, dx, dt)
+    assert abs(ng - no) <= 1e-13 * no
+    ro = M.residual_rows(U, phi, np.arange(m, nt + 1, m))
+    rg = rg.cpu().numpy()
+    assert np.all(rg[0] == 0.0)
+    assert _rel(rg[1:], ro) <= REL
+
+
+@pytest.mark.parametrize("order,tab,cfl,nx,nt,m,nu", [
+    (3, "erk3_kutta", 0.85, 256, 256, 4, 9),
+    (5, "erk5", 0.85, 512, 512, 8, 15),
+    (1, "erk1", 0.85, 64, 256, 2, 2),
+])
+def test_coarse_correction_primitive(order, tab, cfl, nx, nt, m, nu):
+    """C-point residual -> sequential e_j = Psi e_{j-1} + r_j -> U[jm] += e_j ->
+    F-relaxation vs the oracle's two-level coarse correction."""
+    B = _cuda()
+    phi = D.make_phi(order, tab, cfl, nx)
+    fit = OP.fit_hierarchy(phi, nx, m, cfl, (nu,))[0]
+    psi = D.StencilPhi(fit.stencil, nx)
+    U = W.initial_iterate(7, nx, nt, W.u0_fourier(nx, 2))
+    M.f_relax(U, phi, m)
+    Uo = U.copy()
+    # oracle: the second half of vcycle(0) after relaxation
+    cpts = np.arange(m, nt + 1, m)
+    gc = np.zeros((nt // m + 1, nx))
+    gc[1:] = M.residual_rows(Uo, phi, cpts)
+    E = M.sequential_rhs(psi, gc)
+    Uo[cpts] += E[1:]
+    M.f_relax(Uo, phi, m)
+    s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2,
+                [{"kind": "stencil", "offsets": fit.offsets, "coeffs": list(fit.coeffs)}], "FCF")
+    Ug = torch.from_numpy(U).cuda()
+    s.coarse_solve_full(Ug)
+    assert _rel(Ug.cpu().numpy(), Uo) <= REL
+
+
+# ------------------------------------------------------------------ full solves
+def _solve_parity(w, max_iter=None, check_states=True):
+    B = _cuda()
+    phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
+    lib_psi, orc_psi = _oracle_psi(w, phi)
+    max_iter = max_iter or w.max_iter
+    U = w.guess()
+    umax = float(np.max(np.abs(U)))
+    Uo = U.copy()
+    rep = M.solve(Uo, [phi] + orc_psi, w.m, w.dx, w.dt, w.relax, w.tol, max_iter,
+                  keep_states=check_states)
+    s = B.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels, lib_psi, w.relax)
+    g = torch.from_numpy(U).cuda()
+    s.set_guess(g)
+    out = torch.empty_like(g)
+    res = s.solve(w.tol, max_iter, out=out, keep_crows=check_states)
+    kg, ko = res["iterations"], rep.iterations
+    if kg != ko:  # only acceptable as a tie at the tolerance (R16)
+        assert _tie(res["history"][min(kg, ko)], w.tol) or _tie(rep.history[min(kg, ko)], w.tol)
+    assert res["converged"] == rep.converged
+    _hist_ok(res["history"][: ko + 1], rep.history[: kg + 1], w, umax)
+    if check_states:
+        for k in range(min(kg, ko)):
+            assert _rel(res["crows"][k].cpu().numpy(), rep.states[k]) <= REL, k
+    Ug = out.cpu().numpy()
+    assert np.array_equal(Ug[0], U[0])
+    if kg == ko:
+        assert _rel(Ug, Uo) <= REL
+    return res, rep
+
+
+def test_solve_cfg1_ideal():
+    """cfg1 with Psi = Phi^m: one iteration, full size 64 x 256, F-relaxation."""
+    res, rep = _solve_parity(W.CFG1_IDEAL)
+    assert res["iterations"] == 1 and res["converged"]
+
+
+def test_solve_cfg1_redisc():
+    """cfg1 with rediscretised Psi (CFL 1.7): divergent; compared up to the
+    first iteration whose residual exceeds the initial one."""
+    B = _cuda()
+    w = W.CFG1_REDISC
+    phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
+    lib_psi, orc_psi = _oracle_psi(w, phi)
+    U = w.guess()
+    rep = M.solve(U.copy(), [phi] + orc_psi, w.m, w.dx, w.dt, w.relax, w.tol, w.max_iter)
+    s = B.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels, lib_psi, w.relax)
+    s.set_guess(torch.from_numpy(U).cuda())
+    res = s.solve(w.tol, w.max_iter)
+    assert res["iterations"] == rep.iterations == w.max_iter
+    assert not res["converged"] and not rep.converged
+    hg, ho = np.array(res["history"]), np.array(rep.history)
+    # growth-amplified rounding: relative agreement over the whole history
+    assert np.all(np.abs(hg - ho) <= 1e-9 * np.abs(ho)), np.max(np.abs(hg - ho) / np.abs(ho))
+
+
+def test_solve_cfg2_full_size():
+    """cfg2 at its full size 1024 x 4096 (ERK3-Kutta+U3, FCF, m=4, 9-point Psi)."""
+    res, rep = _solve_parity(W.CFG2)
+    assert res["converged"] and 4 <= res["iterations"] <= 8
+
+
+@pytest.mark.parametrize("nx,nt", [(256, 1024), (512, 2048)])
+def test_solve_cfg3_scaled(nx, nt):
+    """cfg3 recipe (ERK5+U5, m=8, 15-point Psi) at reduced sizes."""
+    res, rep = _solve_parity(W.CFG3.scaled(nx, nt))
+    assert res["converged"]
+
+
+@pytest.mark.parametrize("nx,nt,levels", [(256, 1024, 3), (256, 4096, 5), (1024, 4096, 4)])
+def test_solve_cfg5_scaled_vcycle(nx, nt, levels):
+    """cfg5 recipe (ERK3-SSP+U3 V-cycle, m=4, nu_l = 9,13,17,...) at reduced sizes."""
+    w = W.CFG5.scaled(nx, nt, levels=levels)
+    res, rep = _solve_parity(w)
+    assert res["converged"]
+
+
+def test_solve_cfg5_fullwidth_vcycle():
+    """cfg5 at its full width nx = 16384 (the bench launch configurations: halo tiles for
+    the fine sweep, tiled level sweeps and tiled coarsest solve), nt reduced to 1024."""
+    w = W.CFG5.scaled(16384, 1024, levels=4)
+    res, rep = _solve_parity(w, check_states=True)
+    assert res["converged"]
+
+
+def test_solve_parareal_F_relaxation():
+    """Parareal = two-level + F-relaxation with a stencil Psi."""
+    w = W.CFG2.scaled(256, 1024, relax="F", max_iter=40)
+    _solve_parity(w)
