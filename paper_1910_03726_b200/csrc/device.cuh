@@ -77,15 +77,17 @@ __device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<N
     for (int k = 0; k < NR; ++k) buf[warp * E + NL + k] = y[k];
   }
   __syncthreads();
-  if (lane == 0) {
-    const int pw = (warp + NW - 1) % NW;
+  // every lane loads (broadcast address), the edge lanes select: no divergence
+  const int pw = (warp + NW - 1) % NW, nw = (warp + 1) % NW;
 #pragma unroll
-    for (int k = 0; k < NL; ++k) L.v[k] = buf[pw * E + k];
+  for (int k = 0; k < NL; ++k) {
+    const double t = buf[pw * E + k];
+    L.v[k] = (lane == 0) ? t : L.v[k];
   }
-  if (lane == 31) {
-    const int nw = (warp + 1) % NW;
 #pragma unroll
-    for (int k = 0; k < NR; ++k) R.v[k] = buf[nw * E + NL + k];
+  for (int k = 0; k < NR; ++k) {
+    const double t = buf[nw * E + NL + k];
+    R.v[k] = (lane == 31) ? t : R.v[k];
   }
   phase ^= 1;
 }

@@ -45,6 +45,9 @@ struct SweepCfg {
 // scheme: 0 ERK1U1, 1 ERK2U2, 2 ERK3U3, 3 ERK4U4, 4 ERK5U5, 5.. SDIRK
 cudaError_t launch_rk_sweep(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s);
 bool rk_sweep_supported(int scheme, SweepCfg cfg);
+// Persistent TMA-pipelined sweep for halo-tile mode (odd P, even nx; no per-step writes).
+// Tile boundaries are 2*floor(t*(nx/2)/ntiles); HL must be even.
+cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s);
 int rk_scheme_reach_left(int scheme);
 int rk_scheme_reach_right(int scheme);
 int rk_scheme_stages(int scheme);

@@ -291,9 +291,12 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
       return true;
     }
   }
-  // tile mode with halos: window W = NT*P >= T + HL + HR
+  // tile mode with halos: window W = NT*P >= T + HL + HR.  HL is rounded up to even and
+  // tiles are even-aligned (2*floor(t*(nx/2)/ntiles)) so the TMA kernel's bulk copies are
+  // 16-byte aligned.
   const int S = rk_scheme_stages(c->scheme);
-  const int HL = steps * S * rk_scheme_reach_left(c->scheme);
+  int HL = steps * S * rk_scheme_reach_left(c->scheme);
+  HL += HL & 1;
   const int HR = steps * S * rk_scheme_reach_right(c->scheme);
   const int tcand[][2] = {{256, 11}, {128, 11}};
   for (auto &cc : tcand) {
@@ -302,7 +305,7 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
     const int Tmax = W - HL - HR;
     if (Tmax < 64) continue;
     int ntiles = (nx + Tmax - 1) / Tmax;
-    if ((nx + ntiles - 1) / ntiles > Tmax) ++ntiles;
+    while (2 * ((nx / 2 + ntiles - 1) / ntiles) + 1 > Tmax) ++ntiles;
     f.cfg = {cc[0], cc[1]};
     f.ntiles = ntiles;
     f.HL = HL;
@@ -371,6 +374,10 @@ int sweep(mgrit_ctx *c, int cls, SweepArgs a, int total_steps) {
   a.HL = f.HL;
   if (a.partials && (long long)a.nitems * a.ntiles > c->lay.npart)
     return fail(c, MGRIT_ENOMEM, "partials buffer too small");
+  // halo tiles, even nx, no per-step writes: persistent TMA-pipelined kernel
+  const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1) &&
+                   a.each_last < a.each_first && a.in.base;
+  if (tma) return run(c, cls, [&] { return launch_rk_sweep_tma(c->scheme, f.cfg, a, c->stream); });
   return run(c, cls, [&] { return launch_rk_sweep(c->scheme, f.cfg, a, c->stream); });
 }
 

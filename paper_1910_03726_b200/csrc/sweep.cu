@@ -13,6 +13,9 @@
 // The same kernel also serves the FULL-state primitives (F/C relaxation, the
 // all-row residual) and the final F-point materialisation via RowMaps.
 #include "kernels.h"
+#include "tma.cuh"
+
+#include <algorithm>
 
 namespace mg {
 
@@ -105,6 +108,172 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
       for (int i = 1; i <= a.nsteps2; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
       store_slice(const_cast<double *>(rowp(a.r2, item)), x);
     }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Persistent, TMA-pipelined variant for halo-tile mode (odd P => contiguous
+// shared-memory windows).  Each CTA walks work items (interval, tile) with a
+// grid stride; while the FP64 pipes run the m RK steps of item i, the bulk-copy
+// engine prefetches the windows of item i+1 into the other buffer pair and
+// drains the stores (v_{j+1}, r_{j+2}) of item i-1.  Tile boundaries are even so
+// every bulk copy is 16-byte aligned.  Modes: in/cmp/endw/dstore/r2/partials
+// (the production sweeps and the all-row residual); no per-step writes.
+// ---------------------------------------------------------------------------
+template <class SC, int NT, int P>
+__global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant__ SweepArgs a) {
+  static_assert(P % 2 == 1, "contiguous windows need odd P");
+  constexpr int W = NT * P;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(128) double smem[];
+  double *IN[2] = {smem, smem + W};
+  double *CM[2] = {smem + 2 * W, smem + 3 * W};
+  double *edge = smem + 4 * W;
+  double *red = edge + 2 * NW * (SC::NL + SC::NR) + 2;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(red + NW + 2);  // bar[0..1] in, bar[2..3] cmp
+  const int tid = threadIdx.x;
+  const int nx = a.nx;
+  const int total = a.nitems * a.ntiles;
+  const int half = nx >> 1;
+
+  auto tile_beg = [&](int t) { return 2 * (int)(((long long)t * half) / a.ntiles); };
+  auto rowp = [&](const RowMap &r, long long j) -> const double * {
+    return r.base + (r.off + j * r.stride) * (long long)nx;
+  };
+  // issue the window loads of work item w into buffer pair b (one thread)
+  auto issue = [&](int w, int b) {
+    const int item = w / a.ntiles, tile = w - item * a.ntiles;
+    int start = tile_beg(tile) - a.HL;
+    if (start < 0) start += nx;
+    const int n1 = (start + W <= nx) ? W : nx - start;
+    const uint32_t bytes = (uint32_t)W * 8u;
+    mbar_expect_tx(&bar[b], bytes);
+    const double *row = rowp(a.in, item);
+    tma_load_1d(IN[b], row + start, (uint32_t)n1 * 8u, &bar[b]);
+    if (n1 < W) tma_load_1d(IN[b] + n1, row, (uint32_t)(W - n1) * 8u, &bar[b]);
+    if (a.cmp.base) {
+      mbar_expect_tx(&bar[2 + b], bytes);
+      const double *crow = rowp(a.cmp, item);
+      tma_load_1d(CM[b], crow + start, (uint32_t)n1 * 8u, &bar[2 + b]);
+      if (n1 < W) tma_load_1d(CM[b] + n1, crow, (uint32_t)(W - n1) * 8u, &bar[2 + b]);
+    }
+  };
+  // stage x into buf, then bulk-store the owned slice [HL, HL+T) to row[abeg..]
+  auto store = [&](double *row, double *buf, const double(&v)[P], int abeg, int T) {
+    __syncthreads();  // all threads are done reading buf
+#pragma unroll
+    for (int p = 0; p < P; ++p) buf[tid * P + p] = v[p];
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tma_store_1d(row + abeg, buf + a.HL, (uint32_t)T * 8u);
+      bulk_commit();
+    }
+  };
+
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && (int)blockIdx.x < total) issue(blockIdx.x, 0);
+  int phase = 0;
+  int it = 0;
+#pragma unroll 1
+  for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+    const int b = it & 1;
+    const uint32_t par = (uint32_t)((it >> 1) & 1);
+    const int nw = w + gridDim.x;
+    if (tid == 0 && nw < total) {
+      bulk_wait_read_all();  // stores of item it-1 (staged in buffers b^1) have read smem
+      issue(nw, b ^ 1);
+    }
+    const int item = w / a.ntiles, tile = w - item * a.ntiles;
+    const int abeg = tile_beg(tile);
+    const int T = tile_beg(tile + 1) - abeg;
+    mbar_wait(&bar[b], par);
+    double x[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = IN[b][tid * P + p];
+#pragma unroll 1
+    for (int i = 1; i <= a.nsteps1; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
+    if (a.endw.base) store(const_cast<double *>(rowp(a.endw, item)), IN[b], x, abeg, T);
+    if (a.cmp.base) {
+      mbar_wait(&bar[2 + b], par);
+      double d[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) d[p] = x[p] - CM[b][tid * P + p];
+      if (a.partials) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int l = tid * P + p;
+          if (l >= a.HL && l < a.HL + T) sacc = fma(d[p], d[p], sacc);
+        }
+        sacc = block_sum<NT>(sacc, red);
+        if (tid == 0) a.partials[(long long)item * a.ntiles + tile] = sacc;
+      }
+      if (a.dstore.base) {
+        const int jj = item + a.d_phase;
+        if (jj % a.d_every == 0)
+          store(const_cast<double *>(rowp(a.dstore, jj / a.d_every)), CM[b], d, abeg, T);
+      }
+      if (a.nsteps2 > 0 && item < a.p2_items) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) x[p] = d[p];
+#pragma unroll 1
+        for (int i = 1; i <= a.nsteps2; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
+        store(const_cast<double *>(rowp(a.r2, item)), CM[b], x, abeg, T);
+      }
+    }
+    __syncthreads();  // buffers b may be reloaded two items from now
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+template <class SC, int NT, int P>
+static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
+  constexpr int W = NT * P;
+  const size_t smem = sizeof(double) * (4 * W + 2 * (NT / 32) * (SC::NL + SC::NR) + 2 + NT / 32 + 2) +
+                      4 * sizeof(uint64_t) + 16;
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(rk_sweep_tma_kernel<SC, NT, P>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rk_sweep_tma_kernel<SC, NT, P>,
+                                                  NT, smem);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long total = (long long)a.nitems * a.ntiles;
+  if (total <= 0) return cudaSuccess;
+  const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
+  rk_sweep_tma_kernel<SC, NT, P><<<(unsigned)grid, NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+#define MG_TMA_CFGS(X) X(256, 11) X(128, 11)
+
+template <class SC>
+static cudaError_t dispatch_tma(SweepCfg c, const SweepArgs &a, cudaStream_t s) {
+#define MG_CASE(NT_, P_) \
+  if (c.nt_threads == NT_ && c.p == P_) return launch_tma_one<SC, NT_, P_>(a, s);
+  MG_TMA_CFGS(MG_CASE)
+#undef MG_CASE
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s) {
+  switch (scheme) {
+    case 0: return dispatch_tma<ERK1U1>(cfg, a, s);
+    case 1: return dispatch_tma<ERK2U2>(cfg, a, s);
+    case 2: return dispatch_tma<ERK3U3>(cfg, a, s);
+    case 3: return dispatch_tma<ERK4U4>(cfg, a, s);
+    case 4: return dispatch_tma<ERK5U5>(cfg, a, s);
+    default: return cudaErrorInvalidValue;
   }
 }
 
