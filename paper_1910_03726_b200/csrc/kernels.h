@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "device.cuh"
+#include "sdirk.cuh"
 
 namespace mg {
 
@@ -35,6 +36,7 @@ struct SweepArgs {
   RowMap r2;       // phase-2 result
   double *partials;  // [nitems*ntiles] sum(delta^2) over each tile's own outputs
   RKCoeffs co;
+  SdirkCoef sd;      // implicit schemes: factored periodic stage solve (sdirk.cuh)
 };
 
 struct SweepCfg {
@@ -42,7 +44,7 @@ struct SweepCfg {
   int p;           // points per thread
 };
 
-// scheme: 0 ERK1U1, 1 ERK2U2, 2 ERK3U3, 3 ERK4U4, 4 ERK5U5, 5.. SDIRK
+// scheme: 0 ERK1U1, 1 ERK2U2, 2 ERK3U3, 3 ERK4U4, 4 ERK5U5, 5 SDIRK1U1 .. 8 SDIRK4U4
 cudaError_t launch_rk_sweep(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s);
 bool rk_sweep_supported(int scheme, SweepCfg cfg);
 // Persistent TMA-pipelined sweep for halo-tile mode (odd P, even nx; no per-step writes).
@@ -51,6 +53,7 @@ cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cu
 int rk_scheme_reach_left(int scheme);
 int rk_scheme_reach_right(int scheme);
 int rk_scheme_stages(int scheme);
+bool rk_scheme_implicit(int scheme);
 
 // ---- Stencil (Psi) kernels in shifted coordinates ----
 constexpr int MAX_PSI = 64;

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -128,6 +129,10 @@ int scheme_id(int tableau) {
     case MGRIT_TAB_ERK3_KUTTA: return 2;
     case MGRIT_TAB_ERK4: return 3;
     case MGRIT_TAB_ERK5: return 4;
+    case MGRIT_TAB_SDIRK1: return 5;
+    case MGRIT_TAB_SDIRK2: return 6;
+    case MGRIT_TAB_SDIRK3: return 7;
+    case MGRIT_TAB_SDIRK4: return 8;
     default: return -1;
   }
 }
@@ -141,6 +146,103 @@ int tableau_order(int tableau) {
     case MGRIT_TAB_ERK5: return 5;
   }
   return -1;
+}
+
+// Roots of sum_k c[k] x^k (degree n <= 5) by Durand-Kerner in long double, polished by
+// Newton steps; deterministic.
+std::vector<std::complex<long double>> poly_roots(const std::vector<long double> &c) {
+  typedef std::complex<long double> C;
+  const int n = (int)c.size() - 1;
+  std::vector<C> r(n);
+  const C seed(0.4L, 0.9L);
+  for (int k = 0; k < n; ++k) r[k] = std::pow(seed, k);
+  auto eval = [&](C x) {
+    C v = c[n];
+    for (int k = n - 1; k >= 0; --k) v = v * x + (long double)c[k];
+    return v;
+  };
+  auto deriv = [&](C x) {
+    C v = (long double)n * c[n];
+    for (int k = n - 1; k >= 1; --k) v = v * x + (long double)k * c[k];
+    return v;
+  };
+  for (int it = 0; it < 500; ++it) {
+    for (int k = 0; k < n; ++k) {
+      C den = c[n];
+      for (int j = 0; j < n; ++j)
+        if (j != k) den *= (r[k] - r[j]);
+      r[k] -= eval(r[k]) / den;
+    }
+  }
+  for (int k = 0; k < n; ++k)
+    for (int it = 0; it < 4; ++it) {
+      const C d = deriv(r[k]);
+      if (std::abs(d) > 0) r[k] -= eval(r[k]) / d;
+    }
+  return r;
+}
+
+// Factor M = I - a Z (periodic, stencil z_d at d = zlo..zlo+zn-1) into first-order periodic
+// recurrences for the device stage solve (sdirk.cuh).  Returns false if the factorisation is
+// not supported (complex roots, or winding number != 0).
+bool make_sdirk(const double *z, int zlo, int zn, double a, int P, int nx, SdirkCoef &sd,
+                std::string &why) {
+  std::memset(&sd, 0, sizeof(sd));
+  // m_d = delta_d0 - a z_d; polynomial q(x) = sum_d m_d x^(d - zlo)
+  std::vector<long double> q(zn);
+  for (int k = 0; k < zn; ++k) {
+    const int d = zlo + k;
+    q[k] = -(long double)a * (long double)z[k] + (d == 0 ? 1.0L : 0.0L);
+  }
+  while (q.size() > 1 && q.back() == 0.0L) q.pop_back();
+  const int deg = (int)q.size() - 1;
+  const int NL = -zlo;
+  auto roots = poly_roots(q);
+  long double gamma_inv = q[deg];
+  int nin = 0;
+  for (auto &r : roots) {
+    if (std::fabs((double)r.imag()) > 1e-12 * std::max(1.0, (double)std::abs(r))) {
+      why = "complex roots in the SDIRK stage matrix";
+      return false;
+    }
+    const long double rr = r.real();
+    if (std::fabs(rr) < 1.0L) ++nin;
+    else gamma_inv *= -rr;
+  }
+  if (nin != NL) {
+    why = "stage matrix winding number != 0";
+    return false;
+  }
+  if (deg > MAXREC) {
+    why = "too many stage-matrix factors";
+    return false;
+  }
+  sd.gamma = (double)(1.0L / gamma_inv);
+  sd.nrec = deg;
+  int k = 0;
+  // forward (inside) factors first, then backward (outside), in increasing |root|
+  std::vector<long double> rs;
+  for (auto &r : roots) rs.push_back(r.real());
+  std::sort(rs.begin(), rs.end(), [](long double x, long double y) { return std::fabs(x) < std::fabs(y); });
+  for (long double rr : rs) {
+    RecCoef &rc = sd.rec[k++];
+    const bool bwd = std::fabs(rr) >= 1.0L;
+    const long double rho = bwd ? 1.0L / rr : rr;
+    rc.backward = bwd ? 1 : 0;
+    long double pk = 1.0L;
+    for (int i = 0; i <= P; ++i) {
+      rc.rpow[i] = (double)pk;
+      pk *= rho;
+    }
+    const long double rP = powl(rho, (long double)P);
+    long double pj = 1.0L;
+    for (int j = 0; j <= 32; ++j) {
+      rc.rchunk[j] = (double)pj;
+      pj *= rP;
+    }
+    rc.closure = (double)(1.0L / (1.0L - powl(rho, (long double)nx)));
+  }
+  return true;
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -198,6 +300,7 @@ struct mgrit_ctx {
   PsiOp op[MGRIT_MAX_LEVELS];       // stencil Psi of level l >= 1
   double redisc_cfl;
   RKCoeffs fine, coarse_rk;
+  SdirkCoef sd;
   int coarse_q;
   int zlo, zn;
   Tab tab;
@@ -291,6 +394,7 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
       return true;
     }
   }
+  if (rk_scheme_implicit(c->scheme)) return false;  // implicit stage solves need whole rows
   // tile mode with halos: window W = NT*P >= T + HL + HR.  HL is rounded up to even and
   // tiles are even-aligned (2*floor(t*(nx/2)/ntiles)) so the TMA kernel's bulk copies are
   // 16-byte aligned.
@@ -362,6 +466,7 @@ SweepArgs base_sweep(const mgrit_ctx *c) {
   a.each_last = 0;  // none
   a.d_every = 1;
   a.co = c->fine;
+  a.sd = c->sd;
   a.in = a.cmp = a.endw = a.each = a.dstore = a.r2 = kNone;
   return a;
 }
@@ -576,7 +681,7 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
   if (!make_tableau(tableau, c->tab)) return bad(MGRIT_EINVAL, "unknown tableau");
   c->implicit = c->tab.implicit;
   c->scheme = scheme_id(tableau);
-  if (c->implicit || c->scheme < 0) return bad(MGRIT_EUNSUPPORTED, "SDIRK fine propagators are not built yet");
+  if (c->scheme < 0) return bad(MGRIT_EUNSUPPORTED, "unsupported tableau");
   if (!make_layout(nx, nt, m, levels, c->lay)) return bad(MGRIT_EINVAL, "invalid nx/nt/m/levels (nt % m^(levels-1) != 0?)");
   if (workspace_bytes < c->lay.total || !workspace_dev) return bad(MGRIT_ENOMEM, "workspace too small");
   const Upwind &up = kUpwind[order];
@@ -593,6 +698,14 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
     c->fine.b[i] = c->tab.b[i];
     c->fine.mdiag[i] = c->tab.A[i][i];
     for (int j = 0; j < MAXS; ++j) c->fine.A[i][j] = c->tab.A[i][j];
+  }
+  std::memset(&c->sd, 0, sizeof(c->sd));
+  if (c->implicit) {
+    FineCfg f;
+    if (!choose_fine(c, 1, f)) return bad(MGRIT_EUNSUPPORTED, "SDIRK needs nx in {64,128,256,...,4096} (whole-row CTAs)");
+    std::string why;
+    if (!make_sdirk(c->fine.z, c->zlo, c->zn, c->tab.A[0][0], f.cfg.p, nx, c->sd, why))
+      return bad(MGRIT_EUNSUPPORTED, why.c_str());
   }
   // coarse operators
   c->psi_kind = psi[0].kind;
@@ -615,6 +728,7 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
       }
     } else {
       if (levels != 2) return bad(MGRIT_EINVAL, "IDEAL/REDISC Psi only for two levels");
+      if (c->implicit) return bad(MGRIT_EUNSUPPORTED, "RK-form Psi is explicit-only");
       std::memset(&c->coarse_rk, 0, sizeof(c->coarse_rk));
       c->coarse_rk = c->fine;
       if (p.kind == MGRIT_PSI_IDEAL) {

@@ -1,0 +1,149 @@
+// sdirk.cuh — batched periodic banded stage solves of SDIRK Runge-Kutta steps
+// (PAPER.md P:135).
+//
+// Each SDIRK stage solves (I - a_ii Z) y = rhs with Z = dt L the periodic U_p stencil:
+// a circulant band matrix M = sum_d m_d E^d (E = shift).  On the host its symbol
+// polynomial is factored, M = (1/gamma) prod_in (1 - r E^-1) prod_out (1 - rho E),
+// so M^-1 is a product of first-order *periodic* bidiagonal solves
+//     forward   x_i = rho x_{i-1} + f_i      (|rho| < 1, roots inside the unit circle)
+//     backward  x_i = rho x_{i+1} + f_i      (rho = 1/r, roots outside)
+// Each bidiagonal solve is a parallel cyclic reduction (recursive doubling) across
+// the CTA: a sequential pass over the thread's P points, a warp-shuffle scan of the
+// chunk carries, a cross-warp pass, and the rank-1 periodic (Sherman-Morrison)
+// closure c_0 = S / (1 - rho^N).  One __syncthreads per bidiagonal solve.
+#pragma once
+#include "device.cuh"
+
+namespace mg {
+
+constexpr int MAXP = 16;
+constexpr int MAXREC = 4;
+
+struct RecCoef {
+  double rpow[MAXP + 1];   // rho^k, k = 0..P
+  double rchunk[33];       // (rho^P)^j, j = 0..32
+  double closure;          // 1 / (1 - rho^N), N = nx
+  int backward;            // 0: x_i = rho x_{i-1} + f_i ; 1: x_i = rho x_{i+1} + f_i
+  int pad;
+};
+
+struct SdirkCoef {
+  int nrec;
+  int pad;
+  double gamma;            // M^-1 = gamma * prod (bidiagonal inverses)
+  RecCoef rec[MAXREC];
+};
+
+// In-place periodic first-order recurrence over the CTA's whole row (W == nx).
+template <int P, int NT>
+__device__ __forceinline__ void periodic_recurrence(double (&f)[P], const RecCoef &rc,
+                                                    double *wbuf, int &wphase) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double rho = rc.rpow[1];
+  const double mu32 = rc.rchunk[32];
+  double *wb = wbuf + wphase * NW;
+  if (!rc.backward) {
+    double l[P];
+    l[0] = f[0];
+#pragma unroll
+    for (int p = 1; p < P; ++p) l[p] = fma(rho, l[p - 1], f[p]);
+    double A = l[P - 1];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double v = __shfl_up_sync(FULL, A, d);
+      if (lane >= d) A = fma(rc.rchunk[d], v, A);
+    }
+    if (lane == 31) wb[warp] = A;
+    __syncthreads();
+    double tot = 0.0;
+#pragma unroll 1
+    for (int v = 0; v < NW; ++v) tot = fma(mu32, tot, wb[v]);
+    double c = tot * rc.closure;                     // carry entering warp 0 (periodic)
+#pragma unroll 1
+    for (int v = 0; v < warp; ++v) c = fma(mu32, c, wb[v]);
+    const double Aprev = __shfl_up_sync(FULL, A, 1);
+    const double cin = (lane == 0) ? c : fma(rc.rchunk[lane], c, Aprev);
+#pragma unroll
+    for (int p = 0; p < P; ++p) f[p] = fma(rc.rpow[p + 1], cin, l[p]);
+  } else {
+    double l[P];
+    l[P - 1] = f[P - 1];
+#pragma unroll
+    for (int p = P - 2; p >= 0; --p) l[p] = fma(rho, l[p + 1], f[p]);
+    double B = l[0];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double v = __shfl_down_sync(FULL, B, d);
+      if (lane + d < 32) B = fma(rc.rchunk[d], v, B);
+    }
+    if (lane == 0) wb[warp] = B;
+    __syncthreads();
+    double tot = 0.0;
+#pragma unroll 1
+    for (int v = NW - 1; v >= 0; --v) tot = fma(mu32, tot, wb[v]);
+    double c = tot * rc.closure;                     // carry entering the last warp
+#pragma unroll 1
+    for (int v = NW - 1; v > warp; --v) c = fma(mu32, c, wb[v]);
+    const double Bnext = __shfl_down_sync(FULL, B, 1);
+    const double cin = (lane == 31) ? c : fma(rc.rchunk[31 - lane], c, Bnext);
+#pragma unroll
+    for (int p = 0; p < P; ++p) f[p] = fma(rc.rpow[P - p], cin, l[p]);
+  }
+  wphase ^= 1;
+}
+
+template <int P, int NT>
+__device__ __forceinline__ void stage_solve(double (&y)[P], const SdirkCoef &sd, double *wbuf,
+                                            int &wphase) {
+#pragma unroll 1
+  for (int k = 0; k < sd.nrec; ++k) periodic_recurrence<P, NT>(y, sd.rec[k], wbuf, wphase);
+#pragma unroll
+  for (int p = 0; p < P; ++p) y[p] *= sd.gamma;
+}
+
+// One SDIRK step in stage form (b-form update, R14):
+//   (I - a_ii Z) y_i = x + sum_{l<i} a_il k_l,   k_i = Z y_i,   x <- x + sum_i b_i k_i.
+template <class SC, int P, int NT>
+__device__ __forceinline__ void dirk_step(double (&x)[P], const RKCoeffs &c, const SdirkCoef &sd,
+                                          double *edge, int &phase, double *wbuf, int &wphase) {
+  constexpr int S = SC::S;
+  double acc[S][P];
+  double out[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    out[p] = x[p];
+#pragma unroll
+    for (int i = 0; i < S; ++i) acc[i][p] = x[p];
+  }
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    stage_solve<P, NT>(acc[i], sd, wbuf, wphase);
+    double k[P];
+    apply_Z<SC::NL, SC::NR, P, NT>(acc[i], k, c.z, edge, phase);
+#pragma unroll
+    for (int l = i + 1; l < S; ++l) {
+      if (SC::a_nz(l, i)) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) acc[l][p] = fma(c.A[l][i], k[p], acc[l][p]);
+      }
+    }
+    if (SC::b_nz(i)) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) out[p] = fma(c.b[i], k[p], out[p]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) x[p] = out[p];
+}
+
+// SDIRKp + Up pairs (strictly-lower A pattern; the diagonal is the stage solve).
+using SDIRK1U1 = Scheme<1, 1, 0, 0ull, 0x1u, true>;
+using SDIRK2U2 = Scheme<2, 2, 0, abit(1, 0), 0x3u, true>;
+using SDIRK3U3 = Scheme<3, 2, 1, abit(1, 0) | abit(2, 0) | abit(2, 1), 0x7u, true>;
+using SDIRK4U4 = Scheme<5, 3, 1,
+                        abit(1, 0) | abit(2, 0) | abit(2, 1) | abit(3, 0) | abit(3, 1) |
+                            abit(3, 2) | abit(4, 0) | abit(4, 1) | abit(4, 2) | abit(4, 3),
+                        0x1Fu, true>;
+
+}  // namespace mg

@@ -19,6 +19,16 @@
 
 namespace mg {
 
+// One step of Phi: explicit stage form, or SDIRK with periodic banded stage solves.
+template <class SC, int P, int NT>
+__device__ __forceinline__ void phi_step(double (&x)[P], const SweepArgs &a, double *edge,
+                                         int &phase, double *wbuf, int &wphase) {
+  if constexpr (SC::implicit)
+    dirk_step<SC, P, NT>(x, a.co, a.sd, edge, phase, wbuf, wphase);
+  else
+    erk_step<SC, P, NT>(x, a.co, edge, phase);
+}
+
 template <class SC, int NT, int P>
 __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ SweepArgs a) {
   constexpr int SP = Pad<P>::SP;
@@ -29,6 +39,8 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
   double *sB = sA + NT * SP;
   double *edge = sB + NT * SP;
   double *red = edge + 2 * NW * (SC::NL + SC::NR) + 2;
+  double *wbuf = red + NW + 2;  // 2*NW (SDIRK recurrences)
+  int wphase = 0;
 
   const int item = blockIdx.x / a.ntiles;
   const int tile = blockIdx.x - item * a.ntiles;
@@ -73,7 +85,7 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
                     (a.each.off + item * a.each.stride) * (long long)nx, x);
 #pragma unroll 1
   for (int i = 1; i <= a.nsteps1; ++i) {
-    erk_step<SC, P, NT>(x, a.co, edge, phase);
+    phi_step<SC, P, NT>(x, a, edge, phase, wbuf, wphase);
     if (i >= a.each_first && i <= a.each_last)
       store_slice(const_cast<double *>(a.each.base) +
                       (a.each.off + item * a.each.stride + i * a.each_step) * (long long)nx,
@@ -105,7 +117,7 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
 #pragma unroll
       for (int p = 0; p < P; ++p) x[p] = d[p];
 #pragma unroll 1
-      for (int i = 1; i <= a.nsteps2; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
+      for (int i = 1; i <= a.nsteps2; ++i) phi_step<SC, P, NT>(x, a, edge, phase, wbuf, wphase);
       store_slice(const_cast<double *>(rowp(a.r2, item)), x);
     }
   }
@@ -280,23 +292,27 @@ cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cu
 template <class SC> struct SchemeId;
 
 int rk_scheme_reach_left(int scheme) {
-  const int t[] = {ERK1U1::NL, ERK2U2::NL, ERK3U3::NL, ERK4U4::NL, ERK5U5::NL};
-  return (scheme >= 0 && scheme < 5) ? t[scheme] : -1;
+  const int t[] = {ERK1U1::NL, ERK2U2::NL, ERK3U3::NL, ERK4U4::NL, ERK5U5::NL,
+                   SDIRK1U1::NL, SDIRK2U2::NL, SDIRK3U3::NL, SDIRK4U4::NL};
+  return (scheme >= 0 && scheme < 9) ? t[scheme] : -1;
 }
 int rk_scheme_reach_right(int scheme) {
-  const int t[] = {ERK1U1::NR, ERK2U2::NR, ERK3U3::NR, ERK4U4::NR, ERK5U5::NR};
-  return (scheme >= 0 && scheme < 5) ? t[scheme] : -1;
+  const int t[] = {ERK1U1::NR, ERK2U2::NR, ERK3U3::NR, ERK4U4::NR, ERK5U5::NR,
+                   SDIRK1U1::NR, SDIRK2U2::NR, SDIRK3U3::NR, SDIRK4U4::NR};
+  return (scheme >= 0 && scheme < 9) ? t[scheme] : -1;
 }
 int rk_scheme_stages(int scheme) {
-  const int t[] = {ERK1U1::S, ERK2U2::S, ERK3U3::S, ERK4U4::S, ERK5U5::S};
-  return (scheme >= 0 && scheme < 5) ? t[scheme] : -1;
+  const int t[] = {ERK1U1::S, ERK2U2::S, ERK3U3::S, ERK4U4::S, ERK5U5::S,
+                   SDIRK1U1::S, SDIRK2U2::S, SDIRK3U3::S, SDIRK4U4::S};
+  return (scheme >= 0 && scheme < 9) ? t[scheme] : -1;
 }
+bool rk_scheme_implicit(int scheme) { return scheme >= 5 && scheme < 9; }
 
 template <class SC, int NT, int P>
 static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int SP = Pad<P>::SP;
-  const size_t smem =
-      sizeof(double) * (2 * NT * SP + 2 * (NT / 32) * (SC::NL + SC::NR) + 2 + NT / 32 + 2);
+  const size_t smem = sizeof(double) * (2 * NT * SP + 2 * (NT / 32) * (SC::NL + SC::NR) + 2 +
+                                        NT / 32 + 2 + 2 * (NT / 32) + 2);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rk_sweep_kernel<SC, NT, P>,
@@ -321,8 +337,19 @@ static cudaError_t dispatch_cfg(SweepCfg c, const SweepArgs &a, cudaStream_t s) 
   return cudaErrorInvalidConfiguration;
 }
 
+#define MG_IMPL_CFGS(X) X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8)
+template <class SC>
+static cudaError_t dispatch_implicit(SweepCfg c, const SweepArgs &a, cudaStream_t s) {
+#define MG_CASE(NT_, P_) \
+  if (c.nt_threads == NT_ && c.p == P_) return launch_one<SC, NT_, P_>(a, s);
+  MG_IMPL_CFGS(MG_CASE)
+#undef MG_CASE
+  return cudaErrorInvalidConfiguration;
+}
+
 bool rk_sweep_supported(int scheme, SweepCfg c) {
-  if (scheme < 0 || scheme > 4) return false;
+  if (scheme < 0 || scheme > 8) return false;
+  if (scheme >= 5 && c.p == 11) return false;  // implicit: whole periodic rows only
 #define MG_CASE(NT_, P_) \
   if (c.nt_threads == NT_ && c.p == P_) return true;
   MG_CFGS(MG_CASE)
@@ -337,6 +364,10 @@ cudaError_t launch_rk_sweep(int scheme, SweepCfg cfg, const SweepArgs &a, cudaSt
     case 2: return dispatch_cfg<ERK3U3>(cfg, a, s);
     case 3: return dispatch_cfg<ERK4U4>(cfg, a, s);
     case 4: return dispatch_cfg<ERK5U5>(cfg, a, s);
+    case 5: return dispatch_implicit<SDIRK1U1>(cfg, a, s);
+    case 6: return dispatch_implicit<SDIRK2U2>(cfg, a, s);
+    case 7: return dispatch_implicit<SDIRK3U3>(cfg, a, s);
+    case 8: return dispatch_implicit<SDIRK4U4>(cfg, a, s);
     default: return cudaErrorInvalidValue;
   }
 }

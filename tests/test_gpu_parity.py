@@ -77,6 +77,9 @@ PRIM = [  # (order, tableau, cfl, nx, nt, m)
     (4, "erk4", 0.85, 256, 32, 4),
     (5, "erk5", 0.85, 4096, 32, 8),          # cfg3 width: whole periodic rows
     (5, "erk5", 0.85, 12000, 16, 8),         # ERK5 tile mode
+    (1, "sdirk1", 4.0, 64, 32, 2),           # SDIRK: periodic banded stage solves
+    (3, "sdirk3", 4.0, 256, 32, 4),
+    (3, "sdirk3", 4.0, 4096, 16, 4),         # cfg4 width
 ]
 
 
@@ -101,6 +104,17 @@ def test_relax_primitives(order, tab, cfl, nx, nt, m):
         Ug = Ug.cpu().numpy()
         assert np.array_equal(Ug[0], U0[0])
         assert _rel(Ug, Uo) <= REL, (kind, _rel(Ug, Uo))
+
+
+def test_sdirk_complex_roots_unsupported():
+    """SDIRK2+U2 / SDIRK4+U4 stage matrices have complex symbol roots: the library reports
+    EUNSUPPORTED instead of computing anything else."""
+    B = _cuda()
+    for order, tab in [(2, "sdirk2"), (4, "sdirk4")]:
+        with pytest.raises(B.MgritError) as e:
+            B.MGRIT(128, 32, 4, 1.0, 4.0, order, tab, 2,
+                    [{"kind": "stencil", "offsets": [0], "coeffs": [0.5]}], "FCF")
+        assert e.value.code == -5
 
 
 @pytest.mark.parametrize("order,tab,cfl,nx,nt,m", PRIM[:6])
@@ -233,6 +247,21 @@ def test_solve_cfg5_fullwidth_vcycle():
     w = W.CFG5.scaled(16384, 1024, levels=4)
     res, rep = _solve_parity(w, check_states=True)
     assert res["converged"]
+
+
+@pytest.mark.parametrize("nx,nt", [(256, 256), (1024, 1024)])
+def test_solve_cfg4_scaled(nx, nt):
+    """cfg4 recipe (SDIRK3+U3, c = 4, m = 4, eta_tol = 0.01 thresholded Psi)."""
+    res, rep = _solve_parity(W.CFG4.scaled(nx, nt))
+    assert res["converged"]
+
+
+def test_solve_cfg4_literal_11pt_scaled():
+    """cfg4 with the literal 11-point Psi (DESIGN.md R9): no convergence within the cap;
+    histories must still agree."""
+    w = W.CFG4_LITERAL.scaled(256, 1024, max_iter=24)
+    res, rep = _solve_parity(w, check_states=False)
+    assert not res["converged"]
 
 
 def test_solve_parareal_F_relaxation():
