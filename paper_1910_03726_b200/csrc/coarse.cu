@@ -13,6 +13,7 @@
 //    (P:618-624), and its interpolation (correction fused into level l-1's C-rows).
 //  * rk_coarse_kernel: IDEAL (Phi^m) / REDISC Psi in Runge-Kutta form.
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace mg {
 
@@ -233,6 +234,247 @@ __global__ void __launch_bounds__(NT) psi_sweep_kernel(const __grid_constant__ P
     psi_apply<P>(sx, tid * P, a.op, x);
   }
   store(const_cast<double *>(rowp(a.r2, item)), nullptr, origin(2 * m), x);
+}
+
+// --------------------------------------------------------------------------
+// Tile-mode level kernel (odd P => contiguous shared windows) with bulk-copy I/O.
+// All rows an item needs (g rows, u_j, u_{j+1}, v2 rows) are requested by one
+// thread at CTA start (1-2 TMA copies each, completion on one mbarrier per row)
+// so HBM streaming overlaps the Psi steps; outputs leave through two alternating
+// staging buffers with bulk stores (unaligned ends by scalar stores).  Windows
+// start at the even address below the step origin; `off` = origin & 1.
+// --------------------------------------------------------------------------
+template <int P>
+__device__ __forceinline__ void psi_apply_c(const double *__restrict__ s, int base,
+                                            const PsiOp &op, double (&out)[P]) {
+  const double *sp = s + base;
+  double w[P + 3];
+#pragma unroll
+  for (int r = 0; r < P + 3; ++r) w[r] = sp[r];
+#pragma unroll
+  for (int p = 0; p < P; ++p) out[p] = 0.0;
+  const int nu = op.nu, nu4 = nu & ~3;
+  int q0 = 0;
+#pragma unroll 1
+  for (; q0 < nu4; q0 += 4) {
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const double c = op.psi[q0 + qq];
+#pragma unroll
+      for (int p = 0; p < P; ++p) out[p] = fma(c, w[p + qq], out[p]);
+    }
+#pragma unroll
+    for (int r = 0; r + 4 < P + 3; ++r) w[r] = w[r + 4];
+#pragma unroll
+    for (int r = P - 1; r < P + 3; ++r) w[r] = sp[q0 + 4 + r];
+  }
+#pragma unroll 1
+  for (; q0 < nu; ++q0) {
+    const double c = op.psi[q0];
+#pragma unroll
+    for (int p = 0; p < P; ++p) out[p] = fma(c, w[p], out[p]);
+#pragma unroll
+    for (int r = 0; r < P + 2; ++r) w[r] = w[r + 1];
+    w[P + 2] = sp[q0 + P + 3];
+  }
+}
+
+template <int NT, int P>
+__device__ __forceinline__ void psi_put_c(double *s, const double (&x)[P]) {
+  constexpr int W = NT * P;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int l = t * P + p;
+    s[l] = x[p];
+    if (l < PSI_EXT) s[W + l] = x[p];
+  }
+}
+
+template <int NT, int P> struct LevelSmem {
+  static constexpr int W = NT * P;
+  static constexpr int WB = W + 2;                 // even
+  static constexpr int X = (W + PSI_EXT + 1) & ~1;
+  static constexpr int NROW = 8;
+  static constexpr int TOTAL = X + NROW * WB + 2 * WB + 2 * NROW;  // + mbarriers
+};
+
+template <int NT, int P>
+__global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ PsiSweepArgs a) {
+  static_assert(P % 2 == 1, "contiguous windows need odd P");
+  using L = LevelSmem<NT, P>;
+  constexpr int W = L::W, WB = L::WB;
+  extern __shared__ __align__(128) double smem[];
+  double *X = smem;
+  double *RB = smem + L::X;
+  double *ST = RB + L::NROW * WB;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ST + 2 * WB);
+  const int nx = a.nx, tid = threadIdx.x, m = a.m;
+  const int item = blockIdx.x / a.ntiles;
+  const int tile = blockIdx.x - item * a.ntiles;
+  const int half = nx >> 1;
+  const int abeg = 2 * (int)(((long long)tile * half) / a.ntiles);
+  const int T = 2 * (int)(((long long)(tile + 1) * half) / a.ntiles) - abeg;
+  const int o0 = a.op.o0;
+  const bool p2 = !a.interp && item < a.p2_items;
+  const int N = a.interp ? (m - 1) : (p2 ? 2 * m : m);
+  auto origin = [&](int i) { return wrapi((long long)abeg + (long long)(N - i) * o0, nx); };
+  auto rowp = [&](const RowMap &r, long long j) {
+    return r.base + (r.off + j * r.stride) * (long long)nx;
+  };
+  // slots: sweep: 0..m-1 g rows jm+1..jm+m, m: ucmp, m+1: u
+  //        interp: 0: u, 1..m-1: g rows jm+i, m..2m-1: v2 rows jm+i (i = 0..m-1)
+  const long long g0 = a.g.off + (long long)item * a.g.stride;
+  auto slot_row = [&](int k, const double *&row, int &S) -> bool {
+    if (!a.interp) {
+      if (k < m) { row = a.g.base + (g0 + k + 1) * nx; S = origin(k + 1); return true; }
+      if (k == m && a.ucmp.base && p2) { row = rowp(a.ucmp, item); S = origin(m); return true; }
+      if (k == m + 1 && a.u.base) { row = rowp(a.u, item); S = origin(0); return true; }
+      return false;
+    }
+    if (k == 0) { row = rowp(a.u, item); S = origin(0); return a.u.base != nullptr; }
+    if (k < m) { row = a.g.base + (g0 + k) * nx; S = origin(k); return true; }
+    if (k < 2 * m && a.v2.base) {
+      const int i = k - m;
+      row = a.v2.base + (a.v2.off + (long long)item * a.v2.stride + i) * nx;
+      S = origin(i);
+      return true;
+    }
+    return false;
+  };
+  if (tid == 0) {
+    for (int k = 0; k < L::NROW; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+    for (int k = 0; k < L::NROW; ++k) {
+      const double *row;
+      int S;
+      if (!slot_row(k, row, S)) continue;
+      const int S0 = S & ~1;
+      const int n1 = (S0 + WB <= nx) ? WB : nx - S0;
+      mbar_expect_tx(&bar[k], (uint32_t)WB * 8u);
+      tma_load_1d(RB + k * WB, row + S0, (uint32_t)n1 * 8u, &bar[k]);
+      if (n1 < WB) tma_load_1d(RB + k * WB + n1, row, (uint32_t)(WB - n1) * 8u, &bar[k]);
+    }
+  }
+  __syncthreads();
+  auto slot = [&](int k, int S) -> const double * {  // element q of the window at origin S
+    mbar_wait(&bar[k], 0);
+    return RB + k * WB + (S & 1);
+  };
+  int nstore = 0;
+  // out[S .. S+T) = (add ? add[q] : 0) + v[q]  through staging + bulk stores
+  auto store = [&](double *row, int S, const double(&v)[P], const double *add) {
+    const int sb = nstore & 1;
+    if (tid == 0 && nstore >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    ++nstore;
+    __syncthreads();
+    double *st = ST + sb * WB;
+    const int so = S & 1;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int q = tid * P + p;
+      st[so + q] = add ? add[q] + v[p] : v[p];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    // segments [ga, gb) of the periodic slice; scalar stores for odd ends
+    int segs[2][2];
+    int ns = 1;
+    if (S + T <= nx) { segs[0][0] = S; segs[0][1] = S + T; }
+    else { segs[0][0] = S; segs[0][1] = nx; segs[1][0] = 0; segs[1][1] = S + T - nx; ns = 2; }
+    int scalar = 0;
+    for (int k = 0; k < ns; ++k) {
+      int ga = segs[k][0], gb = segs[k][1];
+      const int base = so + (k == 0 ? -S : nx - S);   // smem index of global g = base + g
+      if (ga < gb && (ga & 1)) {
+        if (tid == 1 + scalar) row[ga] = st[base + ga];
+        ++scalar;
+        ++ga;
+      }
+      if (ga < gb && ((gb - ga) & 1)) {
+        if (tid == 1 + scalar) row[gb - 1] = st[base + gb - 1];
+        ++scalar;
+        --gb;
+      }
+      if (tid == 0 && gb > ga) tma_store_1d(row + ga, st + base + ga, (uint32_t)(gb - ga) * 8u);
+    }
+    if (tid == 0) bulk_commit();
+  };
+
+  double x[P];
+  const int ku = a.interp ? 0 : m + 1;
+  if (a.u.base) {
+    const double *su = slot(ku, origin(0));
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = su[tid * P + p];
+  } else {
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = 0.0;
+  }
+  if (a.interp) {
+    const double *add = a.v2.base ? slot(m, origin(0)) : nullptr;
+    store(const_cast<double *>(a.out2.base) + (a.out2.off + (long long)item * a.out2.stride) * nx,
+          origin(0), x, add);
+  }
+  const int n1 = a.interp ? (m - 1) : m;
+#pragma unroll 1
+  for (int i = 1; i <= n1; ++i) {
+    __syncthreads();
+    psi_put_c<NT, P>(X, x);
+    __syncthreads();
+    double y[P];
+    psi_apply_c<P>(X, tid * P, a.op, y);
+    const double *sg = slot(a.interp ? i : i - 1, origin(i));
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * P + p];
+    if (a.interp) {
+      const double *add = a.v2.base ? slot(m + i, origin(i)) : nullptr;
+      store(const_cast<double *>(a.out2.base) +
+                (a.out2.off + (long long)item * a.out2.stride + i) * nx,
+            origin(i), x, add);
+    }
+  }
+  if (!a.interp) {
+    store(const_cast<double *>(rowp(a.v, item)), origin(m), x, nullptr);
+    if (p2) {
+      if (a.ucmp.base) {
+        const double *sc = slot(m, origin(m));
+#pragma unroll
+        for (int p = 0; p < P; ++p) x[p] -= sc[tid * P + p];
+      }
+#pragma unroll 1
+      for (int i = m + 1; i <= 2 * m; ++i) {
+        __syncthreads();
+        psi_put_c<NT, P>(X, x);
+        __syncthreads();
+        psi_apply_c<P>(X, tid * P, a.op, x);
+      }
+      store(const_cast<double *>(rowp(a.r2, item)), origin(2 * m), x, nullptr);
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+template <int NT, int P>
+static cudaError_t launch_level_one(const PsiSweepArgs &a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * LevelSmem<NT, P>::TOTAL + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(psi_level_kernel<NT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  const long long grid = (long long)a.nitems * a.ntiles;
+  if (grid <= 0) return cudaSuccess;
+  psi_level_kernel<NT, P><<<(unsigned)grid, NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_psi_level_tma(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s) {
+  if (a.m > 4 || (a.nx & 1)) return cudaErrorInvalidValue;
+  if (c.nt_threads == 128 && c.p == 9) return launch_level_one<128, 9>(a, s);
+  if (c.nt_threads == 256 && c.p == 9) return launch_level_one<256, 9>(a, s);
+  return cudaErrorInvalidConfiguration;
 }
 
 // --------------------------------------------------------------------------

@@ -97,6 +97,8 @@ struct PsiSweepArgs {
   PsiOp op;
 };
 cudaError_t launch_psi_sweep(SweepCfg cfg, const PsiSweepArgs &a, cudaStream_t s);
+// Tile-mode variant with bulk-copy I/O (odd P, even nx, m <= 4); even tile boundaries.
+cudaError_t launch_psi_level_tma(SweepCfg cfg, const PsiSweepArgs &a, cudaStream_t s);
 
 // RK-form coarse operator (IDEAL = q fine steps, REDISC = one step at CFL m*c),
 // sequential over nsteps, whole periodic row, one CTA.

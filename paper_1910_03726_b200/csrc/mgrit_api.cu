@@ -455,6 +455,20 @@ bool choose_psi(int nx, int halo, bool allow_periodic, PsiCfg &f) {
   return false;
 }
 
+// Tile-mode TMA level kernel: (NT, P) = (128, 9), even tile boundaries.
+bool choose_level_tma(int nx, int m, int halo, PsiCfg &f) {
+  if ((nx & 1) || m > 4) return false;
+  const int W = 128 * 9;
+  if (W > nx) return false;
+  const int Tmax = W - halo;
+  if (Tmax < 128) return false;
+  int ntiles = (nx + Tmax - 1) / Tmax;
+  while (2 * ((nx / 2 + ntiles - 1) / ntiles) > Tmax) ++ntiles;
+  f.cfg = {128, 9};
+  f.ntiles = ntiles;
+  return true;
+}
+
 RowMap rm(const double *b, long long off, long long stride) { return RowMap{b, off, stride}; }
 const RowMap kNone = {nullptr, 0, 0};
 
@@ -553,7 +567,8 @@ int level_sweep(mgrit_ctx *c, int l) {
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
   PsiCfg pc;
-  if (!choose_psi(c->nx, 2 * m * (op.nu - 1), true, pc))
+  const bool tma = choose_level_tma(c->nx, m, 2 * m * (op.nu - 1), pc);
+  if (!tma && !choose_psi(c->nx, 2 * m * (op.nu - 1), true, pc))
     return fail(c, MGRIT_EUNSUPPORTED, "no level-sweep configuration");
   PsiSweepArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -570,6 +585,7 @@ int level_sweep(mgrit_ctx *c, int l) {
   a.p2_items = (int)nc - 1;
   a.v2 = a.out2 = kNone;
   a.op = op;
+  if (tma) return run(c, 1, [&] { return launch_psi_level_tma(pc.cfg, a, c->stream); });
   return run(c, 1, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
 }
 
@@ -580,7 +596,8 @@ int level_interp(mgrit_ctx *c, int l, RowMap v_prev, RowMap out_prev) {
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
   PsiCfg pc;
-  if (!choose_psi(c->nx, (m - 1) * (op.nu - 1), true, pc))
+  const bool tma = choose_level_tma(c->nx, m, (m - 1) * (op.nu - 1), pc);
+  if (!tma && !choose_psi(c->nx, (m - 1) * (op.nu - 1), true, pc))
     return fail(c, MGRIT_EUNSUPPORTED, "no interpolation configuration");
   PsiSweepArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -596,7 +613,8 @@ int level_interp(mgrit_ctx *c, int l, RowMap v_prev, RowMap out_prev) {
   a.v2 = RowMap{v_prev.base, v_prev.off, v_prev.stride * m};
   a.out2 = RowMap{out_prev.base, out_prev.off, out_prev.stride * m};
   a.op = op;
-  int st = run(c, 3, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
+  int st = tma ? run(c, 3, [&] { return launch_psi_level_tma(pc.cfg, a, c->stream); })
+               : run(c, 3, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
   if (st) return st;
   // the last point n = nt_l (level l's last C-row): out[nt_l] = v[nt_l] + u_l[nc]
   const long long ntl = c->ntl[l];
