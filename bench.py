@@ -37,7 +37,11 @@ METRIC = "fine space-time DOF updates/s (fp64) & MGRIT time-to-residual 1e-10"
 UNIT = "DOF-updates/s"
 FP64_PEAK_TFLOPS = 2 * 64 * 148 * 1.965e9 / 1e12   # 64 DFMA/clk/SM x 148 SMs x 1965 MHz
 FP64_PEAK_MEASURED = 34.08                          # tools/probe_fp64 (profiles/), DFMA chains
-FLOPS_PER_POINT_STEP = {3: 33.0, 5: 102.0, 1: 3.0}  # ERK stage form
+# algorithmic flops per point and step of the stage form as implemented:
+# Z with t taps = 1 MUL + (t-1) FMA; every nonzero a_il, b_i = 1 FMA; SDIRK adds its
+# factored stage solves (3 first-order recurrences x 2 FMA + 1 MUL per stage).
+FLOPS_PER_POINT_STEP = {"erk1": 5.0, "erk2": 14.0, "erk3_ssp": 33.0, "erk3_kutta": 33.0,
+                        "erk4": 44.0, "erk5": 102.0, "sdirk3": 72.0}
 
 
 def _dist():
@@ -185,7 +189,7 @@ def run_ours(args, w):
     n_f, ms_f = prof["fine_sweep"]
     nc = w.nt // w.m
     point_steps = w.nx * (nc * w.m + (nc - 1) * w.m)          # phase 1 + phase 2
-    flops = FLOPS_PER_POINT_STEP[w.order] * point_steps
+    flops = FLOPS_PER_POINT_STEP[w.tableau] * point_steps
     avg_ms = ms_f / max(n_f, 1)
     achieved = flops / (avg_ms / 1e3) / 1e12
     shares = {k: round(v[1] / max(ms_total, 1e-9), 4) for k, v in prof.items()}

@@ -291,15 +291,48 @@ __device__ __forceinline__ void psi_put_c(double *s, const double (&x)[P]) {
   }
 }
 
+// Compile-time tap count: the thread's whole input window (P + NU - 1 values) is read
+// once from shared memory and the NU*P FMAs run from registers.
+template <int P, int NU>
+__device__ __forceinline__ void psi_apply_fixed(const double *__restrict__ s, int base,
+                                                const PsiOp &op, double (&out)[P]) {
+  const double *sp = s + base;
+  double w[P + NU - 1];
+#pragma unroll
+  for (int r = 0; r < P + NU - 1; ++r) w[r] = sp[r];
+#pragma unroll
+  for (int p = 0; p < P; ++p) out[p] = 0.0;
+#pragma unroll
+  for (int q = 0; q < NU; ++q) {
+    const double c = op.psi[q];
+#pragma unroll
+    for (int p = 0; p < P; ++p) out[p] = fma(c, w[p + q], out[p]);
+  }
+}
+
+template <int P, int NU>
+__device__ __forceinline__ void psi_apply_any(const double *s, int base, const PsiOp &op,
+                                              double (&out)[P]) {
+  if constexpr (NU > 0)
+    psi_apply_fixed<P, NU>(s, base, op, out);
+  else
+    psi_apply_c<P>(s, base, op, out);
+}
+
 template <int NT, int P> struct LevelSmem {
   static constexpr int W = NT * P;
   static constexpr int WB = W + 2;                 // even
   static constexpr int X = (W + PSI_EXT + 1) & ~1;
-  static constexpr int NROW = 8;
-  static constexpr int TOTAL = X + NROW * WB + 2 * WB + 2 * NROW;  // + mbarriers
+  static constexpr int NROW_MAX = 8;
+  static size_t bytes(int nrow) { return sizeof(double) * (X + (size_t)nrow * WB + 2 * NROW_MAX) + 64; }
 };
 
-template <int NT, int P>
+// Rows of an item (slots, dense):
+//   sweep : g rows jm+1..jm+m, then u_{j+1} (if ucmp), then u_j (if u)
+//   interp: u_j, g rows jm+1..jm+m-1, v2 rows jm+i (i = 0..m-1, if v2)
+// Output staging reuses consumed row buffers: v_{j+1} -> slot of g_1, r_{j+2} -> slot of
+// g_2, interpolated rows in place of their v2 row.
+template <int NT, int P, int NU>
 __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ PsiSweepArgs a) {
   static_assert(P % 2 == 1, "contiguous windows need odd P");
   using L = LevelSmem<NT, P>;
@@ -307,48 +340,48 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
   extern __shared__ __align__(128) double smem[];
   double *X = smem;
   double *RB = smem + L::X;
-  double *ST = RB + L::NROW * WB;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(ST + 2 * WB);
   const int nx = a.nx, tid = threadIdx.x, m = a.m;
+  const bool interp = a.interp != 0;
+  const int nrow = interp ? (1 + (m - 1) + (a.v2.base ? m : 0))
+                          : (m + (a.ucmp.base ? 1 : 0) + (a.u.base ? 1 : 0));
+  uint64_t *bar = reinterpret_cast<uint64_t *>(RB + nrow * WB);
   const int item = blockIdx.x / a.ntiles;
   const int tile = blockIdx.x - item * a.ntiles;
   const int half = nx >> 1;
   const int abeg = 2 * (int)(((long long)tile * half) / a.ntiles);
   const int T = 2 * (int)(((long long)(tile + 1) * half) / a.ntiles) - abeg;
   const int o0 = a.op.o0;
-  const bool p2 = !a.interp && item < a.p2_items;
-  const int N = a.interp ? (m - 1) : (p2 ? 2 * m : m);
+  const bool p2 = !interp && item < a.p2_items;
+  const int N = interp ? (m - 1) : (p2 ? 2 * m : m);
   auto origin = [&](int i) { return wrapi((long long)abeg + (long long)(N - i) * o0, nx); };
   auto rowp = [&](const RowMap &r, long long j) {
     return r.base + (r.off + j * r.stride) * (long long)nx;
   };
-  // slots: sweep: 0..m-1 g rows jm+1..jm+m, m: ucmp, m+1: u
-  //        interp: 0: u, 1..m-1: g rows jm+i, m..2m-1: v2 rows jm+i (i = 0..m-1)
   const long long g0 = a.g.off + (long long)item * a.g.stride;
-  auto slot_row = [&](int k, const double *&row, int &S) -> bool {
-    if (!a.interp) {
-      if (k < m) { row = a.g.base + (g0 + k + 1) * nx; S = origin(k + 1); return true; }
-      if (k == m && a.ucmp.base && p2) { row = rowp(a.ucmp, item); S = origin(m); return true; }
-      if (k == m + 1 && a.u.base) { row = rowp(a.u, item); S = origin(0); return true; }
-      return false;
+  const int k_ucmp = m, k_u = m + (a.ucmp.base ? 1 : 0);
+  auto slot_row = [&](int k, const double *&row, int &S) {
+    if (!interp) {
+      if (k < m) { row = a.g.base + (g0 + k + 1) * nx; S = origin(k + 1); }
+      else if (a.ucmp.base && k == k_ucmp) { row = rowp(a.ucmp, item); S = origin(m); }
+      else { row = rowp(a.u, item); S = origin(0); }
+      return;
     }
-    if (k == 0) { row = rowp(a.u, item); S = origin(0); return a.u.base != nullptr; }
-    if (k < m) { row = a.g.base + (g0 + k) * nx; S = origin(k); return true; }
-    if (k < 2 * m && a.v2.base) {
+    if (k == 0) { row = rowp(a.u, item); S = origin(0); }
+    else if (k < m) { row = a.g.base + (g0 + k) * nx; S = origin(k); }
+    else {
       const int i = k - m;
       row = a.v2.base + (a.v2.off + (long long)item * a.v2.stride + i) * nx;
       S = origin(i);
-      return true;
     }
-    return false;
   };
   if (tid == 0) {
-    for (int k = 0; k < L::NROW; ++k) mbar_init(&bar[k], 1);
+    for (int k = 0; k < nrow; ++k) mbar_init(&bar[k], 1);
     fence_mbar_init();
-    for (int k = 0; k < L::NROW; ++k) {
+    for (int k = 0; k < nrow; ++k) {
       const double *row;
       int S;
-      if (!slot_row(k, row, S)) continue;
+      slot_row(k, row, S);
+      if (!interp && !p2 && a.ucmp.base && k == k_ucmp) continue;  // not needed
       const int S0 = S & ~1;
       const int n1 = (S0 + WB <= nx) ? WB : nx - S0;
       mbar_expect_tx(&bar[k], (uint32_t)WB * 8u);
@@ -357,27 +390,22 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
     }
   }
   __syncthreads();
-  auto slot = [&](int k, int S) -> const double * {  // element q of the window at origin S
+  auto slot = [&](int k, int S) -> double * {  // element q of slot k's window at origin S
     mbar_wait(&bar[k], 0);
     return RB + k * WB + (S & 1);
   };
-  int nstore = 0;
-  // out[S .. S+T) = (add ? add[q] : 0) + v[q]  through staging + bulk stores
-  auto store = [&](double *row, int S, const double(&v)[P], const double *add) {
-    const int sb = nstore & 1;
-    if (tid == 0 && nstore >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-    ++nstore;
+  // out[S .. S+T) = (add ? add[q] : 0) + v[q], staged in buffer `buf` (a consumed row)
+  auto store = [&](double *row, int S, const double(&v)[P], const double *add, double *buf) {
     __syncthreads();
-    double *st = ST + sb * WB;
     const int so = S & 1;
+    double *st = buf + so;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const int q = tid * P + p;
-      st[so + q] = add ? add[q] + v[p] : v[p];
+      st[q] = add ? add[q] + v[p] : v[p];
     }
     fence_proxy_async();
     __syncthreads();
-    // segments [ga, gb) of the periodic slice; scalar stores for odd ends
     int segs[2][2];
     int ns = 1;
     if (S + T <= nx) { segs[0][0] = S; segs[0][1] = S + T; }
@@ -385,60 +413,62 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
     int scalar = 0;
     for (int k = 0; k < ns; ++k) {
       int ga = segs[k][0], gb = segs[k][1];
-      const int base = so + (k == 0 ? -S : nx - S);   // smem index of global g = base + g
+      const int base = so + (k == 0 ? -S : nx - S);   // buffer index of global g = base + g
       if (ga < gb && (ga & 1)) {
-        if (tid == 1 + scalar) row[ga] = st[base + ga];
+        if (tid == 1 + scalar) row[ga] = buf[base + ga];
         ++scalar;
         ++ga;
       }
       if (ga < gb && ((gb - ga) & 1)) {
-        if (tid == 1 + scalar) row[gb - 1] = st[base + gb - 1];
+        if (tid == 1 + scalar) row[gb - 1] = buf[base + gb - 1];
         ++scalar;
         --gb;
       }
-      if (tid == 0 && gb > ga) tma_store_1d(row + ga, st + base + ga, (uint32_t)(gb - ga) * 8u);
+      if (tid == 0 && gb > ga) tma_store_1d(row + ga, buf + base + ga, (uint32_t)(gb - ga) * 8u);
     }
     if (tid == 0) bulk_commit();
   };
 
   double x[P];
-  const int ku = a.interp ? 0 : m + 1;
   if (a.u.base) {
-    const double *su = slot(ku, origin(0));
+    const double *su = slot(interp ? 0 : k_u, origin(0));
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = su[tid * P + p];
   } else {
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = 0.0;
   }
-  if (a.interp) {
-    const double *add = a.v2.base ? slot(m, origin(0)) : nullptr;
+  if (interp) {
+    double *add = a.v2.base ? slot(m, origin(0)) : nullptr;
+    double *buf = a.v2.base ? RB + m * WB : RB;  // v2_0 in place (or the consumed u row)
     store(const_cast<double *>(a.out2.base) + (a.out2.off + (long long)item * a.out2.stride) * nx,
-          origin(0), x, add);
+          origin(0), x, add, buf);
   }
-  const int n1 = a.interp ? (m - 1) : m;
+  const int n1 = interp ? (m - 1) : m;
 #pragma unroll 1
   for (int i = 1; i <= n1; ++i) {
     __syncthreads();
     psi_put_c<NT, P>(X, x);
     __syncthreads();
     double y[P];
-    psi_apply_c<P>(X, tid * P, a.op, y);
-    const double *sg = slot(a.interp ? i : i - 1, origin(i));
+    psi_apply_any<P, NU>(X, tid * P, a.op, y);
+    const int kg = interp ? i : i - 1;
+    const double *sg = slot(kg, origin(i));
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * P + p];
-    if (a.interp) {
-      const double *add = a.v2.base ? slot(m + i, origin(i)) : nullptr;
+    if (interp) {
+      double *add = a.v2.base ? slot(m + i, origin(i)) : nullptr;
+      double *buf = a.v2.base ? RB + (m + i) * WB : RB + kg * WB;
       store(const_cast<double *>(a.out2.base) +
                 (a.out2.off + (long long)item * a.out2.stride + i) * nx,
-            origin(i), x, add);
+            origin(i), x, add, buf);
     }
   }
-  if (!a.interp) {
-    store(const_cast<double *>(rowp(a.v, item)), origin(m), x, nullptr);
+  if (!interp) {
+    store(const_cast<double *>(rowp(a.v, item)), origin(m), x, nullptr, RB);  // slot of g_1
     if (p2) {
       if (a.ucmp.base) {
-        const double *sc = slot(m, origin(m));
+        const double *sc = slot(k_ucmp, origin(m));
 #pragma unroll
         for (int p = 0; p < P; ++p) x[p] -= sc[tid * P + p];
       }
@@ -447,34 +477,44 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
         __syncthreads();
         psi_put_c<NT, P>(X, x);
         __syncthreads();
-        psi_apply_c<P>(X, tid * P, a.op, x);
+        psi_apply_any<P, NU>(X, tid * P, a.op, x);
       }
-      store(const_cast<double *>(rowp(a.r2, item)), origin(2 * m), x, nullptr);
+      store(const_cast<double *>(rowp(a.r2, item)), origin(2 * m), x, nullptr,
+            RB + (m >= 2 ? 1 : 0) * WB);  // slot of g_2
     }
   }
   if (tid == 0) bulk_wait_all();
 }
 
-template <int NT, int P>
+template <int NT, int P, int NU>
 static cudaError_t launch_level_one(const PsiSweepArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * LevelSmem<NT, P>::TOTAL + 64;
+  using L = LevelSmem<NT, P>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(psi_level_kernel<NT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(psi_level_kernel<NT, P, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)L::bytes(L::NROW_MAX));
     attr = true;
   }
+  const int m = a.m;
+  const int nrow = a.interp ? (1 + (m - 1) + (a.v2.base ? m : 0))
+                            : (m + (a.ucmp.base ? 1 : 0) + (a.u.base ? 1 : 0));
   const long long grid = (long long)a.nitems * a.ntiles;
   if (grid <= 0) return cudaSuccess;
-  psi_level_kernel<NT, P><<<(unsigned)grid, NT, smem, s>>>(a);
+  psi_level_kernel<NT, P, NU><<<(unsigned)grid, NT, L::bytes(nrow), s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_psi_level_tma(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s) {
   if (a.m > 4 || (a.nx & 1)) return cudaErrorInvalidValue;
-  if (c.nt_threads == 128 && c.p == 9) return launch_level_one<128, 9>(a, s);
-  if (c.nt_threads == 256 && c.p == 9) return launch_level_one<256, 9>(a, s);
-  return cudaErrorInvalidConfiguration;
+  if (c.nt_threads != 128 || c.p != 9) return cudaErrorInvalidConfiguration;
+  switch (a.op.nu) {
+    case 9: return launch_level_one<128, 9, 9>(a, s);
+    case 13: return launch_level_one<128, 9, 13>(a, s);
+    case 17: return launch_level_one<128, 9, 17>(a, s);
+    case 21: return launch_level_one<128, 9, 21>(a, s);
+    case 25: return launch_level_one<128, 9, 25>(a, s);
+    default: return launch_level_one<128, 9, 0>(a, s);
+  }
 }
 
 // --------------------------------------------------------------------------

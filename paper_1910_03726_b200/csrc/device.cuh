@@ -53,6 +53,16 @@ using ERK5U5 = Scheme<6, 3, 2,
 
 template <int N> struct Arr { double v[N > 0 ? N : 1]; };
 
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// st.shared.f64 under a predicate (no divergent branch).
+__device__ __forceinline__ void st_shared_pred(uint32_t addr, double v, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.f64 [%0], %1; }" ::"r"(addr),
+               "d"(v), "r"((uint32_t)pred)
+               : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Halo exchange: L[k] = y of point (t*P - NL + k), R[k] = y of point (t*P + P + k).
 // `edge` holds 2 * NW * (NL+NR) doubles; `phase` toggles the half in use.
@@ -68,14 +78,12 @@ __device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<N
 #pragma unroll
   for (int k = 0; k < NR; ++k) R.v[k] = __shfl_down_sync(FULL, y[k], 1);
   double *buf = edge + phase * (NW * E);
-  if (lane == 31) {
+  // predicated (not branched) edge stores: lane 31 publishes its tail, lane 0 its head
+  const uint32_t bw = smem_addr(buf + warp * E);
 #pragma unroll
-    for (int k = 0; k < NL; ++k) buf[warp * E + k] = y[P - NL + k];
-  }
-  if (lane == 0) {
+  for (int k = 0; k < NL; ++k) st_shared_pred(bw + 8u * k, y[P - NL + k], lane == 31);
 #pragma unroll
-    for (int k = 0; k < NR; ++k) buf[warp * E + NL + k] = y[k];
-  }
+  for (int k = 0; k < NR; ++k) st_shared_pred(bw + 8u * (NL + k), y[k], lane == 0);
   __syncthreads();
   // every lane loads (broadcast address), the edge lanes select: no divergence
   const int pw = (warp + NW - 1) % NW, nw = (warp + 1) % NW;

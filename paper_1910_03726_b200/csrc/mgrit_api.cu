@@ -14,6 +14,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -402,7 +403,11 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
   int HL = steps * S * rk_scheme_reach_left(c->scheme);
   HL += HL & 1;
   const int HR = steps * S * rk_scheme_reach_right(c->scheme);
-  const int tcand[][2] = {{256, 11}, {128, 11}};
+  int tcand[][2] = {{128, 15}, {256, 11}};
+  if (const char *env = getenv("MGRIT_FINE_TILE")) {  // experiments: "NT,P"
+    int nt_ = 0, p_ = 0;
+    if (sscanf(env, "%d,%d", &nt_, &p_) == 2) { tcand[0][0] = nt_; tcand[0][1] = p_; }
+  }
   for (auto &cc : tcand) {
     const int W = cc[0] * cc[1];
     if (W > nx) continue;
@@ -494,8 +499,8 @@ int sweep(mgrit_ctx *c, int cls, SweepArgs a, int total_steps) {
   if (a.partials && (long long)a.nitems * a.ntiles > c->lay.npart)
     return fail(c, MGRIT_ENOMEM, "partials buffer too small");
   // halo tiles, even nx, no per-step writes: persistent TMA-pipelined kernel
-  const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1) &&
-                   a.each_last < a.each_first && a.in.base;
+  const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1) && a.in.base &&
+                   (a.each_last < a.each_first || !a.cmp.base);
   if (tma) return run(c, cls, [&] { return launch_rk_sweep_tma(c->scheme, f.cfg, a, c->stream); });
   return run(c, cls, [&] { return launch_rk_sweep(c->scheme, f.cfg, a, c->stream); });
 }

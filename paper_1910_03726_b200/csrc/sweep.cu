@@ -16,6 +16,7 @@
 #include "tma.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 namespace mg {
 
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
 // engine prefetches the windows of item i+1 into the other buffer pair and
 // drains the stores (v_{j+1}, r_{j+2}) of item i-1.  Tile boundaries are even so
 // every bulk copy is 16-byte aligned.  Modes: in/cmp/endw/dstore/r2/partials
-// (the production sweeps and the all-row residual); no per-step writes.
+// (the production sweeps and the all-row residual) and per-step writes (each).
 // ---------------------------------------------------------------------------
 template <class SC, int NT, int P>
 __global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant__ SweepArgs a) {
@@ -139,11 +140,14 @@ __global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant_
   constexpr int W = NT * P;
   constexpr int NW = NT / 32;
   extern __shared__ __align__(128) double smem[];
-  double *IN[2] = {smem, smem + W};
-  double *CM[2] = {smem + 2 * W, smem + 3 * W};
-  double *edge = smem + 4 * W;
+  // buffers: IN(b) = smem + b*W (double-buffered prefetch), CM = smem + 2W (the comparison
+  // row u_{j+1}, loaded at item start and consumed after phase 1).  Macros, not pointer
+  // arrays (those would live in local memory).
+#define IN(b) (smem + (b) * W)
+  double *CM = smem + 2 * W;
+  double *edge = smem + 3 * W;
   double *red = edge + 2 * NW * (SC::NL + SC::NR) + 2;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(red + NW + 2);  // bar[0..1] in, bar[2..3] cmp
+  uint64_t *bar = reinterpret_cast<uint64_t *>(red + NW + 2);  // bar[0..1] in, bar[2] cmp
   const int tid = threadIdx.x;
   const int nx = a.nx;
   const int total = a.nitems * a.ntiles;
@@ -153,23 +157,28 @@ __global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant_
   auto rowp = [&](const RowMap &r, long long j) -> const double * {
     return r.base + (r.off + j * r.stride) * (long long)nx;
   };
-  // issue the window loads of work item w into buffer pair b (one thread)
-  auto issue = [&](int w, int b) {
-    const int item = w / a.ntiles, tile = w - item * a.ntiles;
-    int start = tile_beg(tile) - a.HL;
+  // window loads (one thread): `in` rows of item w into IN(b), `cmp` rows into CM
+  auto window = [&](int w, int &start, int &n1) {
+    const int tile = w % a.ntiles;
+    start = tile_beg(tile) - a.HL;
     if (start < 0) start += nx;
-    const int n1 = (start + W <= nx) ? W : nx - start;
-    const uint32_t bytes = (uint32_t)W * 8u;
-    mbar_expect_tx(&bar[b], bytes);
-    const double *row = rowp(a.in, item);
-    tma_load_1d(IN[b], row + start, (uint32_t)n1 * 8u, &bar[b]);
-    if (n1 < W) tma_load_1d(IN[b] + n1, row, (uint32_t)(W - n1) * 8u, &bar[b]);
-    if (a.cmp.base) {
-      mbar_expect_tx(&bar[2 + b], bytes);
-      const double *crow = rowp(a.cmp, item);
-      tma_load_1d(CM[b], crow + start, (uint32_t)n1 * 8u, &bar[2 + b]);
-      if (n1 < W) tma_load_1d(CM[b] + n1, crow, (uint32_t)(W - n1) * 8u, &bar[2 + b]);
-    }
+    n1 = (start + W <= nx) ? W : nx - start;
+  };
+  auto issue_in = [&](int w, int b) {
+    int start, n1;
+    window(w, start, n1);
+    mbar_expect_tx(&bar[b], (uint32_t)W * 8u);
+    const double *row = rowp(a.in, w / a.ntiles);
+    tma_load_1d(IN(b), row + start, (uint32_t)n1 * 8u, &bar[b]);
+    if (n1 < W) tma_load_1d(IN(b) + n1, row, (uint32_t)(W - n1) * 8u, &bar[b]);
+  };
+  auto issue_cmp = [&](int w) {
+    int start, n1;
+    window(w, start, n1);
+    mbar_expect_tx(&bar[2], (uint32_t)W * 8u);
+    const double *row = rowp(a.cmp, w / a.ntiles);
+    tma_load_1d(CM, row + start, (uint32_t)n1 * 8u, &bar[2]);
+    if (n1 < W) tma_load_1d(CM + n1, row, (uint32_t)(W - n1) * 8u, &bar[2]);
   };
   // stage x into buf, then bulk-store the owned slice [HL, HL+T) to row[abeg..]
   auto store = [&](double *row, double *buf, const double(&v)[P], int abeg, int T) {
@@ -185,21 +194,23 @@ __global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant_
   };
 
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0 && (int)blockIdx.x < total) issue(blockIdx.x, 0);
+  if (tid == 0 && (int)blockIdx.x < total) issue_in(blockIdx.x, 0);
   int phase = 0;
   int it = 0;
+  int nstage = 0;
 #pragma unroll 1
   for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
     const int b = it & 1;
     const uint32_t par = (uint32_t)((it >> 1) & 1);
     const int nw = w + gridDim.x;
-    if (tid == 0 && nw < total) {
-      bulk_wait_read_all();  // stores of item it-1 (staged in buffers b^1) have read smem
-      issue(nw, b ^ 1);
+    if (tid == 0) {
+      bulk_wait_read_all();  // stores of item it-1 (staged in IN(b^1) / CM) have read smem
+      if (nw < total) issue_in(nw, b ^ 1);
+      if (a.cmp.base) issue_cmp(w);
     }
     const int item = w / a.ntiles, tile = w - item * a.ntiles;
     const int abeg = tile_beg(tile);
@@ -207,15 +218,29 @@ __global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant_
     mbar_wait(&bar[b], par);
     double x[P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) x[p] = IN[b][tid * P + p];
+    for (int p = 0; p < P; ++p) x[p] = IN(b)[tid * P + p];
+    // per-step writes (F-relaxation / materialisation): alternate the two CM buffers
+    // as staging (no comparison rows in this mode)
+    auto each_store = [&](int i) {
+      if (tid == 0 && nstage >= 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      double *row = const_cast<double *>(a.each.base) +
+                    (a.each.off + (long long)item * a.each.stride + (long long)i * a.each_step) *
+                        (long long)nx;
+      store(row, (nstage & 1) ? CM : IN(b), x, abeg, T);
+      ++nstage;
+    };
+    if (a.each_first == 0 && a.each_last >= 0) each_store(0);
 #pragma unroll 1
-    for (int i = 1; i <= a.nsteps1; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
-    if (a.endw.base) store(const_cast<double *>(rowp(a.endw, item)), IN[b], x, abeg, T);
+    for (int i = 1; i <= a.nsteps1; ++i) {
+      erk_step<SC, P, NT>(x, a.co, edge, phase);
+      if (i >= a.each_first && i <= a.each_last) each_store(i);
+    }
+    if (a.endw.base) store(const_cast<double *>(rowp(a.endw, item)), IN(b), x, abeg, T);
     if (a.cmp.base) {
-      mbar_wait(&bar[2 + b], par);
+      mbar_wait(&bar[2], (uint32_t)(it & 1));
       double d[P];
 #pragma unroll
-      for (int p = 0; p < P; ++p) d[p] = x[p] - CM[b][tid * P + p];
+      for (int p = 0; p < P; ++p) d[p] = x[p] - CM[tid * P + p];
       if (a.partials) {
         double sacc = 0.0;
 #pragma unroll
@@ -229,32 +254,34 @@ __global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant_
       if (a.dstore.base) {
         const int jj = item + a.d_phase;
         if (jj % a.d_every == 0)
-          store(const_cast<double *>(rowp(a.dstore, jj / a.d_every)), CM[b], d, abeg, T);
+          store(const_cast<double *>(rowp(a.dstore, jj / a.d_every)), CM, d, abeg, T);
       }
       if (a.nsteps2 > 0 && item < a.p2_items) {
 #pragma unroll
         for (int p = 0; p < P; ++p) x[p] = d[p];
 #pragma unroll 1
         for (int i = 1; i <= a.nsteps2; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
-        store(const_cast<double *>(rowp(a.r2, item)), CM[b], x, abeg, T);
+        store(const_cast<double *>(rowp(a.r2, item)), CM, x, abeg, T);
       }
     }
     __syncthreads();  // buffers b may be reloaded two items from now
   }
   if (tid == 0) bulk_wait_all();
+#undef IN
 }
 
 template <class SC, int NT, int P>
 static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int W = NT * P;
-  const size_t smem = sizeof(double) * (4 * W + 2 * (NT / 32) * (SC::NL + SC::NR) + 2 + NT / 32 + 2) +
-                      4 * sizeof(uint64_t) + 16;
+  const size_t smem =
+      sizeof(double) * (3 * W + 2 * (NT / 32) * (SC::NL + SC::NR) + 2 + NT / 32 + 2) +
+      4 * sizeof(uint64_t) + 16;
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
     cudaFuncSetAttribute(rk_sweep_tma_kernel<SC, NT, P>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rk_sweep_tma_kernel<SC, NT, P>,
-                                                  NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
+                                                  rk_sweep_tma_kernel<SC, NT, P>, NT, smem);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   int dev = 0, sms = 148;
@@ -267,7 +294,7 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-#define MG_TMA_CFGS(X) X(256, 11) X(128, 11)
+#define MG_TMA_CFGS(X) X(256, 11) X(128, 11) X(128, 15) X(128, 13) X(64, 15) X(96, 15) X(160, 13)
 
 template <class SC>
 static cudaError_t dispatch_tma(SweepCfg c, const SweepArgs &a, cudaStream_t s) {
