@@ -96,6 +96,25 @@ def _profile_traffic():
         return None
 
 
+def aggregate(ms_local: float, dof_local: int, dist=None):
+    """Replicas: every rank solves its own replica; the job time is the
+    max over ranks (device-timed), the value all ranks' DOF updates / that time."""
+    world = 1
+    ms = ms_local
+    dof = dof_local
+    if dist is not None and dist.is_initialized():
+        import torch
+        world = dist.get_world_size()
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([ms_local, float(dof_local)], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        ms = float(tmax[0].item())
+        dof = int(t[1].item())
+    return ms, dof / (ms / 1e3), world
+
+
 # ------------------------------------------------------------------ oracle sample
 def oracle_sample(w, budget_s: float = 12.0):
     """The oracle, as it stands, on a bounded sample of the workload: full-width rows
@@ -175,15 +194,10 @@ def run_ours(args, w):
     if sampler:
         sampler.terminate()
         sampler.wait()
-    ms = ms_total / args.steps
-    if dist:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     K = iters[-1]
     assert all(k == K for k in iters), iters
     dof = problem.dof_updates(w, K)
-    value = dof * world / (ms / 1e3)
+    ms, value, world = aggregate(ms_total / args.steps, dof, dist)
 
     # ---- roofline of the dominant kernel: the fine FCF sweep (class fine_sweep) ----
     n_f, ms_f = prof["fine_sweep"]

@@ -501,6 +501,8 @@ int sweep(mgrit_ctx *c, int cls, SweepArgs a, int total_steps) {
   // halo tiles, even nx, no per-step writes: persistent TMA-pipelined kernel
   const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1) && a.in.base &&
                    (a.each_last < a.each_first || !a.cmp.base);
+  if (tma && f.cfg.nt_threads == 32)
+    return run(c, cls, [&] { return launch_rk_sweep_warp(c->scheme, f.cfg, a, c->stream); });
   if (tma) return run(c, cls, [&] { return launch_rk_sweep_tma(c->scheme, f.cfg, a, c->stream); });
   return run(c, cls, [&] { return launch_rk_sweep(c->scheme, f.cfg, a, c->stream); });
 }

@@ -268,3 +268,74 @@ def test_solve_parareal_F_relaxation():
     """Parareal = two-level + F-relaxation with a stencil Psi."""
     w = W.CFG2.scaled(256, 1024, relax="F", max_iter=40)
     _solve_parity(w)
+
+
+# ------------------------------------------------------------------ full sizes (sampled)
+def _sampled_rows(rng, lo, hi, k):
+    return sorted(set(int(v) for v in rng.integers(lo, hi, size=k)))
+
+
+@pytest.mark.parametrize("wname", ["cfg3", "cfg4", "cfg5"])
+def test_fullsize_fcf_relaxation_sampled(wname):
+    """FCF relaxation of the FULL initial iterate at the workload's full size and in the
+    launch configuration the solver uses (tiles / whole rows), checked on sampled
+    intervals: after F-C-F, row jm+i = Phi^(m+i) of the old row (j-1)m."""
+    B = _cuda()
+    w = W.ALL[wname]
+    phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
+    u0 = torch.from_numpy(w.u0()).cuda()
+    U = torch.empty((w.nt + 1, w.nx), dtype=torch.float64, device="cuda")
+    B.fill_guess(U, w.guess_seed, w.guess_lo, u0=u0)
+    s = B.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, 2,
+                [{"kind": "stencil", "offsets": [0], "coeffs": [0.5]}], "FCF")
+    s.relax_full(U, "FCF")
+    rng = np.random.default_rng(0)
+    nc = w.nt // w.m
+    for j in _sampled_rows(rng, 1, nc, 6) + [nc - 1]:
+        src = W.guess_rows(w.guess_seed, w.nx, np.array([(j - 1) * w.m]), w.guess_lo)[0]
+        if j - 1 == 0:
+            src = w.u0()
+        x = src
+        for _ in range(w.m):
+            x = phi(x)
+        got = U[j * w.m: (j + 1) * w.m].cpu().numpy()
+        for i in range(w.m):
+            if i > 0:
+                x = phi(x)
+            assert _rel(got[i], x) <= REL, (j, i, _rel(got[i], x))
+
+
+@pytest.mark.parametrize("wname", ["cfg3", "cfg4", "cfg5"])
+def test_fullsize_solve_properties(wname):
+    """Full-size solve in the bench configuration: converges in the expected number of
+    iterations, row 0 is u0 bitwise, every sampled F-row satisfies U[n] = Phi U[n-1] to
+    rounding (ideal interpolation), sampled C-row residuals are bounded by the
+    reported final residual, and the library's own all-row residual of the output
+    reproduces hist[K] (R1, R2)."""
+    from paper_1910_03726_b200 import problem
+    B = _cuda()
+    w = W.ALL[wname]
+    s = problem.make_solver(w)
+    g = problem.device_guess(w)
+    s.set_guess(g)
+    out = torch.empty_like(g)
+    res = s.solve(w.tol, w.max_iter, out=out)
+    assert res["converged"]
+    expect = {"cfg3": (3, 7), "cfg4": (4, 7), "cfg5": (5, 9)}[wname]
+    assert expect[0] <= res["iterations"] <= expect[1], res["history"]
+    u0 = w.u0()
+    assert np.array_equal(out[0].cpu().numpy(), u0)
+    phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
+    rng = np.random.default_rng(1)
+    umax = float(out.abs().max())
+    dxdt = w.dx * w.dt
+    for n in _sampled_rows(rng, 1, w.nt + 1, 12):
+        prev = out[n - 1].cpu().numpy()
+        cur = out[n].cpu().numpy()
+        r = phi(prev) - cur
+        if n % w.m:
+            assert np.max(np.abs(r)) <= 1e-12 * umax, (n, np.max(np.abs(r)))
+        else:
+            assert math.sqrt(dxdt * np.sum(r * r)) <= res["history"][-1] * (1 + 1e-9) + 1e-16
+    again = s.residual_full(out)
+    assert abs(again - res["history"][-1]) <= 1e-6 * res["history"][-1] + 1e-15
