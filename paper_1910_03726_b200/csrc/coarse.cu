@@ -68,7 +68,7 @@ template <int NT, int P> struct PsiSmem {
   static constexpr int SP = Pad<P>::SP;
   static constexpr int X = (NT + PSI_EXT / P + 2) * SP;  // state + tail
   static constexpr int G = NT * SP;                      // g window / staging
-  static constexpr int TOTAL = X + 2 * G;
+  static constexpr int TOTAL = 2 * X + 2 * G;   // ping-pong state + ping-pong g/staging
 };
 
 // --------------------------------------------------------------------------
@@ -77,65 +77,68 @@ __global__ void __launch_bounds__(NT) psi_coarse_kernel(const __grid_constant__ 
   constexpr int W = NT * P;
   extern __shared__ double smem[];
   constexpr int SP = Pad<P>::SP;
-  double *sx = smem;                           // state + periodic tail (padded)
-  double *sg = sx + PsiSmem<NT, P>::X;         // g window (padded)
-  double *so = sg + PsiSmem<NT, P>::G;         // output staging (padded)
+  // ping-pong buffers: state (+ periodic tail) and g window; one barrier per step.  The
+  // state buffer of step i also serves the coalesced store of out_{i-1} = v + x_{i-1}.
+#define SX(b) (smem + (b) * PsiSmem<NT, P>::X)
+#define SG(b) (smem + 2 * PsiSmem<NT, P>::X + (b) * PsiSmem<NT, P>::G)
   const int nx = a.nx, tid = threadIdx.x;
   const int tile = blockIdx.x;
   const int abeg = (int)(((long long)tile * nx) / a.ntiles);
   const int T = (int)(((long long)(tile + 1) * nx) / a.ntiles) - abeg;
   const int N = a.nsteps, o0 = a.op.o0;
   // origin of step i: S_i = abeg + (N - i) * o0  (mod nx); S_N = abeg
+  auto origin = [&](int i) { return wrapi((long long)abeg + (long long)(N - i) * o0, nx); };
   double x[P];
-  {
-    const int S0 = wrapi((long long)abeg + (long long)N * o0, nx);
-    if (a.state_in) {
-      for (int q = tid; q < W; q += NT) {
-        int g = S0 + q;
-        if (g >= nx) g -= nx;
-        sx[pidx<P>(q)] = a.state_in[g];
-      }
-      __syncthreads();
-#pragma unroll
-      for (int p = 0; p < P; ++p) x[p] = sx[tid * SP + p];
-    } else {
-#pragma unroll
-      for (int p = 0; p < P; ++p) x[p] = 0.0;
-    }
-  }
-#pragma unroll 1
-  for (int i = 1; i <= N; ++i) {
-    const long long n = a.n0 + i;
-    const int Si = wrapi((long long)abeg + (long long)(N - i) * o0, nx);
-    __syncthreads();
-    psi_put<NT, P>(sx, x);
-    const double *grow = a.g.base + (a.g.off + n * a.g.stride) * (long long)nx;
+  if (a.state_in) {
+    const int S0 = origin(0);
     for (int q = tid; q < W; q += NT) {
-      int g = Si + q;
+      int g = S0 + q;
       if (g >= nx) g -= nx;
-      sg[pidx<P>(q)] = __ldg(grow + g);
+      SG(1)[pidx<P>(q)] = a.state_in[g];
     }
     __syncthreads();
-    double y[P];
-    psi_apply<P>(sx, tid * P, a.op, y);
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      x[p] = y[p] + sg[tid * SP + p];
-      so[tid * SP + p] = x[p];
-    }
-    __syncthreads();
+    for (int p = 0; p < P; ++p) x[p] = SG(1)[tid * SP + p];
+  } else {
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = 0.0;
+  }
+  auto store_out = [&](long long n, int S, const double *sx) {
     double *orow = const_cast<double *>(a.out.base) + (a.out.off + n * a.out.stride) * (long long)nx;
     const double *vrow = a.v.base ? a.v.base + (a.v.off + n * a.v.stride) * (long long)nx : nullptr;
     for (int q = tid; q < T; q += NT) {
-      int g = Si + q;
+      int g = S + q;
       if (g >= nx) g -= nx;
-      orow[g] = vrow ? vrow[g] + so[pidx<P>(q)] : so[pidx<P>(q)];
+      orow[g] = vrow ? vrow[g] + sx[pidx<P>(q)] : sx[pidx<P>(q)];
     }
+  };
+#pragma unroll 1
+  for (int i = 1; i <= N + 1; ++i) {
+    double *sx = SX(i & 1), *sg = SG(i & 1);
+    psi_put<NT, P>(sx, x);                 // x_{i-1}
+    if (i <= N) {
+      const double *grow = a.g.base + (a.g.off + (a.n0 + i) * a.g.stride) * (long long)nx;
+      const int Si = origin(i);
+      for (int q = tid; q < W; q += NT) {
+        int g = Si + q;
+        if (g >= nx) g -= nx;
+        sg[pidx<P>(q)] = __ldg(grow + g);
+      }
+    }
+    __syncthreads();
+    if (i >= 2) store_out(a.n0 + i - 1, origin(i - 1), sx);
+    if (i > N) {
+      if (a.state_out)   // S_N = abeg: the owned slice [abeg, abeg+T)
+        for (int q = tid; q < T; q += NT) a.state_out[abeg + q] = sx[pidx<P>(q)];
+      break;
+    }
+    double y[P];
+    psi_apply<P>(sx, tid * P, a.op, y);
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * SP + p];
   }
-  if (a.state_out) {
-    // S_N = abeg: the owned slice [abeg, abeg+T) is so[0..T)
-    for (int q = tid; q < T; q += NT) a.state_out[abeg + q] = so[pidx<P>(q)];
-  }
+#undef SX
+#undef SG
 }
 
 // --------------------------------------------------------------------------
@@ -324,7 +327,7 @@ template <int NT, int P> struct LevelSmem {
   static constexpr int WB = W + 2;                 // even
   static constexpr int X = (W + PSI_EXT + 1) & ~1;
   static constexpr int NROW_MAX = 8;
-  static size_t bytes(int nrow) { return sizeof(double) * (X + (size_t)nrow * WB + 2 * NROW_MAX) + 64; }
+  static size_t bytes(int nrow) { return sizeof(double) * (2 * X + (size_t)nrow * WB + 2 * NROW_MAX) + 64; }
 };
 
 // Rows of an item (slots, dense):
@@ -338,12 +341,11 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
   using L = LevelSmem<NT, P>;
   constexpr int W = L::W, WB = L::WB;
   extern __shared__ __align__(128) double smem[];
-  double *X = smem;
-  double *RB = smem + L::X;
+  double *X = smem;             // two state buffers (ping-pong): one barrier per step
+  double *RB = smem + 2 * L::X;
   const int nx = a.nx, tid = threadIdx.x, m = a.m;
   const bool interp = a.interp != 0;
-  const int nrow = interp ? (1 + (m - 1) + (a.v2.base ? m : 0))
-                          : (m + (a.ucmp.base ? 1 : 0) + (a.u.base ? 1 : 0));
+  const int nrow = interp ? m : (m + (a.ucmp.base ? 1 : 0) + (a.u.base ? 1 : 0));
   uint64_t *bar = reinterpret_cast<uint64_t *>(RB + nrow * WB);
   const int item = blockIdx.x / a.ntiles;
   const int tile = blockIdx.x - item * a.ntiles;
@@ -367,12 +369,7 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
       return;
     }
     if (k == 0) { row = rowp(a.u, item); S = origin(0); }
-    else if (k < m) { row = a.g.base + (g0 + k) * nx; S = origin(k); }
-    else {
-      const int i = k - m;
-      row = a.v2.base + (a.v2.off + (long long)item * a.v2.stride + i) * nx;
-      S = origin(i);
-    }
+    else { row = a.g.base + (g0 + k) * nx; S = origin(k); }
   };
   if (tid == 0) {
     for (int k = 0; k < nrow; ++k) mbar_init(&bar[k], 1);
@@ -394,16 +391,15 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
     mbar_wait(&bar[k], 0);
     return RB + k * WB + (S & 1);
   };
-  // out[S .. S+T) = (add ? add[q] : 0) + v[q], staged in buffer `buf` (a consumed row)
-  auto store = [&](double *row, int S, const double(&v)[P], const double *add, double *buf) {
-    __syncthreads();
+  // out[S .. S+T) = v[q]  (or out += v[q] with `acc`: bulk reduce-add at L2), staged in
+  // buffer `buf`, a consumed row.  No barrier before staging: each thread overwrites only
+  // buffer positions it read itself in this step (same origin), or positions of a row
+  // consumed at least one barrier ago.
+  auto store = [&](double *row, int S, const double(&v)[P], bool acc, double *buf) {
     const int so = S & 1;
     double *st = buf + so;
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const int q = tid * P + p;
-      st[q] = add ? add[q] + v[p] : v[p];
-    }
+    for (int p = 0; p < P; ++p) st[tid * P + p] = v[p];
     fence_proxy_async();
     __syncthreads();
     int segs[2][2];
@@ -415,16 +411,20 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
       int ga = segs[k][0], gb = segs[k][1];
       const int base = so + (k == 0 ? -S : nx - S);   // buffer index of global g = base + g
       if (ga < gb && (ga & 1)) {
-        if (tid == 1 + scalar) row[ga] = buf[base + ga];
+        if (tid == 1 + scalar) row[ga] = acc ? row[ga] + buf[base + ga] : buf[base + ga];
         ++scalar;
         ++ga;
       }
       if (ga < gb && ((gb - ga) & 1)) {
-        if (tid == 1 + scalar) row[gb - 1] = buf[base + gb - 1];
+        if (tid == 1 + scalar)
+          row[gb - 1] = acc ? row[gb - 1] + buf[base + gb - 1] : buf[base + gb - 1];
         ++scalar;
         --gb;
       }
-      if (tid == 0 && gb > ga) tma_store_1d(row + ga, buf + base + ga, (uint32_t)(gb - ga) * 8u);
+      if (tid == 0 && gb > ga) {
+        if (acc) tma_reduce_add_1d(row + ga, buf + base + ga, (uint32_t)(gb - ga) * 8u);
+        else tma_store_1d(row + ga, buf + base + ga, (uint32_t)(gb - ga) * 8u);
+      }
     }
     if (tid == 0) bulk_commit();
   };
@@ -438,34 +438,35 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = 0.0;
   }
-  if (interp) {
-    double *add = a.v2.base ? slot(m, origin(0)) : nullptr;
-    double *buf = a.v2.base ? RB + m * WB : RB;  // v2_0 in place (or the consumed u row)
+  if (interp)  // out[jm] += u_j  (staged in place of the consumed u row)
     store(const_cast<double *>(a.out2.base) + (a.out2.off + (long long)item * a.out2.stride) * nx,
-          origin(0), x, add, buf);
-  }
+          origin(0), x, true, RB);
   const int n1 = interp ? (m - 1) : m;
+  int sx = 0;
+  // One Psi step: publish x in X[sx&1], one barrier, read the neighbours' values.  The
+  // buffer written next was last read two steps ago, before the previous barrier.
+  auto psi_step = [&](double(&y)[P]) {
+    double *Xb = X + (sx & 1) * L::X;
+    psi_put_c<NT, P>(Xb, x);
+    __syncthreads();
+    psi_apply_any<P, NU>(Xb, tid * P, a.op, y);
+    ++sx;
+  };
 #pragma unroll 1
   for (int i = 1; i <= n1; ++i) {
-    __syncthreads();
-    psi_put_c<NT, P>(X, x);
-    __syncthreads();
     double y[P];
-    psi_apply_any<P, NU>(X, tid * P, a.op, y);
+    psi_step(y);
     const int kg = interp ? i : i - 1;
     const double *sg = slot(kg, origin(i));
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * P + p];
-    if (interp) {
-      double *add = a.v2.base ? slot(m + i, origin(i)) : nullptr;
-      double *buf = a.v2.base ? RB + (m + i) * WB : RB + kg * WB;
+    if (interp)  // out[jm+i] += x_i  (staged in place of the consumed g row)
       store(const_cast<double *>(a.out2.base) +
                 (a.out2.off + (long long)item * a.out2.stride + i) * nx,
-            origin(i), x, add, buf);
-    }
+            origin(i), x, true, RB + kg * WB);
   }
   if (!interp) {
-    store(const_cast<double *>(rowp(a.v, item)), origin(m), x, nullptr, RB);  // slot of g_1
+    store(const_cast<double *>(rowp(a.v, item)), origin(m), x, false, RB);  // slot of g_1
     if (p2) {
       if (a.ucmp.base) {
         const double *sc = slot(k_ucmp, origin(m));
@@ -474,12 +475,12 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
       }
 #pragma unroll 1
       for (int i = m + 1; i <= 2 * m; ++i) {
-        __syncthreads();
-        psi_put_c<NT, P>(X, x);
-        __syncthreads();
-        psi_apply_any<P, NU>(X, tid * P, a.op, x);
+        double y[P];
+        psi_step(y);
+#pragma unroll
+        for (int p = 0; p < P; ++p) x[p] = y[p];
       }
-      store(const_cast<double *>(rowp(a.r2, item)), origin(2 * m), x, nullptr,
+      store(const_cast<double *>(rowp(a.r2, item)), origin(2 * m), x, false,
             RB + (m >= 2 ? 1 : 0) * WB);  // slot of g_2
     }
   }
@@ -496,8 +497,7 @@ static cudaError_t launch_level_one(const PsiSweepArgs &a, cudaStream_t s) {
     attr = true;
   }
   const int m = a.m;
-  const int nrow = a.interp ? (1 + (m - 1) + (a.v2.base ? m : 0))
-                            : (m + (a.ucmp.base ? 1 : 0) + (a.u.base ? 1 : 0));
+  const int nrow = a.interp ? m : (m + (a.ucmp.base ? 1 : 0) + (a.u.base ? 1 : 0));
   const long long grid = (long long)a.nitems * a.ntiles;
   if (grid <= 0) return cudaSuccess;
   psi_level_kernel<NT, P, NU><<<(unsigned)grid, NT, L::bytes(nrow), s>>>(a);

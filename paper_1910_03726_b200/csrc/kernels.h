@@ -94,8 +94,9 @@ struct PsiSweepArgs {
   RowMap v;        // v_{j+1}
   RowMap r2;       // r_{j+2}
   int p2_items;
-  RowMap v2;       // interp: addend rows of level l-1 (row jm+i)
+  RowMap v2;       // interp: addend rows of level l-1 (row jm+i) (periodic kernel)
   RowMap out2;     // interp: output rows of level l-1 (row jm+i)
+  int accumulate;  // interp (TMA kernel): out2 += x (bulk reduce-add), v2 unused
   PsiOp op;
 };
 cudaError_t launch_psi_sweep(SweepCfg cfg, const PsiSweepArgs &a, cudaStream_t s);

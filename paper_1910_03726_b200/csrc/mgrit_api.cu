@@ -273,7 +273,7 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
     ntl /= m;  // nt at level l
     L.g[l] = take((ntl + 1) * row);
     if (l < levels - 1) {
-      L.vl[l] = take((ntl / m + 1) * row);
+      L.vl[l] = 0;
       L.ul[l] = take((ntl / m + 1) * row);
     } else {
       L.vl[l] = L.ul[l] = 0;
@@ -309,6 +309,7 @@ struct mgrit_ctx {
   char *ws;
   double *u0b, *v0b, *g[MGRIT_MAX_LEVELS], *vl[MGRIT_MAX_LEVELS], *ul[MGRIT_MAX_LEVELS];
   double *partials, *scal, *sa, *sb;
+  double *ucur, *unext;   // fine C-rows: current iterate / next (FCF ping-pong of u0b, v0b)
   const double *guess;
   bool have_iterate;   // u0b holds the iterate (after >= 1 iteration)
   std::string err;
@@ -587,7 +588,7 @@ int level_sweep(mgrit_ctx *c, int l) {
   a.u = kNone;
   a.ucmp = kNone;
   a.g = rm(c->g[l], 0, m);
-  a.v = rm(c->vl[l], 1, 1);
+  a.v = rm(c->ul[l], 1, 1);   // v_{j+1} is the uncorrected C-row; the coarse levels add E
   a.r2 = rm(c->g[l + 1], 2, 1);
   a.p2_items = (int)nc - 1;
   a.v2 = a.out2 = kNone;
@@ -596,9 +597,10 @@ int level_sweep(mgrit_ctx *c, int l) {
   return run(c, 1, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
 }
 
-// Level-l interpolation: from corrected C-rows u_l, F-relax with g_l and write
-// level l-1's corrected C-rows: out_{l-1}[n] = v_{l-1}[n] + U_l[n], n = 0..nt_l-1.
-int level_interp(mgrit_ctx *c, int l, RowMap v_prev, RowMap out_prev) {
+// Level-l interpolation: from corrected C-rows u_l, F-relax with g_l and add the level-l
+// values to level l-1's C-rows in place: out_{l-1}[n] += U_l[n], n = 0..nt_l (out_{l-1}
+// holds v_{l-1} written by the level-(l-1) sweep; P:212 correction fused).
+int level_interp(mgrit_ctx *c, int l, RowMap out_prev) {
   const PsiOp &op = c->op[l];
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
@@ -613,45 +615,42 @@ int level_interp(mgrit_ctx *c, int l, RowMap v_prev, RowMap out_prev) {
   a.ntiles = pc.ntiles;
   a.m = m;
   a.interp = 1;
+  a.accumulate = 1;
   a.u = rm(c->ul[l], 0, 1);
   a.ucmp = kNone;
   a.g = rm(c->g[l], 0, m);
   a.v = a.r2 = kNone;
-  a.v2 = RowMap{v_prev.base, v_prev.off, v_prev.stride * m};
   a.out2 = RowMap{out_prev.base, out_prev.off, out_prev.stride * m};
+  a.v2 = tma ? kNone : a.out2;   // periodic kernel: out = v2 + x with v2 == out (in place)
   a.op = op;
   int st = tma ? run(c, 3, [&] { return launch_psi_level_tma(pc.cfg, a, c->stream); })
                : run(c, 3, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
   if (st) return st;
-  // the last point n = nt_l (level l's last C-row): out[nt_l] = v[nt_l] + u_l[nc]
+  // the last point n = nt_l (level l's last C-row): out[nt_l] += u_l[nc]
   const long long ntl = c->ntl[l];
   double *dst = const_cast<double *>(out_prev.base) +
                 (out_prev.off + ntl * out_prev.stride) * (long long)c->nx;
-  const double *vsrc = v_prev.base + (v_prev.off + ntl * v_prev.stride) * (long long)c->nx;
   const double *usrc = c->ul[l] + nc * (long long)c->nx;
-  return run(c, 3, [&] { return mg_add_rows(dst, vsrc, usrc, c->nx, c->stream); });
+  return run(c, 3, [&] { return mg_add_rows(dst, dst, usrc, c->nx, c->stream); });
 }
 
-// C-point correction + V-cycle below level 0 after the fine sweep (g_1 = r).
-int coarse_correction(mgrit_ctx *c, RowMap v0map, RowMap out0map) {
+// Coarse-grid correction below level 0 after the fine sweep (g_1 = r): the fine C-rows
+// `out0` hold v and receive += E (two-level: the sequential solve; V-cycle: level
+// sweeps down, the sequential coarsest solve, interpolations up).
+int coarse_correction(mgrit_ctx *c, RowMap out0) {
   const int L = c->levels;
-  if (L == 2) return coarse_solve_level(c, 1, rm(v0map.base, v0map.off, v0map.stride),
-                                        rm(out0map.base, out0map.off, out0map.stride));
-  // down: levels 1..L-2 sweeps
+  if (L == 2) return coarse_solve_level(c, 1, out0, out0);
   for (int l = 1; l <= L - 2; ++l) {
     int st = level_sweep(c, l);
     if (st) return st;
   }
-  // coarsest: writes u_{L-2}[n] = v_{L-2}[n] + x_n, n = 1..nt_{L-1}
+  // coarsest: u_{L-2}[n] += x_n, n = 1..nt_{L-1}
   {
-    int st = coarse_solve_level(c, L - 1, rm(c->vl[L - 2], 0, 1), rm(c->ul[L - 2], 0, 1));
+    int st = coarse_solve_level(c, L - 1, rm(c->ul[L - 2], 0, 1), rm(c->ul[L - 2], 0, 1));
     if (st) return st;
   }
-  // up: level l interpolation writes level l-1's corrected C-rows
   for (int l = L - 2; l >= 1; --l) {
-    RowMap vprev = (l == 1) ? v0map : rm(c->vl[l - 1], 0, 1);
-    RowMap oprev = (l == 1) ? out0map : rm(c->ul[l - 1], 0, 1);
-    int st = level_interp(c, l, vprev, oprev);
+    int st = level_interp(c, l, (l == 1) ? out0 : rm(c->ul[l - 1], 0, 1));
     if (st) return st;
   }
   return MGRIT_OK;
@@ -774,9 +773,11 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
   c->v0b = (double *)(c->ws + c->lay.v0);
   for (int l = 1; l < levels; ++l) {
     c->g[l] = (double *)(c->ws + c->lay.g[l]);
-    c->vl[l] = (l < levels - 1) ? (double *)(c->ws + c->lay.vl[l]) : nullptr;
+    c->vl[l] = nullptr;
     c->ul[l] = (l < levels - 1) ? (double *)(c->ws + c->lay.ul[l]) : nullptr;
   }
+  c->ucur = c->u0b;
+  c->unext = c->v0b;
   c->partials = (double *)(c->ws + c->lay.partials);
   c->scal = (double *)(c->ws + c->lay.scal);
   c->sa = (double *)(c->ws + c->lay.sa);
@@ -788,7 +789,6 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
   for (int l = 1; l < levels; ++l) {
     cudaMemsetAsync(c->g[l], 0, 2 * row, c->stream);
     if (l < levels - 1) {
-      cudaMemsetAsync(c->vl[l], 0, row, c->stream);
       cudaMemsetAsync(c->ul[l], 0, row, c->stream);
     }
   }
@@ -938,6 +938,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   const bool fcf = c->relax == MGRIT_RELAX_FCF;
   int st;
   // row 0 of the C-row buffers = u0
+  c->ucur = c->u0b;
+  c->unext = c->v0b;
   cudaMemcpyAsync(c->u0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream);
   cudaMemcpyAsync(c->v0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream);
   // hist[0]: all-row residual of the guess
@@ -946,7 +948,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   if (st) return st;
   if (hist) hist[0] = r0;
   if (!fcf)  // Parareal: the coarse correction updates the C-rows in place (v = u)
-    cudaMemcpy2DAsync(c->u0b, row, c->guess, row * m, row, nc + 1, cudaMemcpyDeviceToDevice,
+    cudaMemcpy2DAsync(c->ucur, row, c->guess, row * m, row, nc + 1, cudaMemcpyDeviceToDevice,
                       c->stream);
   int k = 0;
   bool conv = r0 < tol;
@@ -954,6 +956,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   c->have_iterate = false;
   FineCfg f;
   if (!choose_fine(c, fcf ? 2 * m : m, f)) return fail(c, MGRIT_EUNSUPPORTED, "no sweep cfg");
+  // FCF sweep: reads the current C-rows (the guess's at k = 0), writes v into `unext`
+  // (the next iterate before its coarse correction), delta norm, r -> g_1.
   auto do_sweep = [&](bool first, bool want_norm) -> int {
     SweepArgs a = base_sweep(c);
     a.nitems = (int)nc;
@@ -962,12 +966,12 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       a.in = rm(c->guess, 0, m);
       a.cmp = rm(c->guess, m, m);
     } else {
-      a.in = rm(c->u0b, 0, 1);
-      a.cmp = rm(c->u0b, 1, 1);
+      a.in = rm(c->ucur, 0, 1);
+      a.cmp = rm(c->ucur, 1, 1);
     }
     a.partials = want_norm ? c->partials : nullptr;
     if (fcf) {
-      a.endw = rm(c->v0b, 1, 1);
+      a.endw = rm(c->unext, 1, 1);
       a.nsteps2 = m;
       a.p2_items = (int)nc - 1;
       a.r2 = rm(c->g[1], 2, 1);
@@ -976,21 +980,21 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       a.d_every = 1;
       a.d_phase = 0;
     }
-    if (!want_norm && !fcf) a.partials = nullptr;
     return sweep(c, 0, a, fcf ? 2 * m : m);
   };
   if (!conv && !nonfinite && max_iter > 0) {
     st = do_sweep(true, false);
     if (st) return st;
     while (true) {
-      // coarse-grid correction -> u0b
-      RowMap vmap = fcf ? rm(c->v0b, 0, 1) : rm(c->u0b, 0, 1);
-      st = coarse_correction(c, vmap, rm(c->u0b, 0, 1));
+      // coarse-grid correction: (FCF) unext += E, then unext becomes the iterate;
+      // (F) ucur += e in place
+      st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
       if (st) return st;
+      if (fcf) std::swap(c->ucur, c->unext);
       c->have_iterate = true;
       ++k;
       if (crows_hist)
-        cudaMemcpyAsync(crows_hist + (size_t)(k - 1) * (nc + 1) * nx, c->u0b, (nc + 1) * row,
+        cudaMemcpyAsync(crows_hist + (size_t)(k - 1) * (nc + 1) * nx, c->ucur, (nc + 1) * row,
                         cudaMemcpyDeviceToDevice, c->stream);
       // residual of iterate k (computed by the next sweep)
       st = do_sweep(false, true);
@@ -1014,14 +1018,14 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       SweepArgs a = base_sweep(c);
       a.nitems = (int)nc;
       a.nsteps1 = m - 1;
-      a.in = rm(c->u0b, 0, 1);
+      a.in = rm(c->ucur, 0, 1);
       a.each = rm(out_dev, 0, m);
       a.each_step = 1;
       a.each_first = 0;
       a.each_last = m - 1;
       st = sweep(c, 3, a, m - 1);
       if (st) return st;
-      cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->u0b + (size_t)nc * nx, row,
+      cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->ucur + (size_t)nc * nx, row,
                       cudaMemcpyDeviceToDevice, c->stream);
     }
   }
@@ -1037,7 +1041,7 @@ int mgrit_get_crows(mgrit_ctx *c, double *out_dev) {
   const long long nc = c->nt / c->m;
   const size_t row = (size_t)c->nx * sizeof(double);
   if (c->have_iterate)
-    cudaMemcpyAsync(out_dev, c->u0b, (nc + 1) * row, cudaMemcpyDeviceToDevice, c->stream);
+    cudaMemcpyAsync(out_dev, c->ucur, (nc + 1) * row, cudaMemcpyDeviceToDevice, c->stream);
   else
     cudaMemcpy2DAsync(out_dev, row, c->guess, row * c->m, row, nc + 1, cudaMemcpyDeviceToDevice, c->stream);
   return MGRIT_OK;

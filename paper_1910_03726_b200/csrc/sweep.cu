@@ -525,7 +525,7 @@ static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
 }
 
 #define MG_CFGS(X)                                                                          \
-  X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8) X(128, 11) X(256, 11)
+  X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8) X(128, 11) X(256, 11) X(128, 15)
 
 template <class SC>
 static cudaError_t dispatch_cfg(SweepCfg c, const SweepArgs &a, cudaStream_t s) {

@@ -48,6 +48,13 @@ __device__ __forceinline__ void tma_store_1d(void *dst_g, const void *src_s, uin
                "r"(smem_u32(src_s)), "r"(bytes)
                : "memory");
 }
+// shared -> global element-wise fp64 add at L2 (dst += src), bulk group tracked.
+__device__ __forceinline__ void tma_reduce_add_1d(void *dst_g, const void *src_s, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(
+                   dst_g),
+               "r"(smem_u32(src_s)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
