@@ -248,7 +248,7 @@ def run_ours(args, w):
                    "final_residual": res["history"][-1],
                    "parallelism": f"replicas{world}",
                    "l2": "inputs larger than L2 (8 GiB state vs 126 MB L2)"},
-        "roofline": {"bound": "alu", "kernel": "rk_sweep_kernel<ERK3U3,256,11> (fine FCF sweep)",
+        "roofline": {"bound": "alu", "kernel": s.describe() + " (fine FCF sweep)",
                      "achieved": round(achieved, 3), "peak": round(FP64_PEAK_TFLOPS, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
                      "peak_note": "FP64 pipe: 64 DFMA/clk/SM x 148 x 1.965 GHz (derived); "

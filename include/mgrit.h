@@ -181,6 +181,8 @@ int mgrit_fill_guess(double *dst_dev, long long row0, long long rows, int nx, ui
 #define MGRIT_PROF_CLASSES 6
 int mgrit_profile_enable(mgrit_ctx *ctx, int on);
 int mgrit_profile_read(mgrit_ctx *ctx, long long *launches, double *ms);
+/* Human-readable launch configuration of the fine sweep / level kernels (host-only). */
+int mgrit_describe(const mgrit_ctx *ctx, char *buf, size_t len);
 /* Total kernel launches since setup (or the last profile reset). */
 long long mgrit_launch_count(const mgrit_ctx *ctx);
 

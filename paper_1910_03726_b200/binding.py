@@ -66,6 +66,7 @@ _SIGS = [
     ("mgrit_profile_read", C.c_int, [C.c_void_p, C.POINTER(C.c_longlong),
                                      C.POINTER(C.c_double)]),
     ("mgrit_launch_count", C.c_longlong, [C.c_void_p]),
+    ("mgrit_describe", C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
 ]
 
 
@@ -259,3 +260,8 @@ class MGRIT:
 
     def launch_count(self) -> int:
         return lib().mgrit_launch_count(self.ctx)
+
+    def describe(self) -> str:
+        buf = C.create_string_buffer(256)
+        self._check(lib().mgrit_describe(self.ctx, buf, 256), "describe")
+        return buf.value.decode()

@@ -42,6 +42,7 @@ struct SweepArgs {
 struct SweepCfg {
   int nt_threads;  // NT
   int p;           // points per thread
+  int minb = 0;    // TMA kernel: __launch_bounds__ min blocks per SM (0 = default)
 };
 
 // scheme: 0 ERK1U1, 1 ERK2U2, 2 ERK3U3, 3 ERK4U4, 4 ERK5U5, 5 SDIRK1U1 .. 8 SDIRK4U4

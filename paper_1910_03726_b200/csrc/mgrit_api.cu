@@ -404,10 +404,12 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
   int HL = steps * S * rk_scheme_reach_left(c->scheme);
   HL += HL & 1;
   const int HR = steps * S * rk_scheme_reach_right(c->scheme);
-  int tcand[][2] = {{128, 15}, {256, 11}};
-  if (const char *env = getenv("MGRIT_FINE_TILE")) {  // experiments: "NT,P"
-    int nt_ = 0, p_ = 0;
-    if (sscanf(env, "%d,%d", &nt_, &p_) == 2) { tcand[0][0] = nt_; tcand[0][1] = p_; }
+  int tcand[][3] = {{128, 15, 0}, {256, 11, 0}};
+  if (const char *env = getenv("MGRIT_FINE_TILE")) {  // experiments: "NT,P[,minBlocks]"
+    int nt_ = 0, p_ = 0, mb_ = 0;
+    if (sscanf(env, "%d,%d,%d", &nt_, &p_, &mb_) >= 2) {
+      tcand[0][0] = nt_; tcand[0][1] = p_; tcand[0][2] = mb_;
+    }
   }
   for (auto &cc : tcand) {
     const int W = cc[0] * cc[1];
@@ -416,7 +418,7 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
     if (Tmax < 64) continue;
     int ntiles = (nx + Tmax - 1) / Tmax;
     while (2 * ((nx / 2 + ntiles - 1) / ntiles) + 1 > Tmax) ++ntiles;
-    f.cfg = {cc[0], cc[1]};
+    f.cfg = {cc[0], cc[1], cc[2]};
     f.ntiles = ntiles;
     f.HL = HL;
     return true;
@@ -1077,5 +1079,19 @@ int mgrit_profile_read(mgrit_ctx *c, long long *launches, double *ms) {
 }
 
 long long mgrit_launch_count(const mgrit_ctx *c) { return c ? c->launches : -1; }
+
+int mgrit_describe(const mgrit_ctx *c, char *buf, size_t len) {
+  if (!c || !buf || len == 0) return MGRIT_EINVAL;
+  FineCfg f;
+  const int m = c->m;
+  const bool ok = choose_fine(c, c->relax == MGRIT_RELAX_FCF ? 2 * m : m, f);
+  const bool tma = ok && f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1);
+  const char *kern = !ok ? "none" : (tma ? (f.cfg.nt_threads == 32 ? "rk_sweep_warp_kernel"
+                                                                    : "rk_sweep_tma_kernel")
+                                         : "rk_sweep_kernel");
+  snprintf(buf, len, "fine=%s<scheme%d,NT=%d,P=%d> tiles=%d halo=%d levels=%d", kern, c->scheme,
+           ok ? f.cfg.nt_threads : 0, ok ? f.cfg.p : 0, ok ? f.ntiles : 0, ok ? f.HL : 0, c->levels);
+  return MGRIT_OK;
+}
 
 }  // extern "C"

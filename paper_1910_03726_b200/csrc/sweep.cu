@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
 // every bulk copy is 16-byte aligned.  Modes: in/cmp/endw/dstore/r2/partials
 // (the production sweeps and the all-row residual) and per-step writes (each).
 // ---------------------------------------------------------------------------
-template <class SC, int NT, int P>
-__global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant__ SweepArgs a) {
+template <class SC, int NT, int P, int MINB>
+__global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_constant__ SweepArgs a) {
   static_assert(P % 2 == 1, "contiguous windows need odd P");
   constexpr int W = NT * P;
   constexpr int NW = NT / 32;
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(NT) rk_sweep_tma_kernel(const __grid_constant_
 #undef IN
 }
 
-template <class SC, int NT, int P>
+template <class SC, int NT, int P, int MINB>
 static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int W = NT * P;
   const size_t smem =
@@ -288,10 +288,10 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
       4 * sizeof(uint64_t) + 16;
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
-    cudaFuncSetAttribute(rk_sweep_tma_kernel<SC, NT, P>,
+    cudaFuncSetAttribute(rk_sweep_tma_kernel<SC, NT, P, MINB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
-                                                  rk_sweep_tma_kernel<SC, NT, P>, NT, smem);
+                                                  rk_sweep_tma_kernel<SC, NT, P, MINB>, NT, smem);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   int dev = 0, sms = 148;
@@ -300,7 +300,7 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   const long long total = (long long)a.nitems * a.ntiles;
   if (total <= 0) return cudaSuccess;
   const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
-  rk_sweep_tma_kernel<SC, NT, P><<<(unsigned)grid, NT, smem, s>>>(a);
+  rk_sweep_tma_kernel<SC, NT, P, MINB><<<(unsigned)grid, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -308,10 +308,14 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
 
 template <class SC>
 static cudaError_t dispatch_tma(SweepCfg c, const SweepArgs &a, cudaStream_t s) {
+// default: no min-blocks hint (ptxas picks 128 registers for 128x15 -> 4 CTAs/SM)
 #define MG_CASE(NT_, P_) \
-  if (c.nt_threads == NT_ && c.p == P_) return launch_tma_one<SC, NT_, P_>(a, s);
+  if (c.nt_threads == NT_ && c.p == P_ && c.minb == 0) \
+    return launch_tma_one<SC, NT_, P_, 0>(a, s);
   MG_TMA_CFGS(MG_CASE)
 #undef MG_CASE
+  if (c.nt_threads == 128 && c.p == 15 && c.minb == 3) return launch_tma_one<SC, 128, 15, 3>(a, s);
+  if (c.nt_threads == 128 && c.p == 15 && c.minb == 2) return launch_tma_one<SC, 128, 15, 2>(a, s);
   return cudaErrorInvalidConfiguration;
 }
 
