@@ -19,9 +19,10 @@ namespace mg {
 
 constexpr int PSI_EXT = MAX_PSI + 8;  // shared-memory tail for wrap/overrun reads
 
+// (g mod nx) for |g| < 2^31 (32-bit division; origins are computed once per step/item)
 __device__ __forceinline__ int wrapi(long long g, int nx) {
-  long long r = g % nx;
-  return (int)(r < 0 ? r + nx : r);
+  const int r = (int)g % nx;
+  return r < 0 ? r + nx : r;
 }
 
 // x'[p] = sum_q psi_q s[base + p + q]  (s holds the current state, unpadded).
@@ -72,73 +73,257 @@ template <int NT, int P> struct PsiSmem {
 };
 
 // --------------------------------------------------------------------------
-template <int NT, int P>
+// cp.async (LDGSTS) 8-byte copy global -> shared, per-thread groups.
+__device__ __forceinline__ void cp_async8(void *dst_s, const void *src_g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_s)), "l"(src_g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// fp64 add at L2, no return (fire-and-forget RED).
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// Sequential solve  x_n = Psi x_{n-1} + g_n,  out_n += x_n  (n = n0+1 .. n0+N).
+// The dependent chain runs in one CTA per (trapezoid) tile with no global latency inside a
+// step: g rows stream into a ring of R contiguous slots by TMA bulk copies issued R-1 steps
+// ahead (mbarrier per slot); each step applies Psi from the padded state buffer, then a
+// coalesced pass adds g_n and writes x_n both to the state (padded) and to a contiguous
+// staging slot, whose bulk reduce-add performs the C-point correction out_n += x_n at L2
+// (out holds v_n).  Two barriers per step, three staging slots, ping-pong state buffers.
+template <int NT, int P, int R>
+struct CoarseSmem {
+  static constexpr int W = NT * P;
+  static constexpr int X = PsiSmem<NT, P>::X;        // padded state + tail
+  static constexpr int WB = W + 2;                    // contiguous row slot (even)
+  static constexpr int TOTAL = 2 * X + R * WB + 3 * WB + 2 * R + 8;
+};
+
+template <int NT, int P, int R>
 __global__ void __launch_bounds__(NT) psi_coarse_kernel(const __grid_constant__ CoarseArgs a) {
-  constexpr int W = NT * P;
-  extern __shared__ double smem[];
-  constexpr int SP = Pad<P>::SP;
-  // ping-pong buffers: state (+ periodic tail) and g window; one barrier per step.  The
-  // state buffer of step i also serves the coalesced store of out_{i-1} = v + x_{i-1}.
-#define SX(b) (smem + (b) * PsiSmem<NT, P>::X)
-#define SG(b) (smem + 2 * PsiSmem<NT, P>::X + (b) * PsiSmem<NT, P>::G)
+  using CS = CoarseSmem<NT, P, R>;
+  constexpr int W = NT * P, WB = CS::WB;
+  extern __shared__ __align__(128) double smem[];
+#define SX(b) (smem + (b) * CS::X)
+#define GR(k) (smem + 2 * CS::X + (k) * WB)
+#define ST(k) (smem + 2 * CS::X + R * WB + (k) * WB)
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * CS::X + (R + 3) * WB);
   const int nx = a.nx, tid = threadIdx.x;
   const int tile = blockIdx.x;
   const int abeg = (int)(((long long)tile * nx) / a.ntiles);
   const int T = (int)(((long long)(tile + 1) * nx) / a.ntiles) - abeg;
   const int N = a.nsteps, o0 = a.op.o0;
-  // origin of step i: S_i = abeg + (N - i) * o0  (mod nx); S_N = abeg
+  const bool periodic = (a.ntiles == 1 && W == nx);
   auto origin = [&](int i) { return wrapi((long long)abeg + (long long)(N - i) * o0, nx); };
-  double x[P];
+  auto fetch = [&](int i) {  // (thread 0) g row of step i -> ring slot i % R
+    if (i > N) return;
+    const double *grow = a.g.base + (a.g.off + (a.n0 + i) * a.g.stride) * (long long)nx;
+    const int S0 = origin(i) & ~1;
+    const int n1 = (S0 + WB <= nx) ? WB : nx - S0;
+    uint64_t *b = &bar[i % R];
+    mbar_expect_tx(b, (uint32_t)WB * 8u);
+    tma_load_1d(GR(i % R), grow + S0, (uint32_t)n1 * 8u, b);
+    if (n1 < WB) tma_load_1d(GR(i % R) + n1, grow, (uint32_t)(WB - n1) * 8u, b);
+  };
+  if (tid == 0) {
+    for (int k = 0; k < R; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 1; i < R; ++i) fetch(i);
+  // x_0 into SX(0)
   if (a.state_in) {
     const int S0 = origin(0);
     for (int q = tid; q < W; q += NT) {
       int g = S0 + q;
       if (g >= nx) g -= nx;
-      SG(1)[pidx<P>(q)] = a.state_in[g];
+      const double v = a.state_in[g];
+      SX(0)[pidx<P>(q)] = v;
+      if (q < PSI_EXT) SX(0)[pidx<P>(W + q)] = v;
+    }
+  } else {
+    for (int q = tid; q < W + PSI_EXT; q += NT) SX(0)[pidx<P>(q)] = 0.0;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int i = 1; i <= N; ++i) {
+    const double *sprev = SX((i - 1) & 1);
+    double *scur = SX(i & 1);
+    double y[P];
+    psi_apply<P>(sprev, threadIdx.x * P, a.op, y);
+    psi_put<NT, P>(scur, y);
+    if (tid == 0) {
+      fetch(i + R - 1);  // slot (i-1) % R was consumed before the last barrier
+      if (i > 3) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // ST((i)%3) free
     }
     __syncthreads();
+    // coalesced pass: x_i = y + g_i  (state, tail, staging)
+    const int Si = origin(i);
+    mbar_wait(&bar[i % R], (uint32_t)(((i - 1) / R) & 1));
+    const double *gi = GR(i % R) + (Si & 1);
+    double *st = ST(i % 3) + (Si & 1);
+    for (int q = tid; q < W; q += NT) {
+      const int ix = pidx<P>(q);
+      const double v = scur[ix] + gi[q];
+      scur[ix] = v;
+      if (q < PSI_EXT) scur[pidx<P>(W + q)] = v;
+      if (q < T) st[q] = v;
+    }
+    if (periodic) {  // the tail mirrors the start of the row
+      // (entries W + q, q < PSI_EXT were written above from the same q)
+    }
+    fence_proxy_async();
+    __syncthreads();
+    // out_i[S_i .. S_i+T) += staging (bulk reduce-add; odd ends by scalar RMW)
+    double *orow = const_cast<double *>(a.out.base) + (a.out.off + (a.n0 + i) * a.out.stride) * (long long)nx;
+    const double *buf = ST(i % 3);
+    const int so = Si & 1;
+    int segs[2][2];
+    int ns = 1;
+    if (Si + T <= nx) { segs[0][0] = Si; segs[0][1] = Si + T; }
+    else { segs[0][0] = Si; segs[0][1] = nx; segs[1][0] = 0; segs[1][1] = Si + T - nx; ns = 2; }
+    int scalar = 0;
+    for (int k = 0; k < ns; ++k) {
+      int ga = segs[k][0], gb = segs[k][1];
+      const int base = so + (k == 0 ? -Si : nx - Si);
+      if (ga < gb && (ga & 1)) {
+        if (tid == 1 + scalar) orow[ga] += buf[base + ga];
+        ++scalar;
+        ++ga;
+      }
+      if (ga < gb && ((gb - ga) & 1)) {
+        if (tid == 1 + scalar) orow[gb - 1] += buf[base + gb - 1];
+        ++scalar;
+        --gb;
+      }
+      if (tid == 0 && gb > ga) tma_reduce_add_1d(orow + ga, buf + base + ga, (uint32_t)(gb - ga) * 8u);
+    }
+    if (tid == 0) bulk_commit();
+  }
+  if (a.state_out) {  // S_N = abeg: the owned slice [abeg, abeg+T)
+    const double *sN = SX(N & 1);
+    for (int q = tid; q < T; q += NT) a.state_out[abeg + q] = sN[pidx<P>(q)];
+  }
+  if (tid == 0) bulk_wait_all();
+#undef SX
+#undef GR
+#undef ST
+}
+
+// --------------------------------------------------------------------------
+// Periodic single-CTA sequential solve (two-level coarse grid), fixed
+// coordinates: thread t owns points [tP, tP+P) of the whole row (NT*P == nx).  Each
+// thread streams ITS OWN elements of g_n and of out_n (= v_n) D steps ahead into a
+// per-thread ring (cp.async, no cross-thread visibility needed), so the only barrier per
+// step is the one publishing x_n for the stencil.  Psi is applied at read base
+// (tP + o0) mod nx of the padded state, whose periodic tail mirrors its start.
+template <int NT, int P, int D>
+__global__ void __launch_bounds__(NT) psi_seq_periodic_kernel(const __grid_constant__ CoarseArgs a) {
+  constexpr int W = NT * P;
+  constexpr int SP = Pad<P>::SP;
+  using PS = PsiSmem<NT, P>;
+  extern __shared__ __align__(16) double smem[];
+  double *S0 = smem, *S1 = smem + PS::X;
+  double *ring = smem + 2 * PS::X;           // [D][2][NT*SP]: g and v slots (padded)
+  const int tid = threadIdx.x;
+  const int N = a.nsteps;
+  const int o0 = a.op.o0;
+  int rb = (tid * P + o0) % W;
+  if (rb < 0) rb += W;
+  const double *gbase = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)W;
+  double *obase = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)W;
+  const long long gst = a.g.stride * (long long)W, ost = a.out.stride * (long long)W;
+  auto fetch = [&](int i) {
+    if (i <= N) {
+      double *gs = ring + ((i % D) * 2) * (NT * SP) + tid * SP;
+      double *vs = gs + NT * SP;
+      const double *gr = gbase + i * gst + tid * P;
+      const double *vr = obase + i * ost + tid * P;
 #pragma unroll
-    for (int p = 0; p < P; ++p) x[p] = SG(1)[tid * SP + p];
+      for (int p = 0; p < P; ++p) {
+        cp_async8(gs + p, gr + p);
+        cp_async8(vs + p, vr + p);
+      }
+    }
+    cp_async_commit();
+  };
+  double x[P];
+  if (a.state_in) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = a.state_in[tid * P + p];
   } else {
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = 0.0;
   }
-  auto store_out = [&](long long n, int S, const double *sx) {
-    double *orow = const_cast<double *>(a.out.base) + (a.out.off + n * a.out.stride) * (long long)nx;
-    const double *vrow = a.v.base ? a.v.base + (a.v.off + n * a.v.stride) * (long long)nx : nullptr;
-    for (int q = tid; q < T; q += NT) {
-      int g = S + q;
-      if (g >= nx) g -= nx;
-      orow[g] = vrow ? vrow[g] + sx[pidx<P>(q)] : sx[pidx<P>(q)];
-    }
-  };
+  for (int i = 1; i < D; ++i) fetch(i);
+  psi_put<NT, P>(S0, x);
+  __syncthreads();
 #pragma unroll 1
-  for (int i = 1; i <= N + 1; ++i) {
-    double *sx = SX(i & 1), *sg = SG(i & 1);
-    psi_put<NT, P>(sx, x);                 // x_{i-1}
-    if (i <= N) {
-      const double *grow = a.g.base + (a.g.off + (a.n0 + i) * a.g.stride) * (long long)nx;
-      const int Si = origin(i);
-      for (int q = tid; q < W; q += NT) {
-        int g = Si + q;
-        if (g >= nx) g -= nx;
-        sg[pidx<P>(q)] = __ldg(grow + g);
-      }
-    }
-    __syncthreads();
-    if (i >= 2) store_out(a.n0 + i - 1, origin(i - 1), sx);
-    if (i > N) {
-      if (a.state_out)   // S_N = abeg: the owned slice [abeg, abeg+T)
-        for (int q = tid; q < T; q += NT) a.state_out[abeg + q] = sx[pidx<P>(q)];
-      break;
-    }
+  for (int i = 1; i <= N; ++i) {
+    fetch(i + D - 1);
+    const double *sprev = (i & 1) ? S0 : S1;
+    double *scur = (i & 1) ? S1 : S0;
     double y[P];
-    psi_apply<P>(sx, tid * P, a.op, y);
+    psi_apply<P>(sprev, rb, a.op, y);
+    cp_async_wait<D - 1>();                    // own g_i, v_i landed
+    const double *gs = ring + ((i % D) * 2) * (NT * SP) + tid * SP;
+    const double *vs = gs + NT * SP;
+    double *orow = obase + i * ost + tid * P;
 #pragma unroll
-    for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * SP + p];
+    for (int p = 0; p < P; ++p) {
+      x[p] = y[p] + gs[p];
+      orow[p] = vs[p] + x[p];                  // correction u_i = v_i + e_i
+    }
+    psi_put<NT, P>(scur, x);
+    __syncthreads();
   }
-#undef SX
-#undef SG
+  if (a.state_out) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) a.state_out[tid * P + p] = x[p];
+  }
+  cp_async_wait<0>();
+}
+
+template <int NT, int P, int D>
+constexpr size_t seq_smem() {
+  return sizeof(double) * (2 * PsiSmem<NT, P>::X + (size_t)D * 2 * NT * Pad<P>::SP);
+}
+
+template <int NT, int P, int D>
+static cudaError_t launch_seq_periodic_d(const CoarseArgs &a, cudaStream_t s) {
+  const size_t smem = seq_smem<NT, P, D>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(psi_seq_periodic_kernel<NT, P, D>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  psi_seq_periodic_kernel<NT, P, D><<<1, NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// prefetch depth: 8 steps when shared memory allows (rows <= 2048 points), else 4 or 2
+template <int NT, int P>
+static cudaError_t launch_seq_periodic(const CoarseArgs &a, cudaStream_t s) {
+  if constexpr (seq_smem<NT, P, 8>() <= 220 * 1024) return launch_seq_periodic_d<NT, P, 8>(a, s);
+  else if constexpr (seq_smem<NT, P, 4>() <= 220 * 1024) return launch_seq_periodic_d<NT, P, 4>(a, s);
+  else return launch_seq_periodic_d<NT, P, 2>(a, s);
+}
+
+cudaError_t launch_psi_seq_periodic(SweepCfg c, const CoarseArgs &a, cudaStream_t s) {
+  if (a.nsteps <= 0) return cudaSuccess;
+  if (c.nt_threads == 32 && c.p == 2) return launch_seq_periodic<32, 2>(a, s);
+  if (c.nt_threads == 32 && c.p == 4) return launch_seq_periodic<32, 4>(a, s);
+  if (c.nt_threads == 32 && c.p == 8) return launch_seq_periodic<32, 8>(a, s);
+  if (c.nt_threads == 64 && c.p == 8) return launch_seq_periodic<64, 8>(a, s);
+  if (c.nt_threads == 128 && c.p == 8) return launch_seq_periodic<128, 8>(a, s);
+  if (c.nt_threads == 256 && c.p == 8) return launch_seq_periodic<256, 8>(a, s);
+  if (c.nt_threads == 512 && c.p == 8) return launch_seq_periodic<512, 8>(a, s);
+  return cudaErrorInvalidConfiguration;
 }
 
 // --------------------------------------------------------------------------
@@ -585,17 +770,26 @@ __global__ void fill_guess_kernel(double *dst, long long row0, long long rows, i
 #define MG_PSI_CFGS(X) \
   X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8)
 
-template <int NT, int P>
-static cudaError_t launch_coarse_one(const CoarseArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * PsiSmem<NT, P>::TOTAL;
+template <int NT, int P, int R>
+static cudaError_t launch_coarse_ring(const CoarseArgs &a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * CoarseSmem<NT, P, R>::TOTAL;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(psi_coarse_kernel<NT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(psi_coarse_kernel<NT, P, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
-  psi_coarse_kernel<NT, P><<<a.ntiles, NT, smem, s>>>(a);
+  psi_coarse_kernel<NT, P, R><<<a.ntiles, NT, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+// ring depth: 8 slots where shared memory allows, else 4
+template <int NT, int P>
+static cudaError_t launch_coarse_one(const CoarseArgs &a, cudaStream_t s) {
+  if constexpr (sizeof(double) * CoarseSmem<NT, P, 8>::TOTAL <= 220 * 1024)
+    return launch_coarse_ring<NT, P, 8>(a, s);
+  else
+    return launch_coarse_ring<NT, P, 4>(a, s);
 }
 
 template <int NT, int P>

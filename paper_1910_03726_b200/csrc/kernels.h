@@ -67,19 +67,21 @@ struct PsiOp {
 };
 
 // Sequential (coarsest-level) solve over steps n0+1..n0+nsteps of
-//   x_n = Psi x_{n-1} + g_n,   out_n = v_n + x_n
+//   x_n = Psi x_{n-1} + g_n,   out_n += x_n      (out holds v_n)
 // in trapezoid tiles (no inter-CTA communication inside a launch).
 struct CoarseArgs {
   int nx, ntiles, nsteps;
   long long n0;
   RowMap g;        // g row n  (n = n0+i)
-  RowMap v;        // addend row n (base null: 0)
-  RowMap out;      // out row n
+  RowMap out;      // out row n (accumulated)
   const double *state_in;  // x_{n0} (nx), null: zero
   double *state_out;       // x_{n0+nsteps} (nx), null: not stored
   PsiOp op;
 };
 cudaError_t launch_psi_coarse(SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);
+// Periodic whole-row single-CTA variant (NT*P == nx), fixed coordinates, per-thread
+// cp.async streaming of g and out rows.
+cudaError_t launch_psi_seq_periodic(SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);
 
 // Level-l (l >= 2) relaxation sweep of the V-cycle with Psi_l and RHS g (u = 0 start):
 //   phase 1: x_i = Psi x_{i-1} + g[jm+i], i=1..m, x_0 = u_j (null: 0) -> v_{j+1}

@@ -522,7 +522,7 @@ int reduce_norm(mgrit_ctx *c, long long n, double *norm2_host) {
 }
 
 // Sequential coarse solve on level l (= levels-1, the coarsest) for steps 1..ntl:
-//   x_n = Psi x_{n-1} + g_n, out_n = v_n + x_n.
+//   x_n = Psi x_{n-1} + g_n, out_n = v_n + x_n  (stencil Psi: v == out, accumulated).
 int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
   const long long N = c->ntl[l];
   if (c->psi_kind != MGRIT_PSI_STENCIL) {
@@ -562,11 +562,12 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
   a.nsteps = (int)N;
   a.n0 = 0;
   a.g = rm(c->g[l], 0, 1);
-  a.v = v;
   a.out = out;
   a.state_in = nullptr;
   a.state_out = nullptr;
   a.op = op;
+  if (pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx)
+    return run(c, 2, [&] { return launch_psi_seq_periodic(pc.cfg, a, c->stream); });
   return run(c, 2, [&] { return launch_psi_coarse(pc.cfg, a, c->stream); });
 }
 
