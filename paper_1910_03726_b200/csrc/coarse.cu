@@ -216,41 +216,48 @@ __global__ void __launch_bounds__(NT) psi_coarse_kernel(const __grid_constant__ 
 
 // --------------------------------------------------------------------------
 // Periodic single-CTA sequential solve (two-level coarse grid), fixed
-// coordinates: thread t owns points [tP, tP+P) of the whole row (NT*P == nx).  Each
-// thread streams ITS OWN elements of g_n and of out_n (= v_n) D steps ahead into a
-// per-thread ring (cp.async, no cross-thread visibility needed), so the only barrier per
-// step is the one publishing x_n for the stencil.  Psi is applied at read base
-// (tP + o0) mod nx of the padded state, whose periodic tail mirrors its start.
+// coordinates: thread t owns points [tP, tP+P) of the whole row (NT*P == nx) for the
+// stencil, read at base (tP + o0) mod nx from the padded state whose periodic tail
+// mirrors its start.  The rows g_n and v_n (the uncorrected C-row) stream into a
+// ring of D contiguous slots by TMA bulk copies issued D-1 steps ahead; a coalesced pass
+// per step adds g_n into the state and writes u_n = v_n + x_n with coalesced stores.
+// Two barriers per step; no global latency inside the chain.
+template <int NT, int P, int D>
+struct SeqSmem {
+  static constexpr int W = NT * P;
+  static constexpr int X = PsiSmem<NT, P>::X;
+  static constexpr size_t BYTES = sizeof(double) * (2 * (size_t)X + 2 * (size_t)D * W) + 8 * D + 64;
+};
+
 template <int NT, int P, int D>
 __global__ void __launch_bounds__(NT) psi_seq_periodic_kernel(const __grid_constant__ CoarseArgs a) {
+  using SS = SeqSmem<NT, P, D>;
   constexpr int W = NT * P;
-  constexpr int SP = Pad<P>::SP;
-  using PS = PsiSmem<NT, P>;
-  extern __shared__ __align__(16) double smem[];
-  double *S0 = smem, *S1 = smem + PS::X;
-  double *ring = smem + 2 * PS::X;           // [D][2][NT*SP]: g and v slots (padded)
+  extern __shared__ __align__(128) double smem[];
+  double *S0 = smem, *S1 = smem + SS::X;
+  double *ring = smem + 2 * SS::X;                 // [D][2][W]: g, v (contiguous)
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ring + 2 * (size_t)D * W);
   const int tid = threadIdx.x;
   const int N = a.nsteps;
-  const int o0 = a.op.o0;
-  int rb = (tid * P + o0) % W;
+  int rb = (tid * P + a.op.o0) % W;
   if (rb < 0) rb += W;
   const double *gbase = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)W;
   double *obase = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)W;
   const long long gst = a.g.stride * (long long)W, ost = a.out.stride * (long long)W;
-  auto fetch = [&](int i) {
-    if (i <= N) {
-      double *gs = ring + ((i % D) * 2) * (NT * SP) + tid * SP;
-      double *vs = gs + NT * SP;
-      const double *gr = gbase + i * gst + tid * P;
-      const double *vr = obase + i * ost + tid * P;
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        cp_async8(gs + p, gr + p);
-        cp_async8(vs + p, vr + p);
-      }
-    }
-    cp_async_commit();
+  auto fetch = [&](int i) {  // thread 0: rows g_i, v_i -> slot i % D
+    if (i > N) return;
+    double *gs = ring + (size_t)(i % D) * 2 * W;
+    mbar_expect_tx(&bar[i % D], (uint32_t)(2 * W) * 8u);
+    tma_load_1d(gs, gbase + i * gst, (uint32_t)W * 8u, &bar[i % D]);
+    tma_load_1d(gs + W, obase + i * ost, (uint32_t)W * 8u, &bar[i % D]);
   };
+  if (tid == 0) {
+    for (int k = 0; k < D; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 1; i < D; ++i) fetch(i);
   double x[P];
   if (a.state_in) {
 #pragma unroll
@@ -259,43 +266,42 @@ __global__ void __launch_bounds__(NT) psi_seq_periodic_kernel(const __grid_const
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = 0.0;
   }
-  for (int i = 1; i < D; ++i) fetch(i);
   psi_put<NT, P>(S0, x);
   __syncthreads();
 #pragma unroll 1
   for (int i = 1; i <= N; ++i) {
-    fetch(i + D - 1);
     const double *sprev = (i & 1) ? S0 : S1;
     double *scur = (i & 1) ? S1 : S0;
     double y[P];
     psi_apply<P>(sprev, rb, a.op, y);
-    cp_async_wait<D - 1>();                    // own g_i, v_i landed
-    const double *gs = ring + ((i % D) * 2) * (NT * SP) + tid * SP;
-    const double *vs = gs + NT * SP;
-    double *orow = obase + i * ost + tid * P;
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      x[p] = y[p] + gs[p];
-      orow[p] = vs[p] + x[p];                  // correction u_i = v_i + e_i
+    for (int p = 0; p < P; ++p) scur[tid * Pad<P>::SP + p] = y[p];
+    if (tid == 0) fetch(i + D - 1);              // slot (i-1) % D was consumed last step
+    __syncthreads();
+    mbar_wait(&bar[i % D], (uint32_t)(((i - 1) / D) & 1));
+    const double *gs = ring + (size_t)(i % D) * 2 * W;
+    const double *vs = gs + W;
+    double *orow = obase + i * ost;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int q = tid + k * NT;
+      const int ix = pidx<P>(q);
+      const double xv = scur[ix] + gs[q];       // x_i = Psi x_{i-1} + g_i
+      scur[ix] = xv;
+      if (q < PSI_EXT) scur[pidx<P>(W + q)] = xv;
+      orow[q] = vs[q] + xv;                     // u_i = v_i + e_i
     }
-    psi_put<NT, P>(scur, x);
     __syncthreads();
   }
   if (a.state_out) {
-#pragma unroll
-    for (int p = 0; p < P; ++p) a.state_out[tid * P + p] = x[p];
+    const double *sN = (N & 1) ? S1 : S0;
+    for (int q = tid; q < W; q += NT) a.state_out[q] = sN[pidx<P>(q)];
   }
-  cp_async_wait<0>();
-}
-
-template <int NT, int P, int D>
-constexpr size_t seq_smem() {
-  return sizeof(double) * (2 * PsiSmem<NT, P>::X + (size_t)D * 2 * NT * Pad<P>::SP);
 }
 
 template <int NT, int P, int D>
 static cudaError_t launch_seq_periodic_d(const CoarseArgs &a, cudaStream_t s) {
-  const size_t smem = seq_smem<NT, P, D>();
+  const size_t smem = SeqSmem<NT, P, D>::BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(psi_seq_periodic_kernel<NT, P, D>,
@@ -306,11 +312,11 @@ static cudaError_t launch_seq_periodic_d(const CoarseArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// prefetch depth: 8 steps when shared memory allows (rows <= 2048 points), else 4 or 2
+// prefetch depth: up to 8 steps where shared memory allows
 template <int NT, int P>
 static cudaError_t launch_seq_periodic(const CoarseArgs &a, cudaStream_t s) {
-  if constexpr (seq_smem<NT, P, 8>() <= 220 * 1024) return launch_seq_periodic_d<NT, P, 8>(a, s);
-  else if constexpr (seq_smem<NT, P, 4>() <= 220 * 1024) return launch_seq_periodic_d<NT, P, 4>(a, s);
+  if constexpr (SeqSmem<NT, P, 8>::BYTES <= 220 * 1024) return launch_seq_periodic_d<NT, P, 8>(a, s);
+  else if constexpr (SeqSmem<NT, P, 4>::BYTES <= 220 * 1024) return launch_seq_periodic_d<NT, P, 4>(a, s);
   else return launch_seq_periodic_d<NT, P, 2>(a, s);
 }
 
@@ -323,6 +329,8 @@ cudaError_t launch_psi_seq_periodic(SweepCfg c, const CoarseArgs &a, cudaStream_
   if (c.nt_threads == 128 && c.p == 8) return launch_seq_periodic<128, 8>(a, s);
   if (c.nt_threads == 256 && c.p == 8) return launch_seq_periodic<256, 8>(a, s);
   if (c.nt_threads == 512 && c.p == 8) return launch_seq_periodic<512, 8>(a, s);
+  if (c.nt_threads == 1024 && c.p == 4) return launch_seq_periodic<1024, 4>(a, s);
+  if (c.nt_threads == 256 && c.p == 4) return launch_seq_periodic<256, 4>(a, s);
   return cudaErrorInvalidConfiguration;
 }
 

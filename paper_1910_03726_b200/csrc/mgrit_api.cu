@@ -566,8 +566,13 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
   a.state_in = nullptr;
   a.state_out = nullptr;
   a.op = op;
-  if (pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx)
-    return run(c, 2, [&] { return launch_psi_seq_periodic(pc.cfg, a, c->stream); });
+  if (pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx) {
+    SweepCfg sc = pc.cfg;  // more threads per row for the latency-bound chain
+    if (c->nx == 4096) sc = {1024, 4};
+    else if (c->nx == 1024) sc = {256, 4};
+    if (const char *env = getenv("MGRIT_SEQ_CFG")) sscanf(env, "%d,%d", &sc.nt_threads, &sc.p);
+    return run(c, 2, [&] { return launch_psi_seq_periodic(sc, a, c->stream); });
+  }
   return run(c, 2, [&] { return launch_psi_coarse(pc.cfg, a, c->stream); });
 }
 
