@@ -834,7 +834,7 @@ cudaError_t launch_psi_sweep(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s) 
 
 template <class SC>
 static cudaError_t launch_rkc(SweepCfg c, const RKCoarseArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (2 * (c.nt_threads / 32) * (SC::NL + SC::NR) + 4);
+  const size_t smem = sizeof(double) * (2 * c.nt_threads * (SC::NL + SC::NR) + 4);
   if (c.nt_threads == 32 && c.p == 2) {
     rk_coarse_kernel<SC, 32, 2><<<1, 32, smem, s>>>(a);
   } else if (c.nt_threads == 32 && c.p == 4) {

@@ -65,7 +65,7 @@ __device__ __forceinline__ void st_shared_pred(uint32_t addr, double v, bool pre
 
 // ---------------------------------------------------------------------------
 // Halo exchange: L[k] = y of point (t*P - NL + k), R[k] = y of point (t*P + P + k).
-// `edge` holds 2 * NW * (NL+NR) doubles; `phase` toggles the half in use.
+// `edge` holds 2 * NT * (NL+NR) doubles; `phase` toggles the half in use.
 // ---------------------------------------------------------------------------
 template <int NL, int NR, int P, int NT>
 __device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<NR> &R,
@@ -77,24 +77,24 @@ __device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<N
   for (int k = 0; k < NL; ++k) L.v[k] = __shfl_up_sync(FULL, y[P - NL + k], 1);
 #pragma unroll
   for (int k = 0; k < NR; ++k) R.v[k] = __shfl_down_sync(FULL, y[k], 1);
-  double *buf = edge + phase * (NW * E);
-  // predicated (not branched) edge stores: lane 31 publishes its tail, lane 0 its head
-  const uint32_t bw = smem_addr(buf + warp * E);
+  // Every lane publishes its tail and head into its own slot (no predicated or divergent
+  // stores, so no reconvergence point the deferred barrier could block on); lane 0 reads
+  // the previous warp's lane-31 tail, lane 31 the next warp's lane-0 head.
+  double *buf = edge + phase * (NW * 32 * E);
 #pragma unroll
-  for (int k = 0; k < NL; ++k) st_shared_pred(bw + 8u * k, y[P - NL + k], lane == 31);
+  for (int k = 0; k < NL; ++k) buf[(warp * 32 + lane) * E + k] = y[P - NL + k];
 #pragma unroll
-  for (int k = 0; k < NR; ++k) st_shared_pred(bw + 8u * (NL + k), y[k], lane == 0);
+  for (int k = 0; k < NR; ++k) buf[(warp * 32 + lane) * E + NL + k] = y[k];
   __syncthreads();
-  // every lane loads (broadcast address), the edge lanes select: no divergence
   const int pw = (warp + NW - 1) % NW, nw = (warp + 1) % NW;
 #pragma unroll
   for (int k = 0; k < NL; ++k) {
-    const double t = buf[pw * E + k];
+    const double t = buf[(pw * 32 + 31) * E + k];
     L.v[k] = (lane == 0) ? t : L.v[k];
   }
 #pragma unroll
   for (int k = 0; k < NR; ++k) {
-    const double t = buf[nw * E + NL + k];
+    const double t = buf[(nw * 32) * E + NL + k];
     R.v[k] = (lane == 31) ? t : R.v[k];
   }
   phase ^= 1;

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
   double *sA = smem;
   double *sB = sA + NT * SP;
   double *edge = sB + NT * SP;
-  double *red = edge + 2 * NW * (SC::NL + SC::NR) + 2;
+  double *red = edge + 2 * NT * (SC::NL + SC::NR) + 2;
   double *wbuf = red + NW + 2;  // 2*NW (SDIRK recurrences)
   int wphase = 0;
 
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
 #define IN(b) (smem + (b) * W)
   double *CM = smem + 2 * W;
   double *edge = smem + 3 * W;
-  double *red = edge + 2 * NW * (SC::NL + SC::NR) + 2;
+  double *red = edge + 2 * NT * (SC::NL + SC::NR) + 2;
   uint64_t *bar = reinterpret_cast<uint64_t *>(red + NW + 2);  // bar[0..1] in, bar[2] cmp
   const int tid = threadIdx.x;
   const int nx = a.nx;
@@ -284,7 +284,7 @@ template <class SC, int NT, int P, int MINB>
 static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int W = NT * P;
   const size_t smem =
-      sizeof(double) * (3 * W + 2 * (NT / 32) * (SC::NL + SC::NR) + 2 + NT / 32 + 2) +
+      sizeof(double) * (3 * W + 2 * NT * (SC::NL + SC::NR) + 2 + NT / 32 + 2) +
       4 * sizeof(uint64_t) + 16;
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
@@ -514,7 +514,7 @@ bool rk_scheme_implicit(int scheme) { return scheme >= 5 && scheme < 9; }
 template <class SC, int NT, int P>
 static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int SP = Pad<P>::SP;
-  const size_t smem = sizeof(double) * (2 * NT * SP + 2 * (NT / 32) * (SC::NL + SC::NR) + 2 +
+  const size_t smem = sizeof(double) * (2 * NT * SP + 2 * NT * (SC::NL + SC::NR) + 2 +
                                         NT / 32 + 2 + 2 * (NT / 32) + 2);
   static bool attr = false;
   if (!attr) {
