@@ -860,8 +860,30 @@ cudaError_t launch_rk_coarse(int scheme, SweepCfg c, const RKCoarseArgs &a, cuda
   }
 }
 
+// Deterministic two-pass sum: pass 1 sums fixed contiguous chunks (one block each), pass 2
+// sums the chunk results in order (same value for the same input, any launch timing).
+__global__ void __launch_bounds__(256) reduce_chunks_kernel(const double *__restrict__ p, long long n,
+                                                            long long chunk, double *part) {
+  __shared__ double red[8];
+  const long long b0 = blockIdx.x * chunk, b1 = b0 + chunk < n ? b0 + chunk : n;
+  double s = 0.0;
+  for (long long i = b0 + threadIdx.x; i < b1; i += 256) s += p[i];
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 cudaError_t launch_reduce(const double *partials, long long n, double *out, cudaStream_t s) {
-  reduce_kernel<<<1, 1024, 0, s>>>(partials, n, out);
+  constexpr long long kChunks = 512;
+  if (n <= 65536) {
+    reduce_kernel<<<1, 1024, 0, s>>>(partials, n, out);
+    return cudaGetLastError();
+  }
+  const long long chunk = (n + kChunks - 1) / kChunks;
+  // chunk sums go to out[1 .. kChunks] (the caller's scalar area holds >= 64 doubles;
+  // the partials buffer tail is used instead to stay in bounds)
+  double *tmp = const_cast<double *>(partials) + n;  // workspace reserves room after n
+  reduce_chunks_kernel<<<(unsigned)kChunks, 256, 0, s>>>(partials, n, chunk, tmp);
+  reduce_kernel<<<1, 1024, 0, s>>>(tmp, kChunks, out);
   return cudaGetLastError();
 }
 

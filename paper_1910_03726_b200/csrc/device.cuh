@@ -122,63 +122,6 @@ __device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
   }
 }
 
-// Warp-private variant: the window belongs to one warp, neighbours come only from
-// shuffles; lane 0 / lane 31 receive their own values (the wrap-around is garbage and
-// stays inside the discarded halo).  No shared memory, no barrier.
-template <int NL, int NR, int P>
-__device__ __forceinline__ void apply_Z_warp(const double (&y)[P], double (&k)[P],
-                                             const double *__restrict__ z) {
-  Arr<NL> L;
-  Arr<NR> R;
-#pragma unroll
-  for (int q = 0; q < NL; ++q) L.v[q] = __shfl_up_sync(FULL, y[P - NL + q], 1);
-#pragma unroll
-  for (int q = 0; q < NR; ++q) R.v[q] = __shfl_down_sync(FULL, y[q], 1);
-#pragma unroll
-  for (int p = 0; p < P; ++p) {
-    double acc = 0.0;
-#pragma unroll
-    for (int d = -NL; d <= NR; ++d) {
-      const int q = p + d;
-      const double v = (q < 0) ? L.v[(NL + q) < 0 ? 0 : (NL + q)]
-                               : (q >= P ? R.v[(q - P) < NR ? (q - P) : 0] : y[q < P ? q : 0]);
-      acc = (d == -NL) ? z[0] * v : fma(z[d + NL], v, acc);
-    }
-    k[p] = acc;
-  }
-}
-
-template <class SC, int P>
-__device__ __forceinline__ void erk_step_warp(double (&x)[P], const RKCoeffs &c) {
-  constexpr int S = SC::S;
-  double acc[S][P];
-  double out[P];
-#pragma unroll
-  for (int p = 0; p < P; ++p) {
-    out[p] = x[p];
-#pragma unroll
-    for (int i = 0; i < S; ++i) acc[i][p] = x[p];
-  }
-#pragma unroll
-  for (int i = 0; i < S; ++i) {
-    double k[P];
-    apply_Z_warp<SC::NL, SC::NR, P>(acc[i], k, c.z);
-#pragma unroll
-    for (int l = i + 1; l < S; ++l) {
-      if (SC::a_nz(l, i)) {
-#pragma unroll
-        for (int p = 0; p < P; ++p) acc[l][p] = fma(c.A[l][i], k[p], acc[l][p]);
-      }
-    }
-    if (SC::b_nz(i)) {
-#pragma unroll
-      for (int p = 0; p < P; ++p) out[p] = fma(c.b[i], k[p], out[p]);
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < P; ++p) x[p] = out[p];
-}
-
 // One explicit RK step in stage form (App. A):
 //   k_i = Z(x + sum_{l<i} a_il k_l),  x <- x + sum_i b_i k_i.
 // Partial stage sums are accumulated as soon as k_l is known (same summation

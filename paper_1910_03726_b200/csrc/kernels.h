@@ -51,8 +51,6 @@ bool rk_sweep_supported(int scheme, SweepCfg cfg);
 // Persistent TMA-pipelined sweep for halo-tile mode (odd P, even nx; no per-step writes).
 // Tile boundaries are 2*floor(t*(nx/2)/ntiles); HL must be even.
 cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s);
-// Warp-tile variant (each warp an independent worker, window 32*P, no CTA barriers).
-cudaError_t launch_rk_sweep_warp(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s);
 int rk_scheme_reach_left(int scheme);
 int rk_scheme_reach_right(int scheme);
 int rk_scheme_stages(int scheme);

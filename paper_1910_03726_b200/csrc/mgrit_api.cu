@@ -281,7 +281,7 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
   }
   // partials: largest sweep = all nt rows x up to 64 tiles
   L.npart = (long long)(nt + 1) * 64;
-  L.partials = take(L.npart * sizeof(double));
+  L.partials = take((L.npart + 1024) * sizeof(double));  // + room for the reduction chunks
   L.scal = take(64 * sizeof(double));
   L.sa = take(row);
   L.sb = take(row);
@@ -504,15 +504,26 @@ int sweep(mgrit_ctx *c, int cls, SweepArgs a, int total_steps) {
   // halo tiles, even nx, no per-step writes: persistent TMA-pipelined kernel
   const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1) && a.in.base &&
                    (a.each_last < a.each_first || !a.cmp.base);
-  if (tma && f.cfg.nt_threads == 32)
-    return run(c, cls, [&] { return launch_rk_sweep_warp(c->scheme, f.cfg, a, c->stream); });
+  if (a.partials && tma && (long long)a.nitems * a.ntiles * (f.cfg.nt_threads / 32) > c->lay.npart)
+    return fail(c, MGRIT_ENOMEM, "partials buffer too small");
   if (tma) return run(c, cls, [&] { return launch_rk_sweep_tma(c->scheme, f.cfg, a, c->stream); });
   return run(c, cls, [&] { return launch_rk_sweep(c->scheme, f.cfg, a, c->stream); });
+}
+
+// Number of norm partials a sweep of `items` items writes (per tile; the TMA kernel writes
+// one per warp).
+long long partial_count(const mgrit_ctx *c, long long items, int total_steps) {
+  FineCfg f;
+  if (!choose_fine(c, total_steps, f)) return 0;
+  const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1);
+  const int per = tma ? f.cfg.nt_threads / 32 : 1;
+  return items * f.ntiles * per;
 }
 
 int reduce_norm(mgrit_ctx *c, long long n, double *norm2_host) {
   int st = run(c, 5, [&] { return launch_reduce(c->partials, n, c->scal, c->stream); });
   if (st) return st;
+  if (n > 65536) c->launches++;  // two-pass reduction = two kernels
   if (norm2_host) {
     cudaError_t e = cudaMemcpyAsync(norm2_host, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -904,10 +915,8 @@ int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, 
   }
   int st = sweep(c, 4, a, 1);
   if (st) return st;
-  FineCfg f;
-  choose_fine(c, 1, f);
   double n2 = 0;
-  st = reduce_norm(c, (long long)c->nt * f.ntiles, norm_host ? &n2 : nullptr);
+  st = reduce_norm(c, partial_count(c, c->nt, 1), norm_host ? &n2 : nullptr);
   if (st) return st;
   if (norm_host) *norm_host = std::sqrt(c->dx * c->dt * n2);
   return MGRIT_OK;
@@ -1008,7 +1017,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       st = do_sweep(false, true);
       if (st) return st;
       double n2;
-      st = reduce_norm(c, nc * f.ntiles, &n2);
+      st = reduce_norm(c, partial_count(c, nc, fcf ? 2 * m : m), &n2);
       if (st) return st;
       const double rk = std::sqrt(c->dx * c->dt * n2);
       if (hist) hist[k] = rk;
@@ -1092,9 +1101,7 @@ int mgrit_describe(const mgrit_ctx *c, char *buf, size_t len) {
   const int m = c->m;
   const bool ok = choose_fine(c, c->relax == MGRIT_RELAX_FCF ? 2 * m : m, f);
   const bool tma = ok && f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1);
-  const char *kern = !ok ? "none" : (tma ? (f.cfg.nt_threads == 32 ? "rk_sweep_warp_kernel"
-                                                                    : "rk_sweep_tma_kernel")
-                                         : "rk_sweep_kernel");
+  const char *kern = !ok ? "none" : (tma ? "rk_sweep_tma_kernel" : "rk_sweep_kernel");
   snprintf(buf, len, "fine=%s<scheme%d,NT=%d,P=%d> tiles=%d halo=%d levels=%d", kern, c->scheme,
            ok ? f.cfg.nt_threads : 0, ok ? f.cfg.p : 0, ok ? f.ntiles : 0, ok ? f.HL : 0, c->levels);
   return MGRIT_OK;

@@ -180,9 +180,13 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
     tma_load_1d(CM, row + start, (uint32_t)n1 * 8u, &bar[2]);
     if (n1 < W) tma_load_1d(CM + n1, row, (uint32_t)(W - n1) * 8u, &bar[2]);
   };
-  // stage x into buf, then bulk-store the owned slice [HL, HL+T) to row[abeg..]
-  auto store = [&](double *row, double *buf, const double(&v)[P], int abeg, int T) {
-    __syncthreads();  // all threads are done reading buf
+  // stage x into buf, then bulk-store the owned slice [HL, HL+T) to row[abeg..].  The
+  // leading barrier is needed only when buf was read by other threads since the last
+  // barrier (per-step staging after thread 0's read-completion wait); the production
+  // stores stage into windows last read many barriers ago or in place.
+  auto store = [&](double *row, double *buf, const double(&v)[P], int abeg, int T,
+                   bool lead_barrier) {
+    if (lead_barrier) __syncthreads();
 #pragma unroll
     for (int p = 0; p < P; ++p) buf[tid * P + p] = v[p];
     fence_proxy_async();
@@ -235,17 +239,29 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
       double *row = const_cast<double *>(a.each.base) +
                     (a.each.off + (long long)item * a.each.stride + (long long)i * a.each_step) *
                         (long long)nx;
-      store(row, (nstage & 1) ? CM : IN(b), x, abeg, T);
+      store(row, (nstage & 1) ? CM : IN(b), x, abeg, T, true);
       ++nstage;
     };
+    // Step 1 is peeled so the thread-0 prefetch does not sit inside the step loop (a
+    // divergent region there costs a reconvergence point per step); per-step writes get
+    // their own loop for the same reason.
     if (a.each_first == 0 && a.each_last >= 0) each_store(0);
-#pragma unroll 1
-    for (int i = 1; i <= a.nsteps1; ++i) {
+    if (a.nsteps1 >= 1) {
       erk_step<SC, P, NT>(x, a.co, edge, phase);
-      if (!early && i == 1) issue_loads();
-      if (i >= a.each_first && i <= a.each_last) each_store(i);
+      if (!early) issue_loads();
+      if (1 >= a.each_first && 1 <= a.each_last) each_store(1);
     }
-    if (a.endw.base) store(const_cast<double *>(rowp(a.endw, item)), IN(b), x, abeg, T);
+    if (a.each_last >= a.each_first) {
+#pragma unroll 1
+      for (int i = 2; i <= a.nsteps1; ++i) {
+        erk_step<SC, P, NT>(x, a.co, edge, phase);
+        if (i >= a.each_first && i <= a.each_last) each_store(i);
+      }
+    } else {
+#pragma unroll 1
+      for (int i = 2; i <= a.nsteps1; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
+    }
+    if (a.endw.base) store(const_cast<double *>(rowp(a.endw, item)), IN(b), x, abeg, T, false);
     if (a.cmp.base) {
       mbar_wait(&bar[2], (uint32_t)(it & 1));
       double d[P];
@@ -258,23 +274,23 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
           const int l = tid * P + p;
           if (l >= a.HL && l < a.HL + T) sacc = fma(d[p], d[p], sacc);
         }
-        sacc = block_sum<NT>(sacc, red);
-        if (tid == 0) a.partials[(long long)item * a.ntiles + tile] = sacc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(FULL, sacc, o);
+        if ((tid & 31) == 0) a.partials[((long long)item * a.ntiles + tile) * NW + (tid >> 5)] = sacc;
       }
       if (a.dstore.base) {
         const int jj = item + a.d_phase;
         if (jj % a.d_every == 0)
-          store(const_cast<double *>(rowp(a.dstore, jj / a.d_every)), CM, d, abeg, T);
+          store(const_cast<double *>(rowp(a.dstore, jj / a.d_every)), CM, d, abeg, T, false);
       }
       if (a.nsteps2 > 0 && item < a.p2_items) {
 #pragma unroll
         for (int p = 0; p < P; ++p) x[p] = d[p];
 #pragma unroll 1
         for (int i = 1; i <= a.nsteps2; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
-        store(const_cast<double *>(rowp(a.r2, item)), CM, x, abeg, T);
+        store(const_cast<double *>(rowp(a.r2, item)), CM, x, abeg, T, false);
       }
     }
-    __syncthreads();  // buffers b may be reloaded two items from now
   }
   if (tid == 0) bulk_wait_all();
 #undef IN
@@ -326,168 +342,6 @@ cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cu
     case 2: return dispatch_tma<ERK3U3>(cfg, a, s);
     case 3: return dispatch_tma<ERK4U4>(cfg, a, s);
     case 4: return dispatch_tma<ERK5U5>(cfg, a, s);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-tile variant: every warp is an independent persistent worker over work items
-// (interval, tile) with its own 32*P-point window, TMA buffers and mbarriers.  The
-// stencil halo comes from shuffles only (no __syncthreads anywhere in the step loop);
-// the price is a per-warp halo (HL + HR points of W = 32*P).
-// ---------------------------------------------------------------------------
-template <class SC, int P, int WPC>
-__global__ void __launch_bounds__(32 * WPC) rk_sweep_warp_kernel(const __grid_constant__ SweepArgs a) {
-  static_assert(P % 2 == 1, "contiguous windows need odd P");
-  constexpr int W = 32 * P;
-  extern __shared__ __align__(128) double smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double *base = smem + (size_t)wid * (3 * W + 4);
-  double *IN0 = base, *IN1 = base + W, *CM = base + 2 * W;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(base + 3 * W);  // 3 mbarriers (+1 pad)
-  const int nx = a.nx;
-  const int total = a.nitems * a.ntiles;
-  const int half = nx >> 1;
-  const int gw = blockIdx.x * WPC + wid, nwarps = gridDim.x * WPC;
-  auto tile_beg = [&](int t) { return 2 * (int)(((long long)t * half) / a.ntiles); };
-  auto rowp = [&](const RowMap &r, long long j) -> const double * {
-    return r.base + (r.off + j * r.stride) * (long long)nx;
-  };
-  auto issue_row = [&](const double *row, int w, double *dst, uint64_t *b) {
-    int start = tile_beg(w % a.ntiles) - a.HL;
-    if (start < 0) start += nx;
-    const int n1 = (start + W <= nx) ? W : nx - start;
-    mbar_expect_tx(b, (uint32_t)W * 8u);
-    tma_load_1d(dst, row + start, (uint32_t)n1 * 8u, b);
-    if (n1 < W) tma_load_1d(dst + n1, row, (uint32_t)(W - n1) * 8u, b);
-  };
-  auto store = [&](double *row, double *buf, const double(&v)[P], int abeg, int T) {
-    __syncwarp();
-#pragma unroll
-    for (int p = 0; p < P; ++p) buf[lane * P + p] = v[p];
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_1d(row + abeg, buf + a.HL, (uint32_t)T * 8u);
-      bulk_commit();
-    }
-  };
-  if (lane == 0) {
-    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  if (lane == 0 && gw < total) issue_row(rowp(a.in, gw / a.ntiles), gw, IN0, &bar[0]);
-  int it = 0, nstage = 0;
-#pragma unroll 1
-  for (int w = gw; w < total; w += nwarps, ++it) {
-    const int b = it & 1;
-    double *INb = b ? IN1 : IN0, *INn = b ? IN0 : IN1;
-    const int nw = w + nwarps;
-    const int item = w / a.ntiles, tile = w - item * a.ntiles;
-    const int abeg = tile_beg(tile);
-    const int T = tile_beg(tile + 1) - abeg;
-    auto issue_loads = [&]() {
-      if (lane == 0) {
-        bulk_wait_read_all();
-        if (nw < total) issue_row(rowp(a.in, nw / a.ntiles), nw, INn, &bar[b ^ 1]);
-        if (a.cmp.base) issue_row(rowp(a.cmp, item), w, CM, &bar[2]);
-      }
-    };
-    const bool early = a.nsteps1 < 2;
-    if (early) issue_loads();
-    mbar_wait(&bar[b], (uint32_t)((it >> 1) & 1));
-    double x[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) x[p] = INb[lane * P + p];
-    auto each_store = [&](int i) {
-      if (lane == 0 && nstage >= 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      double *row = const_cast<double *>(a.each.base) +
-                    (a.each.off + (long long)item * a.each.stride + (long long)i * a.each_step) *
-                        (long long)nx;
-      store(row, (nstage & 1) ? CM : INb, x, abeg, T);
-      ++nstage;
-    };
-    if (a.each_first == 0 && a.each_last >= 0) each_store(0);
-#pragma unroll 1
-    for (int i = 1; i <= a.nsteps1; ++i) {
-      erk_step_warp<SC, P>(x, a.co);
-      if (!early && i == 1) issue_loads();
-      if (i >= a.each_first && i <= a.each_last) each_store(i);
-    }
-    if (a.endw.base) store(const_cast<double *>(rowp(a.endw, item)), INb, x, abeg, T);
-    if (a.cmp.base) {
-      mbar_wait(&bar[2], (uint32_t)(it & 1));
-      double d[P];
-#pragma unroll
-      for (int p = 0; p < P; ++p) d[p] = x[p] - CM[lane * P + p];
-      if (a.partials) {
-        double sacc = 0.0;
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const int l = lane * P + p;
-          if (l >= a.HL && l < a.HL + T) sacc = fma(d[p], d[p], sacc);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(FULL, sacc, o);
-        if (lane == 0) a.partials[(long long)item * a.ntiles + tile] = sacc;
-      }
-      if (a.dstore.base) {
-        const int jj = item + a.d_phase;
-        if (jj % a.d_every == 0)
-          store(const_cast<double *>(rowp(a.dstore, jj / a.d_every)), CM, d, abeg, T);
-      }
-      if (a.nsteps2 > 0 && item < a.p2_items) {
-#pragma unroll
-        for (int p = 0; p < P; ++p) x[p] = d[p];
-#pragma unroll 1
-        for (int i = 1; i <= a.nsteps2; ++i) erk_step_warp<SC, P>(x, a.co);
-        store(const_cast<double *>(rowp(a.r2, item)), CM, x, abeg, T);
-      }
-    }
-    __syncwarp();
-  }
-  if (lane == 0) bulk_wait_all();
-}
-
-template <class SC, int P, int WPC>
-static cudaError_t launch_warp_one(const SweepArgs &a, cudaStream_t s) {
-  constexpr int W = 32 * P;
-  const size_t smem = sizeof(double) * (size_t)WPC * (3 * W + 4) + 16;
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(rk_sweep_warp_kernel<SC, P, WPC>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rk_sweep_warp_kernel<SC, P, WPC>,
-                                                  32 * WPC, smem);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long total = (long long)a.nitems * a.ntiles;
-  if (total <= 0) return cudaSuccess;
-  long long grid = ((long long)sms * blocks_per_sm);
-  grid = std::min<long long>(grid, (total + WPC - 1) / WPC);
-  rk_sweep_warp_kernel<SC, P, WPC><<<(unsigned)grid, 32 * WPC, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
-// cfg.nt_threads == 32 selects the warp-tile kernel (WPC warps per CTA = 4).
-template <class SC>
-static cudaError_t dispatch_warp(SweepCfg c, const SweepArgs &a, cudaStream_t s) {
-  if (c.p == 15) return launch_warp_one<SC, 15, 4>(a, s);
-  if (c.p == 19) return launch_warp_one<SC, 19, 4>(a, s);
-  if (c.p == 23) return launch_warp_one<SC, 23, 2>(a, s);
-  return cudaErrorInvalidConfiguration;
-}
-
-cudaError_t launch_rk_sweep_warp(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s) {
-  switch (scheme) {
-    case 0: return dispatch_warp<ERK1U1>(cfg, a, s);
-    case 1: return dispatch_warp<ERK2U2>(cfg, a, s);
-    case 2: return dispatch_warp<ERK3U3>(cfg, a, s);
-    case 3: return dispatch_warp<ERK4U4>(cfg, a, s);
     default: return cudaErrorInvalidValue;
   }
 }
