@@ -51,6 +51,10 @@ bool rk_sweep_supported(int scheme, SweepCfg cfg);
 // Persistent TMA-pipelined sweep for halo-tile mode (odd P, even nx; no per-step writes).
 // Tile boundaries are 2*floor(t*(nx/2)/ntiles); HL must be even.
 cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s);
+// All-row residual of consecutive rows in.row(n-1) -> in.row(n), n = 1..a.nitems, in
+// (tile, chunk-of-rows) work items; one per-warp partial per item.
+cudaError_t launch_rk_residual_tma(int scheme, SweepCfg cfg, const SweepArgs &a, int chunk,
+                                   cudaStream_t s);
 int rk_scheme_reach_left(int scheme);
 int rk_scheme_reach_right(int scheme);
 int rk_scheme_stages(int scheme);

@@ -898,9 +898,34 @@ int mgrit_relax(mgrit_ctx *c, int level, int kind, double *U) {
   return st;
 }
 
+// Rows per work item of the streaming all-row residual kernel.
+constexpr int kResidualChunk = 64;
+
 int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, double *r_dev) {
   if (!c || !U) return MGRIT_EINVAL;
   if (level != 0) return fail(c, MGRIT_EUNSUPPORTED, "FULL primitives are level 0 only");
+  FineCfg f;
+  if (!r_dev && choose_fine(c, 1, f) && f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1)) {
+    // norm only: streaming kernel, every row loaded once
+    SweepArgs a = base_sweep(c);
+    a.nitems = c->nt;
+    a.in = rm(U, 0, 1);
+    a.ntiles = f.ntiles;
+    a.HL = f.HL;
+    a.partials = c->partials;
+    const long long np = (long long)((c->nt + kResidualChunk - 1) / kResidualChunk) * f.ntiles *
+                         (f.cfg.nt_threads / 32);
+    if (np > c->lay.npart) return fail(c, MGRIT_ENOMEM, "partials buffer too small");
+    int st = run(c, 4, [&] {
+      return launch_rk_residual_tma(c->scheme, f.cfg, a, kResidualChunk, c->stream);
+    });
+    if (st) return st;
+    double n2 = 0;
+    st = reduce_norm(c, np, norm_host ? &n2 : nullptr);
+    if (st) return st;
+    if (norm_host) *norm_host = std::sqrt(c->dx * c->dt * n2);
+    return MGRIT_OK;
+  }
   SweepArgs a = base_sweep(c);
   a.nitems = c->nt;
   a.nsteps1 = 1;

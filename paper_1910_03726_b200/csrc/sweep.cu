@@ -346,6 +346,125 @@ cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cu
   }
 }
 
+// ---------------------------------------------------------------------------
+// All-row residual r_n = Phi U[n-1] - U[n] (hist[0]) in halo tiles: a work item
+// is a (tile, chunk of consecutive rows); the CTA streams the chunk's rows through a
+// ring of three windows (TMA), so every row is loaded once and serves first as the
+// comparison row and then as the next input.  Per-warp partial sums of r^2.
+// ---------------------------------------------------------------------------
+template <class SC, int NT, int P>
+__global__ void __launch_bounds__(NT) rk_residual_tma_kernel(const __grid_constant__ SweepArgs a,
+                                                             int chunk) {
+  static_assert(P % 2 == 1, "contiguous windows need odd P");
+  constexpr int W = NT * P;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(128) double smem[];
+  double *edge = smem + 3 * W;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(edge + 2 * NT * (SC::NL + SC::NR) + 2);
+  const int tid = threadIdx.x;
+  const int nx = a.nx, half = nx >> 1;
+  const int nrows = a.nitems;                       // residual rows n = 1..nrows
+  const int nchunks = (nrows + chunk - 1) / chunk;
+  const int total = nchunks * a.ntiles;
+  auto tile_beg = [&](int t) { return 2 * (int)(((long long)t * half) / a.ntiles); };
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  unsigned parity = 0;  // bit s = parity of the next completion of ring slot s
+  int phase = 0;
+#pragma unroll 1
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const int tile = w % a.ntiles, ch = w / a.ntiles;
+    const int r0 = ch * chunk, r1 = min(nrows, r0 + chunk);  // residual rows r0+1 .. r1
+    const int abeg = tile_beg(tile), T = tile_beg(tile + 1) - abeg;
+    int start = abeg - a.HL;
+    if (start < 0) start += nx;
+    const int n1 = (start + W <= nx) ? W : nx - start;
+    auto issue = [&](int row, int slot) {  // thread 0: guess row `row` -> ring slot
+      const double *src = a.in.base + (a.in.off + (long long)row * a.in.stride) * (long long)nx;
+      double *dst = smem + slot * W;
+      mbar_expect_tx(&bar[slot], (uint32_t)W * 8u);
+      tma_load_1d(dst, src + start, (uint32_t)n1 * 8u, &bar[slot]);
+      if (n1 < W) tma_load_1d(dst + n1, src, (uint32_t)(W - n1) * 8u, &bar[slot]);
+    };
+    __syncthreads();  // previous item's readers are done with every slot
+    if (tid == 0) {
+      issue(r0, 0);
+      issue(r0 + 1, 1);
+    }
+    double sacc = 0.0;
+    int s_in = 0;
+#pragma unroll 1
+    for (int n = r0; n < r1; ++n) {
+      const int s_cmp = (s_in + 1) % 3, s_next = (s_in + 2) % 3;
+      mbar_wait(&bar[s_in], (parity >> s_in) & 1u);
+      double x[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) x[p] = smem[s_in * W + tid * P + p];
+      if (tid == 0 && n + 2 <= r1) issue(n + 2, s_next);   // slot s_next was read last row
+      erk_step<SC, P, NT>(x, a.co, edge, phase);
+      mbar_wait(&bar[s_cmp], (parity >> s_cmp) & 1u);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const double d = x[p] - smem[s_cmp * W + tid * P + p];
+        const int l = tid * P + p;
+        if (l >= a.HL && l < a.HL + T) sacc = fma(d, d, sacc);
+      }
+      parity ^= 1u << s_in;  // the input slot's completion is consumed
+      s_in = s_cmp;
+    }
+    parity ^= 1u << s_in;  // ... and the last comparison row's
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(FULL, sacc, o);
+    if ((tid & 31) == 0) a.partials[((long long)ch * a.ntiles + tile) * NW + (tid >> 5)] = sacc;
+  }
+}
+
+template <class SC, int NT, int P>
+static cudaError_t launch_residual_one(const SweepArgs &a, int chunk, cudaStream_t s) {
+  constexpr int W = NT * P;
+  const size_t smem = sizeof(double) * (3 * W + 2 * NT * (SC::NL + SC::NR) + 4) + 64;
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(rk_residual_tma_kernel<SC, NT, P>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rk_residual_tma_kernel<SC, NT, P>,
+                                                  NT, smem);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long total = (long long)((a.nitems + chunk - 1) / chunk) * a.ntiles;
+  if (total <= 0) return cudaSuccess;
+  const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
+  rk_residual_tma_kernel<SC, NT, P><<<(unsigned)grid, NT, smem, s>>>(a, chunk);
+  return cudaGetLastError();
+}
+
+template <class SC>
+static cudaError_t dispatch_residual(SweepCfg c, const SweepArgs &a, int chunk, cudaStream_t s) {
+#define MG_CASE(NT_, P_) \
+  if (c.nt_threads == NT_ && c.p == P_) return launch_residual_one<SC, NT_, P_>(a, chunk, s);
+  MG_TMA_CFGS(MG_CASE)
+#undef MG_CASE
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_rk_residual_tma(int scheme, SweepCfg cfg, const SweepArgs &a, int chunk,
+                                   cudaStream_t s) {
+  switch (scheme) {
+    case 0: return dispatch_residual<ERK1U1>(cfg, a, chunk, s);
+    case 1: return dispatch_residual<ERK2U2>(cfg, a, chunk, s);
+    case 2: return dispatch_residual<ERK3U3>(cfg, a, chunk, s);
+    case 3: return dispatch_residual<ERK4U4>(cfg, a, chunk, s);
+    case 4: return dispatch_residual<ERK5U5>(cfg, a, chunk, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <class SC> struct SchemeId;
 
 int rk_scheme_reach_left(int scheme) {

@@ -126,9 +126,12 @@ def test_residual_primitive(order, tab, cfl, nx, nt, m):
     dx, dt = 2.0 / nx, cfl * 2.0 / nx
     s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2,
                 [{"kind": "stencil", "offsets": [0], "coeffs": [0.5]}], "FCF")
-    ng, rg = s.residual_full(torch.from_numpy(U).cuda(), want_r=True)
+    Ug = torch.from_numpy(U).cuda()
+    ng, rg = s.residual_full(Ug, want_r=True)
     no = M.residual_norm(U, phi, dx, dt)
     assert abs(ng - no) <= 1e-13 * no
+    ng2 = s.residual_full(Ug)            # norm only: the streaming kernel in tile mode
+    assert abs(ng2 - no) <= 1e-13 * no
     ro = M.residual_rows(U, phi, np.arange(m, nt + 1, m))
     rg = rg.cpu().numpy()
     assert np.all(rg[0] == 0.0)
