@@ -15,6 +15,10 @@
 #include "kernels.h"
 #include "tma.cuh"
 
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 namespace mg {
 
 constexpr int PSI_EXT = MAX_PSI + 8;  // shared-memory tail for wrap/overrun reads
@@ -318,6 +322,141 @@ static cudaError_t launch_seq_periodic(const CoarseArgs &a, cudaStream_t s) {
   if constexpr (SeqSmem<NT, P, 8>::BYTES <= 220 * 1024) return launch_seq_periodic_d<NT, P, 8>(a, s);
   else if constexpr (SeqSmem<NT, P, 4>::BYTES <= 220 * 1024) return launch_seq_periodic_d<NT, P, 4>(a, s);
   else return launch_seq_periodic_d<NT, P, 2>(a, s);
+}
+
+// --------------------------------------------------------------------------
+// Cluster-wide periodic sequential solve (two-level coarse grid): the periodic
+// row is split over the CL CTAs of one thread-block cluster (CTA c owns [c*Wc, (c+1)*Wc),
+// Wc = NT*P), so a step's nu*nx FMAs run on CL SMs.  Per step: Psi from the CTA's padded
+// buffer (own values + left/right halos), x_n = Psi x_{n-1} + g_n, u_n = v_n + x_n
+// (P:212), publish own x_n, one cluster barrier, pull the halos from the neighbours'
+// shared memory (DSMEM), one CTA barrier.  g_n and v_n of the thread's own points are
+// prefetched D steps ahead into registers (loop unrolled by D).
+template <int NT, int P, int CL, int D>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
+    psi_seq_cluster_kernel(const __grid_constant__ CoarseArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int Wc = NT * P;
+  constexpr int SP = Pad<P>::SP;
+  constexpr int HMAX = 64;                         // max halo per side (host-checked)
+  constexpr int BL = ((HMAX + Wc + HMAX + PSI_EXT) / P + 2) * SP;  // padded buffer length
+  extern __shared__ __align__(16) double smem[];
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
+  const int N = a.nsteps, o0 = a.op.o0, nu = a.op.nu;
+  const int HL = o0 < 0 ? -o0 : 0;                 // left halo (points before the slice)
+  const int HR = (o0 + nu - 1) > 0 ? (o0 + nu - 1) : 0;
+  const int gx0 = rank * Wc + tid * P;             // global index of the thread's first point
+  const double *gb = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)a.nx + gx0;
+  double *ob = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)a.nx + gx0;
+  const long long gst = a.g.stride * (long long)a.nx, ost = a.out.stride * (long long)a.nx;
+  const int prev = (rank + CL - 1) % CL, next = (rank + 1) % CL;
+  // local index l (0 = first left-halo point) -> padded buffer slot
+  auto put_own = [&](double *buf, const double(&x)[P]) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) buf[pidx<P>(HMAX + tid * P + p)] = x[p];
+  };
+  auto pull_halo = [&](double *buf) {  // after the cluster barrier
+    if (tid < HL) {                    // left halo: previous CTA's last HL own points
+      const double *rb = cluster.map_shared_rank(buf, prev);
+      buf[pidx<P>(HMAX - HL + tid)] = rb[pidx<P>(HMAX + Wc - HL + tid)];
+    } else if (tid < HL + HR) {        // right halo: next CTA's first HR own points
+      const int k = tid - HL;
+      const double *rb = cluster.map_shared_rank(buf, next);
+      buf[pidx<P>(HMAX + Wc + k)] = rb[pidx<P>(HMAX + k)];
+    }
+  };
+  double x[P];
+  if (a.state_in) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = a.state_in[gx0 + p];
+  } else {
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = 0.0;
+  }
+  double *B0 = smem, *B1 = smem + BL;
+  put_own(B0, x);
+  cluster.sync();
+  pull_halo(B0);
+  __syncthreads();
+  double gq[D][P], vq[D][P];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    if (1 + d <= N) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        gq[d][p] = __ldg(gb + (1 + d) * gst + p);
+        vq[d][p] = ob[(1 + d) * ost + p];
+      }
+    }
+  }
+  int cur = 0;
+#pragma unroll 1
+  for (int i0 = 1; i0 <= N; i0 += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int i = i0 + d;
+      if (i <= N) {
+        const double *bc = cur ? B1 : B0;
+        double *bn = cur ? B0 : B1;
+        double y[P];
+        psi_apply<P>(bc, HMAX - HL + tid * P + (o0 + HL), a.op, y);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          x[p] = y[p] + gq[d][p];
+          ob[i * ost + p] = vq[d][p] + x[p];   // u_i = v_i + e_i
+        }
+        if (i + D <= N) {                      // refill this ring slot D steps ahead
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            gq[d][p] = __ldg(gb + (i + D) * gst + p);
+            vq[d][p] = ob[(i + D) * ost + p];
+          }
+        }
+        put_own(bn, x);
+        cluster.sync();
+        pull_halo(bn);
+        __syncthreads();
+        cur ^= 1;
+      }
+    }
+  }
+  if (a.state_out) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) a.state_out[gx0 + p] = x[p];
+  }
+  cluster.sync();  // no CTA exits while a neighbour may still read its shared memory
+}
+
+template <int NT, int P, int CL>
+static cudaError_t launch_seq_cluster(const CoarseArgs &a, cudaStream_t s) {
+  constexpr int Wc = NT * P;
+  constexpr int SP = Pad<P>::SP;
+  constexpr int BL = ((64 + Wc + 64 + PSI_EXT) / P + 2) * SP;
+  const size_t smem = sizeof(double) * 2 * BL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, 4>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (CL > 8)
+      cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, 4>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  psi_seq_cluster_kernel<NT, P, CL, 4><<<CL, NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// nx = CL * NT * P; the halos (-o0, o0+nu-1) must be <= 64 and <= NT*P (host-checked).
+cudaError_t launch_psi_seq_cluster(int cl, SweepCfg c, const CoarseArgs &a, cudaStream_t s) {
+  if (a.nsteps <= 0) return cudaSuccess;
+  if (cl == 8 && c.nt_threads == 128 && c.p == 4) return launch_seq_cluster<128, 4, 8>(a, s);
+  if (cl == 8 && c.nt_threads == 32 && c.p == 4) return launch_seq_cluster<32, 4, 8>(a, s);
+  if (cl == 16 && c.nt_threads == 64 && c.p == 4) return launch_seq_cluster<64, 4, 16>(a, s);
+  if (cl == 16 && c.nt_threads == 32 && c.p == 2) return launch_seq_cluster<32, 2, 16>(a, s);
+  if (cl == 8 && c.nt_threads == 64 && c.p == 2) return launch_seq_cluster<64, 2, 8>(a, s);
+  return cudaErrorInvalidConfiguration;
 }
 
 cudaError_t launch_psi_seq_periodic(SweepCfg c, const CoarseArgs &a, cudaStream_t s) {
@@ -697,9 +836,168 @@ static cudaError_t launch_level_one(const PsiSweepArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Persistent V-cycle level sweep (zero initial guess, no comparison row): the CTA walks
+// items with a grid stride and prefetches the next item's m g-rows into the other of two
+// row sets while the current item steps, so HBM streaming never waits on a CTA start.
+template <int NT, int P, int NU>
+__global__ void __launch_bounds__(NT) psi_level_persist_kernel(const __grid_constant__ PsiSweepArgs a) {
+  static_assert(P % 2 == 1, "contiguous windows need odd P");
+  using L = LevelSmem<NT, P>;
+  constexpr int W = L::W, WB = L::WB;
+  constexpr int MR = 4;                        // rows per set (m <= 4)
+  extern __shared__ __align__(128) double smem[];
+  double *X = smem;
+  double *RB = smem + 2 * L::X;                // [2][MR][WB]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(RB + 2 * MR * WB);
+  const int nx = a.nx, tid = threadIdx.x, m = a.m;
+  const int half = nx >> 1;
+  const int total = a.nitems * a.ntiles;
+  const int o0 = a.op.o0;
+  auto tile_beg = [&](int t) { return 2 * (int)(((long long)t * half) / a.ntiles); };
+  // origin of step i of an item: S_i = abeg + (N - i) o0 (mod nx), N = 2m (m if no phase 2)
+  auto origin = [&](int abeg, int N, int i) { return wrapi((long long)abeg + (long long)(N - i) * o0, nx); };
+  auto issue_item = [&](int w, int set) {      // thread 0: g rows jm+1..jm+m of item w
+    const int item = w / a.ntiles, tile = w - item * a.ntiles;
+    const int abeg = tile_beg(tile);
+    const int N = item < a.p2_items ? 2 * m : m;
+    const long long g0 = a.g.off + (long long)item * a.g.stride;
+    for (int k = 0; k < m; ++k) {
+      const double *row = a.g.base + (g0 + k + 1) * nx;
+      const int S0 = origin(abeg, N, k + 1) & ~1;
+      const int n1 = (S0 + WB <= nx) ? WB : nx - S0;
+      double *dst = RB + (set * MR + k) * WB;
+      uint64_t *b = &bar[set * MR + k];
+      mbar_expect_tx(b, (uint32_t)WB * 8u);
+      tma_load_1d(dst, row + S0, (uint32_t)n1 * 8u, b);
+      if (n1 < WB) tma_load_1d(dst + n1, row, (uint32_t)(WB - n1) * 8u, b);
+    }
+  };
+  if (tid == 0) {
+    for (int k = 0; k < 2 * MR; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && (int)blockIdx.x < total) issue_item(blockIdx.x, 0);
+  int sx = 0, it = 0;
+#pragma unroll 1
+  for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
+    const int set = it & 1;
+    const uint32_t par = (uint32_t)((it >> 1) & 1);
+    const int item = w / a.ntiles, tile = w - item * a.ntiles;
+    const int abeg = tile_beg(tile);
+    const int T = tile_beg(tile + 1) - abeg;
+    const bool p2 = item < a.p2_items;
+    const int N = p2 ? 2 * m : m;
+    __syncthreads();                           // item it-1's scalar stores read set^1
+    if (tid == 0) {
+      bulk_wait_read_all();                    // ... and its bulk stores have read it too
+      const int nw = w + gridDim.x;
+      if (nw < total) issue_item(nw, set ^ 1);
+    }
+    auto store = [&](double *row, int S, const double(&v)[P], double *buf) {
+      const int so = S & 1;
+      double *st = buf + so;
+#pragma unroll
+      for (int p = 0; p < P; ++p) st[tid * P + p] = v[p];
+      fence_proxy_async();
+      __syncthreads();
+      int segs[2][2];
+      int ns = 1;
+      if (S + T <= nx) { segs[0][0] = S; segs[0][1] = S + T; }
+      else { segs[0][0] = S; segs[0][1] = nx; segs[1][0] = 0; segs[1][1] = S + T - nx; ns = 2; }
+      int scalar = 0;
+      for (int k = 0; k < ns; ++k) {
+        int ga = segs[k][0], gb = segs[k][1];
+        const int base = so + (k == 0 ? -S : nx - S);
+        if (ga < gb && (ga & 1)) {
+          if (tid == 1 + scalar) row[ga] = buf[base + ga];
+          ++scalar;
+          ++ga;
+        }
+        if (ga < gb && ((gb - ga) & 1)) {
+          if (tid == 1 + scalar) row[gb - 1] = buf[base + gb - 1];
+          ++scalar;
+          --gb;
+        }
+        if (tid == 0 && gb > ga) tma_store_1d(row + ga, buf + base + ga, (uint32_t)(gb - ga) * 8u);
+      }
+      if (tid == 0) bulk_commit();
+    };
+    auto psi_step = [&](double(&y)[P], const double(&xin)[P]) {
+      double *Xb = X + (sx & 1) * L::X;
+      psi_put_c<NT, P>(Xb, xin);
+      __syncthreads();
+      psi_apply_any<P, NU>(Xb, tid * P, a.op, y);
+      ++sx;
+    };
+    double x[P];
+    // step 1 from the zero state: x_1 = g[jm+1]
+    {
+      mbar_wait(&bar[set * MR + 0], par);
+      const double *sg = RB + (set * MR + 0) * WB + (origin(abeg, N, 1) & 1);
+#pragma unroll
+      for (int p = 0; p < P; ++p) x[p] = 0.0 + sg[tid * P + p];
+    }
+#pragma unroll 1
+    for (int i = 2; i <= m; ++i) {
+      double y[P];
+      psi_step(y, x);
+      mbar_wait(&bar[set * MR + i - 1], par);
+      const double *sg = RB + (set * MR + i - 1) * WB + (origin(abeg, N, i) & 1);
+#pragma unroll
+      for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * P + p];
+    }
+    store(const_cast<double *>(a.v.base) + (a.v.off + (long long)item * a.v.stride) * nx,
+          origin(abeg, N, m), x, RB + (set * MR + 0) * WB);   // v_{j+1} (slot of g_1)
+    if (p2) {
+#pragma unroll 1
+      for (int i = m + 1; i <= 2 * m; ++i) {
+        double y[P];
+        psi_step(y, x);
+#pragma unroll
+        for (int p = 0; p < P; ++p) x[p] = y[p];
+      }
+      store(const_cast<double *>(a.r2.base) + (a.r2.off + (long long)item * a.r2.stride) * nx,
+            origin(abeg, N, 2 * m), x, RB + (set * MR + 1) * WB);  // r_{j+2} (slot of g_2)
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+template <int NT, int P, int NU>
+static cudaError_t launch_level_persist_one(const PsiSweepArgs &a, cudaStream_t s) {
+  using L = LevelSmem<NT, P>;
+  const size_t smem = sizeof(double) * (2 * L::X + 2 * 4 * (size_t)L::WB + 16) + 64;
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(psi_level_persist_kernel<NT, P, NU>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, psi_level_persist_kernel<NT, P, NU>,
+                                                  NT, smem);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long total = (long long)a.nitems * a.ntiles;
+  if (total <= 0) return cudaSuccess;
+  const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
+  psi_level_persist_kernel<NT, P, NU><<<(unsigned)grid, NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_psi_level_tma(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s) {
   if (a.m > 4 || (a.nx & 1)) return cudaErrorInvalidValue;
   if (c.nt_threads != 128 || c.p != 9) return cudaErrorInvalidConfiguration;
+  if (!a.interp && !a.u.base && !a.ucmp.base) {  // coarse-level sweep: persistent variant
+    switch (a.op.nu) {
+      case 9: return launch_level_persist_one<128, 9, 9>(a, s);
+      case 13: return launch_level_persist_one<128, 9, 13>(a, s);
+      case 17: return launch_level_persist_one<128, 9, 17>(a, s);
+      case 21: return launch_level_persist_one<128, 9, 21>(a, s);
+      default: return launch_level_persist_one<128, 9, 0>(a, s);
+    }
+  }
   switch (a.op.nu) {
     case 9: return launch_level_one<128, 9, 9>(a, s);
     case 13: return launch_level_one<128, 9, 13>(a, s);
