@@ -327,20 +327,33 @@ static cudaError_t launch_seq_periodic(const CoarseArgs &a, cudaStream_t s) {
 // --------------------------------------------------------------------------
 // Cluster-wide periodic sequential solve (two-level coarse grid): the periodic
 // row is split over the CL CTAs of one thread-block cluster (CTA c owns [c*Wc, (c+1)*Wc),
-// Wc = NT*P), so a step's nu*nx FMAs run on CL SMs.  Per step: Psi from the CTA's padded
-// buffer (own values + left/right halos), x_n = Psi x_{n-1} + g_n, u_n = v_n + x_n
-// (P:212), publish own x_n, one cluster barrier, pull the halos from the neighbours'
-// shared memory (DSMEM), one CTA barrier.  g_n and v_n of the thread's own points are
-// prefetched D steps ahead into registers (loop unrolled by D).
+// Wc = NT*P), so a step's nu*nx FMAs run on CL SMs.  Per step i: Psi from the CTA's
+// buffer bc (own values + left/right halos), x_i = Psi x_{i-1} + g_i, u_i = v_i + x_i
+// (P:212); own x_i goes to the local buffer bn, the boundary values are pushed into the
+// neighbours' bn halos (DSMEM stores), then one split cluster barrier (arrive.release,
+// output store + prefetch, wait.acquire).  bn of step i is bc of step i-1, whose last
+// reader passed the previous cluster barrier, so one barrier per step suffices.
+// g_i and v_i of the thread's own points are prefetched D steps ahead into registers.
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NT, int P> struct ClusterSmem {
+  static constexpr int HMAX = 64;  // max halo per side (host-checked)
+  static constexpr int BL = ((HMAX + NT * P + HMAX + PSI_EXT) / P + 2) * Pad<P>::SP;
+  static constexpr size_t BYTES = sizeof(double) * 2 * BL;
+};
+
 template <int NT, int P, int CL, int D>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     psi_seq_cluster_kernel(const __grid_constant__ CoarseArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  constexpr int Wc = NT * P;
-  constexpr int SP = Pad<P>::SP;
-  constexpr int HMAX = 64;                         // max halo per side (host-checked)
-  constexpr int BL = ((HMAX + Wc + HMAX + PSI_EXT) / P + 2) * SP;  // padded buffer length
+  using CS = ClusterSmem<NT, P>;
+  constexpr int Wc = NT * P, HMAX = CS::HMAX, BL = CS::BL;
   extern __shared__ __align__(16) double smem[];
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x;
@@ -351,22 +364,24 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
   const double *gb = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)a.nx + gx0;
   double *ob = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)a.nx + gx0;
   const long long gst = a.g.stride * (long long)a.nx, ost = a.out.stride * (long long)a.nx;
-  const int prev = (rank + CL - 1) % CL, next = (rank + 1) % CL;
-  // local index l (0 = first left-halo point) -> padded buffer slot
-  auto put_own = [&](double *buf, const double(&x)[P]) {
+  double *B[2] = {smem, smem + BL};
+  double *Bp[2], *Bn[2];                           // neighbours' buffers (DSMEM)
 #pragma unroll
-    for (int p = 0; p < P; ++p) buf[pidx<P>(HMAX + tid * P + p)] = x[p];
-  };
-  auto pull_halo = [&](double *buf) {  // after the cluster barrier
-    if (tid < HL) {                    // left halo: previous CTA's last HL own points
-      const double *rb = cluster.map_shared_rank(buf, prev);
-      buf[pidx<P>(HMAX - HL + tid)] = rb[pidx<P>(HMAX + Wc - HL + tid)];
-    } else if (tid < HL + HR) {        // right halo: next CTA's first HR own points
-      const int k = tid - HL;
-      const double *rb = cluster.map_shared_rank(buf, next);
-      buf[pidx<P>(HMAX + Wc + k)] = rb[pidx<P>(HMAX + k)];
+  for (int k = 0; k < 2; ++k) {
+    Bp[k] = cluster.map_shared_rank(B[k], (rank + CL - 1) % CL);
+    Bn[k] = cluster.map_shared_rank(B[k], (rank + 1) % CL);
+  }
+  // local buffer index: HMAX + l for own point l; l < 0 left halo, l >= Wc right halo
+  auto publish = [&](int k, const double(&x)[P]) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int l = tid * P + p;
+      B[k][pidx<P>(HMAX + l)] = x[p];
+      if (l < HR) Bp[k][pidx<P>(HMAX + Wc + l)] = x[p];          // prev's right halo
+      if (l >= Wc - HL) Bn[k][pidx<P>(HMAX + l - Wc)] = x[p];    // next's left halo
     }
   };
+  for (int q = tid; q < 2 * BL; q += NT) smem[q] = 0.0;  // over-read slots stay finite
   double x[P];
   if (a.state_in) {
 #pragma unroll
@@ -375,11 +390,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = 0.0;
   }
-  double *B0 = smem, *B1 = smem + BL;
-  put_own(B0, x);
-  cluster.sync();
-  pull_halo(B0);
-  __syncthreads();
+  cluster.sync();  // every CTA zeroed before any remote store lands
+  publish(0, x);
   double gq[D][P], vq[D][P];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
@@ -391,22 +403,23 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       }
     }
   }
-  int cur = 0;
+  cluster_arrive();
+  cluster_wait();
+  const int base = HMAX + tid * P + o0;
 #pragma unroll 1
   for (int i0 = 1; i0 <= N; i0 += D) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const int i = i0 + d;
       if (i <= N) {
-        const double *bc = cur ? B1 : B0;
-        double *bn = cur ? B0 : B1;
         double y[P];
-        psi_apply<P>(bc, HMAX - HL + tid * P + (o0 + HL), a.op, y);
+        psi_apply<P>(B[(i - 1) & 1], base, a.op, y);
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          x[p] = y[p] + gq[d][p];
-          ob[i * ost + p] = vq[d][p] + x[p];   // u_i = v_i + e_i
-        }
+        for (int p = 0; p < P; ++p) x[p] = y[p] + gq[d][p];
+        publish(i & 1, x);
+        cluster_arrive();
+#pragma unroll
+        for (int p = 0; p < P; ++p) ob[i * ost + p] = vq[d][p] + x[p];  // u_i = v_i + e_i
         if (i + D <= N) {                      // refill this ring slot D steps ahead
 #pragma unroll
           for (int p = 0; p < P; ++p) {
@@ -414,11 +427,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
             vq[d][p] = ob[(i + D) * ost + p];
           }
         }
-        put_own(bn, x);
-        cluster.sync();
-        pull_halo(bn);
-        __syncthreads();
-        cur ^= 1;
+        cluster_wait();
       }
     }
   }
@@ -426,15 +435,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
 #pragma unroll
     for (int p = 0; p < P; ++p) a.state_out[gx0 + p] = x[p];
   }
-  cluster.sync();  // no CTA exits while a neighbour may still read its shared memory
 }
 
 template <int NT, int P, int CL>
 static cudaError_t launch_seq_cluster(const CoarseArgs &a, cudaStream_t s) {
-  constexpr int Wc = NT * P;
-  constexpr int SP = Pad<P>::SP;
-  constexpr int BL = ((64 + Wc + 64 + PSI_EXT) / P + 2) * SP;
-  const size_t smem = sizeof(double) * 2 * BL;
+  const size_t smem = ClusterSmem<NT, P>::BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, 4>,

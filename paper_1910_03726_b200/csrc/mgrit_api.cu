@@ -578,6 +578,19 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
   a.state_out = nullptr;
   a.op = op;
   if (pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx) {
+    // Thread-block cluster: the row split over CL SMs (DSMEM halos).
+    int cl = 0;
+    SweepCfg cc = {0, 0};
+    if (c->nx == 4096) { cl = 8; cc = {128, 4}; }
+    else if (c->nx == 1024) { cl = 8; cc = {32, 4}; }
+    if (const char *env = getenv("MGRIT_SEQ_CLUSTER")) {
+      cl = 0;
+      sscanf(env, "%d,%d,%d", &cl, &cc.nt_threads, &cc.p);
+    }
+    const int hl = std::max(0, -op.o0), hr = std::max(0, op.o0 + op.nu - 1);
+    if (cl > 1 && cl * cc.nt_threads * cc.p == c->nx && hl <= 64 && hr <= 64 &&
+        hl <= cc.nt_threads * cc.p && hr <= cc.nt_threads * cc.p)
+      return run(c, 2, [&] { return launch_psi_seq_cluster(cl, cc, a, c->stream); });
     SweepCfg sc = pc.cfg;  // more threads per row for the latency-bound chain
     if (c->nx == 4096) sc = {1024, 4};
     else if (c->nx == 1024) sc = {256, 4};
