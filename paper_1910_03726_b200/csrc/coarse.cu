@@ -341,28 +341,41 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int NT, int P> struct ClusterSmem {
+template <int NT, int P, int D> struct ClusterSmem {
   static constexpr int HMAX = 64;  // max halo per side (host-checked)
-  static constexpr int BL = ((HMAX + NT * P + HMAX + PSI_EXT) / P + 2) * Pad<P>::SP;
-  static constexpr size_t BYTES = sizeof(double) * 2 * BL;
+  static constexpr int Wc = NT * P;
+  static constexpr int BL = ((HMAX + Wc + HMAX + PSI_EXT) / P + 2) * Pad<P>::SP;
+  static constexpr int NSTAGE = 3;                  // output staging rows
+  // doubles: 2 state buffers | D x (g, v) slices | NSTAGE output slices | D mbarriers
+  static constexpr size_t RING = 2 * (size_t)BL;
+  static constexpr size_t STAGE = RING + 2 * (size_t)D * Wc;
+  static constexpr size_t BAR = STAGE + (size_t)NSTAGE * Wc;
+  static constexpr size_t BYTES = sizeof(double) * BAR + 8 * D;
 };
 
+// Global memory is touched only by the async proxy (TMA bulk loads of g_i / v_i into a
+// D-deep ring, bulk stores of u_i from a 3-deep staging ring, both issued by thread 0),
+// so the cluster barrier's release orders nothing but the shared-memory state.
 template <int NT, int P, int CL, int D>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     psi_seq_cluster_kernel(const __grid_constant__ CoarseArgs a) {
+  static_assert(P % 2 == 0, "P even (16-byte vector staging)");
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  using CS = ClusterSmem<NT, P>;
-  constexpr int Wc = NT * P, HMAX = CS::HMAX, BL = CS::BL;
-  extern __shared__ __align__(16) double smem[];
+  using CS = ClusterSmem<NT, P, D>;
+  constexpr int Wc = CS::Wc, HMAX = CS::HMAX, BL = CS::BL;
+  extern __shared__ __align__(128) double smem[];
+  double *ring = smem + CS::RING;                  // slot k: g at k*2Wc, v at k*2Wc + Wc
+  double *stage = smem + CS::STAGE;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + CS::BAR);
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x;
   const int N = a.nsteps, o0 = a.op.o0, nu = a.op.nu;
   const int HL = o0 < 0 ? -o0 : 0;                 // left halo (points before the slice)
   const int HR = (o0 + nu - 1) > 0 ? (o0 + nu - 1) : 0;
   const int gx0 = rank * Wc + tid * P;             // global index of the thread's first point
-  const double *gb = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)a.nx + gx0;
-  double *ob = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)a.nx + gx0;
+  const double *gb = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)a.nx + rank * Wc;
+  double *ob = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)a.nx + rank * Wc;
   const long long gst = a.g.stride * (long long)a.nx, ost = a.out.stride * (long long)a.nx;
   double *B[2] = {smem, smem + BL};
   double *Bp[2], *Bn[2];                           // neighbours' buffers (DSMEM)
@@ -371,6 +384,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     Bp[k] = cluster.map_shared_rank(B[k], (rank + CL - 1) % CL);
     Bn[k] = cluster.map_shared_rank(B[k], (rank + 1) % CL);
   }
+  auto fetch = [&](int i) {  // thread 0: g_i, v_i slices -> slot i % D
+    if (i > N) return;
+    double *gs = ring + (size_t)(i % D) * 2 * Wc;
+    mbar_expect_tx(&bar[i % D], (uint32_t)(2 * Wc) * 8u);
+    tma_load_1d(gs, gb + i * gst, (uint32_t)Wc * 8u, &bar[i % D]);
+    tma_load_1d(gs + Wc, ob + i * ost, (uint32_t)Wc * 8u, &bar[i % D]);
+  };
   // local buffer index: HMAX + l for own point l; l < 0 left halo, l >= Wc right halo
   auto publish = [&](int k, const double(&x)[P]) {
 #pragma unroll
@@ -382,6 +402,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     }
   };
   for (int q = tid; q < 2 * BL; q += NT) smem[q] = 0.0;  // over-read slots stay finite
+  if (tid == 0) {
+    for (int k = 0; k < D; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+  }
   double x[P];
   if (a.state_in) {
 #pragma unroll
@@ -390,66 +414,60 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = 0.0;
   }
-  cluster.sync();  // every CTA zeroed before any remote store lands
+  cluster.sync();  // every CTA zeroed before any remote store lands; barriers initialised
+  if (tid == 0)
+    for (int i = 1; i <= D; ++i) fetch(i);
   publish(0, x);
-  double gq[D][P], vq[D][P];
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    if (1 + d <= N) {
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        gq[d][p] = __ldg(gb + (1 + d) * gst + p);
-        vq[d][p] = ob[(1 + d) * ost + p];
-      }
-    }
-  }
   cluster_arrive();
   cluster_wait();
   const int base = HMAX + tid * P + o0;
 #pragma unroll 1
-  for (int i0 = 1; i0 <= N; i0 += D) {
+  for (int i = 1; i <= N; ++i) {
+    double y[P];
+    psi_apply<P>(B[(i - 1) & 1], base, a.op, y);
+    mbar_wait(&bar[i % D], (uint32_t)(((i - 1) / D) & 1));
+    const double *gs = ring + (size_t)(i % D) * 2 * Wc + tid * P;
+    double *st = stage + (size_t)(i % CS::NSTAGE) * Wc + tid * P;
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int i = i0 + d;
-      if (i <= N) {
-        double y[P];
-        psi_apply<P>(B[(i - 1) & 1], base, a.op, y);
-#pragma unroll
-        for (int p = 0; p < P; ++p) x[p] = y[p] + gq[d][p];
-        publish(i & 1, x);
-        cluster_arrive();
-#pragma unroll
-        for (int p = 0; p < P; ++p) ob[i * ost + p] = vq[d][p] + x[p];  // u_i = v_i + e_i
-        if (i + D <= N) {                      // refill this ring slot D steps ahead
-#pragma unroll
-          for (int p = 0; p < P; ++p) {
-            gq[d][p] = __ldg(gb + (i + D) * gst + p);
-            vq[d][p] = ob[(i + D) * ost + p];
-          }
-        }
-        cluster_wait();
-      }
+    for (int p = 0; p < P; p += 2) {
+      const double2 g2 = *reinterpret_cast<const double2 *>(gs + p);
+      const double2 v2 = *reinterpret_cast<const double2 *>(gs + Wc + p);
+      x[p] = y[p] + g2.x;                           // x_i = Psi x_{i-1} + g_i
+      x[p + 1] = y[p + 1] + g2.y;
+      *reinterpret_cast<double2 *>(st + p) = make_double2(v2.x + x[p], v2.y + x[p + 1]);  // u_i
+    }
+    publish(i & 1, x);
+    fence_proxy_async();
+    cluster_arrive();
+    cluster_wait();
+    if (tid == 0) {  // slot i % D and staging row i are complete in this CTA
+      tma_store_1d(ob + i * ost, stage + (size_t)(i % CS::NSTAGE) * Wc, (uint32_t)Wc * 8u);
+      bulk_commit();
+      bulk_wait_read_all_but1();                    // staging row i-1 read (reused at i+2)
+      fetch(i + D);
     }
   }
   if (a.state_out) {
 #pragma unroll
     for (int p = 0; p < P; ++p) a.state_out[gx0 + p] = x[p];
   }
+  if (tid == 0) bulk_wait_all();
 }
 
 template <int NT, int P, int CL>
 static cudaError_t launch_seq_cluster(const CoarseArgs &a, cudaStream_t s) {
-  const size_t smem = ClusterSmem<NT, P>::BYTES;
+  constexpr int D = 8;
+  const size_t smem = ClusterSmem<NT, P, D>::BYTES;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, 4>,
+    cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, D>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (CL > 8)
-      cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, 4>,
+      cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, D>,
                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
-  psi_seq_cluster_kernel<NT, P, CL, 4><<<CL, NT, smem, s>>>(a);
+  psi_seq_cluster_kernel<NT, P, CL, D><<<CL, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 

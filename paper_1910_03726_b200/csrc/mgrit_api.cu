@@ -582,7 +582,7 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
     int cl = 0;
     SweepCfg cc = {0, 0};
     if (c->nx == 4096) { cl = 8; cc = {128, 4}; }
-    else if (c->nx == 1024) { cl = 8; cc = {32, 4}; }
+    else if (c->nx == 1024) { cl = 8; cc = {64, 2}; }
     if (const char *env = getenv("MGRIT_SEQ_CLUSTER")) {
       cl = 0;
       sscanf(env, "%d,%d,%d", &cl, &cc.nt_threads, &cc.p);
