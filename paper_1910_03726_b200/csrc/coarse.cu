@@ -328,17 +328,35 @@ static cudaError_t launch_seq_periodic(const CoarseArgs &a, cudaStream_t s) {
 // Cluster-wide periodic sequential solve (two-level coarse grid): the periodic
 // row is split over the CL CTAs of one thread-block cluster (CTA c owns [c*Wc, (c+1)*Wc),
 // Wc = NT*P), so a step's nu*nx FMAs run on CL SMs.  Per step i: Psi from the CTA's
-// buffer bc (own values + left/right halos), x_i = Psi x_{i-1} + g_i, u_i = v_i + x_i
-// (P:212); own x_i goes to the local buffer bn, the boundary values are pushed into the
-// neighbours' bn halos (DSMEM stores), then one split cluster barrier (arrive.release,
-// output store + prefetch, wait.acquire).  bn of step i is bc of step i-1, whose last
-// reader passed the previous cluster barrier, so one barrier per step suffices.
-// g_i and v_i of the thread's own points are prefetched D steps ahead into registers.
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+// buffer B[(i-1)&1] (own values + left/right halos of x_{i-1}), x_i = Psi x_{i-1} + g_i,
+// u_i = v_i + x_i.  Own x_i goes to the local buffer B[i&1]; the boundary values
+// are written straight into the neighbours' B[i&1] halos with st.async, each completing
+// bytes on the receiver's halo mbarrier hb[i&1] -- point-to-point, no cluster barrier and
+// no memory fence in the loop.  WAR safety by causality: a neighbour writes my B[i&1]
+// (step i) only after receiving my x_{i-1}, sent after this CTA's __syncthreads that
+// follows every read of B[i&1] (step i-1).
+// Global memory is touched only by the async proxy: TMA bulk loads of g_i / v_i into a
+// D-deep ring and bulk stores of u_i from a 3-deep staging ring, issued by thread 0.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
 }
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
 }
 
 template <int NT, int P, int D> struct ClusterSmem {
@@ -346,16 +364,13 @@ template <int NT, int P, int D> struct ClusterSmem {
   static constexpr int Wc = NT * P;
   static constexpr int BL = ((HMAX + Wc + HMAX + PSI_EXT) / P + 2) * Pad<P>::SP;
   static constexpr int NSTAGE = 3;                  // output staging rows
-  // doubles: 2 state buffers | D x (g, v) slices | NSTAGE output slices | D mbarriers
+  // doubles: 2 state buffers | D x (g, v) slices | NSTAGE output slices | D + 2 mbarriers
   static constexpr size_t RING = 2 * (size_t)BL;
   static constexpr size_t STAGE = RING + 2 * (size_t)D * Wc;
   static constexpr size_t BAR = STAGE + (size_t)NSTAGE * Wc;
-  static constexpr size_t BYTES = sizeof(double) * BAR + 8 * D;
+  static constexpr size_t BYTES = sizeof(double) * BAR + 8 * (D + 2);
 };
 
-// Global memory is touched only by the async proxy (TMA bulk loads of g_i / v_i into a
-// D-deep ring, bulk stores of u_i from a 3-deep staging ring, both issued by thread 0),
-// so the cluster barrier's release orders nothing but the shared-memory state.
 template <int NT, int P, int CL, int D>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     psi_seq_cluster_kernel(const __grid_constant__ CoarseArgs a) {
@@ -367,23 +382,22 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
   extern __shared__ __align__(128) double smem[];
   double *ring = smem + CS::RING;                  // slot k: g at k*2Wc, v at k*2Wc + Wc
   double *stage = smem + CS::STAGE;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + CS::BAR);
-  const int rank = (int)cluster.block_rank();
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + CS::BAR);  // [D] loads, [2] halos
+  uint64_t *hb = bar + D;
+  const uint32_t rank = cluster.block_rank();
   const int tid = threadIdx.x;
   const int N = a.nsteps, o0 = a.op.o0, nu = a.op.nu;
   const int HL = o0 < 0 ? -o0 : 0;                 // left halo (points before the slice)
   const int HR = (o0 + nu - 1) > 0 ? (o0 + nu - 1) : 0;
+  const uint32_t hbytes = (uint32_t)(HL + HR) * 8u;
   const int gx0 = rank * Wc + tid * P;             // global index of the thread's first point
   const double *gb = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)a.nx + rank * Wc;
   double *ob = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)a.nx + rank * Wc;
   const long long gst = a.g.stride * (long long)a.nx, ost = a.out.stride * (long long)a.nx;
-  double *B[2] = {smem, smem + BL};
-  double *Bp[2], *Bn[2];                           // neighbours' buffers (DSMEM)
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    Bp[k] = cluster.map_shared_rank(B[k], (rank + CL - 1) % CL);
-    Bn[k] = cluster.map_shared_rank(B[k], (rank + 1) % CL);
-  }
+  const uint32_t rprev = (rank + CL - 1) % CL, rnext = (rank + 1) % CL;
+  const uint32_t s_base = smem_u32(smem);
+  const uint32_t p_base = mapa_shared(s_base, rprev), n_base = mapa_shared(s_base, rnext);
+  const uint32_t p_hb = mapa_shared(smem_u32(hb), rprev), n_hb = mapa_shared(smem_u32(hb), rnext);
   auto fetch = [&](int i) {  // thread 0: g_i, v_i slices -> slot i % D
     if (i > N) return;
     double *gs = ring + (size_t)(i % D) * 2 * Wc;
@@ -392,19 +406,27 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     tma_load_1d(gs + Wc, ob + i * ost, (uint32_t)Wc * 8u, &bar[i % D]);
   };
   // local buffer index: HMAX + l for own point l; l < 0 left halo, l >= Wc right halo
-  auto publish = [&](int k, const double(&x)[P]) {
+  auto publish_local = [&](int k, const double(&x)[P]) {
+    double *bk = smem + k * BL;
+#pragma unroll
+    for (int p = 0; p < P; ++p) bk[pidx<P>(HMAX + tid * P + p)] = x[p];
+  };
+  auto send_halo = [&](int k, const double(&x)[P]) {
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const int l = tid * P + p;
-      B[k][pidx<P>(HMAX + l)] = x[p];
-      if (l < HR) Bp[k][pidx<P>(HMAX + Wc + l)] = x[p];          // prev's right halo
-      if (l >= Wc - HL) Bn[k][pidx<P>(HMAX + l - Wc)] = x[p];    // next's left halo
+      if (l < HR)            // prev's right halo
+        st_async_f64(p_base + 8u * (uint32_t)(k * BL + pidx<P>(HMAX + Wc + l)), x[p], p_hb + 8u * k);
+      if (l >= Wc - HL)      // next's left halo
+        st_async_f64(n_base + 8u * (uint32_t)(k * BL + pidx<P>(HMAX + l - Wc)), x[p], n_hb + 8u * k);
     }
   };
   for (int q = tid; q < 2 * BL; q += NT) smem[q] = 0.0;  // over-read slots stay finite
   if (tid == 0) {
-    for (int k = 0; k < D; ++k) mbar_init(&bar[k], 1);
+    for (int k = 0; k < D + 2; ++k) mbar_init(&bar[k], 1);
     fence_mbar_init();
+    mbar_expect_tx(&hb[0], hbytes);                // halos of x_0 and x_1
+    mbar_expect_tx(&hb[1], hbytes);
   }
   double x[P];
   if (a.state_in) {
@@ -414,17 +436,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = 0.0;
   }
-  cluster.sync();  // every CTA zeroed before any remote store lands; barriers initialised
+  cluster.sync();  // buffers zeroed, barriers armed everywhere before any remote store
   if (tid == 0)
     for (int i = 1; i <= D; ++i) fetch(i);
-  publish(0, x);
-  cluster_arrive();
-  cluster_wait();
+  publish_local(0, x);
+  send_halo(0, x);
+  __syncthreads();
   const int base = HMAX + tid * P + o0;
 #pragma unroll 1
   for (int i = 1; i <= N; ++i) {
+    const int kp = (i - 1) & 1, kc = i & 1;
+    mbar_wait_cluster(&hb[kp], (uint32_t)(((i - 1) >> 1) & 1));  // halos of x_{i-1}
     double y[P];
-    psi_apply<P>(B[(i - 1) & 1], base, a.op, y);
+    psi_apply<P>(smem + kp * BL, base, a.op, y);
     mbar_wait(&bar[i % D], (uint32_t)(((i - 1) / D) & 1));
     const double *gs = ring + (size_t)(i % D) * 2 * Wc + tid * P;
     double *st = stage + (size_t)(i % CS::NSTAGE) * Wc + tid * P;
@@ -436,11 +460,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       x[p + 1] = y[p + 1] + g2.y;
       *reinterpret_cast<double2 *>(st + p) = make_double2(v2.x + x[p], v2.y + x[p + 1]);  // u_i
     }
-    publish(i & 1, x);
+    publish_local(kc, x);
     fence_proxy_async();
-    cluster_arrive();
-    cluster_wait();
-    if (tid == 0) {  // slot i % D and staging row i are complete in this CTA
+    __syncthreads();  // reads of B[kp], the ring slot and the staging row complete
+    send_halo(kc, x);
+    if (tid == 0) {
+      mbar_expect_tx(&hb[kp], hbytes);              // re-arm for the halos of x_{i+1}
       tma_store_1d(ob + i * ost, stage + (size_t)(i % CS::NSTAGE) * Wc, (uint32_t)Wc * 8u);
       bulk_commit();
       bulk_wait_read_all_but1();                    // staging row i-1 read (reused at i+2)
@@ -452,6 +477,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     for (int p = 0; p < P; ++p) a.state_out[gx0 + p] = x[p];
   }
   if (tid == 0) bulk_wait_all();
+  // the halos of x_N (and the re-armed phase of x_{N+1}) may still be landing here:
+  // wait for x_N's, and keep every CTA's shared memory alive until all have
+  mbar_wait_cluster(&hb[N & 1], (uint32_t)((N >> 1) & 1));
+  cluster.sync();
 }
 
 template <int NT, int P, int CL>
