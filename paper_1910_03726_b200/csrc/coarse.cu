@@ -359,74 +359,95 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
   } while (!done);
 }
 
-template <int NT, int P, int D> struct ClusterSmem {
+template <int NT, int P> struct ClusterSmem {
   static constexpr int HMAX = 64;  // max halo per side (host-checked)
   static constexpr int Wc = NT * P;
   static constexpr int BL = ((HMAX + Wc + HMAX + PSI_EXT) / P + 2) * Pad<P>::SP;
-  static constexpr int NSTAGE = 3;                  // output staging rows
-  // doubles: 2 state buffers | D x (g, v) slices | NSTAGE output slices | D + 2 mbarriers
-  static constexpr size_t RING = 2 * (size_t)BL;
-  static constexpr size_t STAGE = RING + 2 * (size_t)D * Wc;
-  static constexpr size_t BAR = STAGE + (size_t)NSTAGE * Wc;
-  static constexpr size_t BYTES = sizeof(double) * BAR + 8 * (D + 2);
+  static constexpr size_t BYTES = sizeof(double) * 2 * BL + 24;  // 2 state buffers, 3 mbarriers
 };
 
-template <int NT, int P, int CL, int D>
+// y_p = sum_q psi_q x[base + p + q], q < NU4 (coefficients zero-padded past nu): the whole
+// window is loaded at once and each output keeps two partial sums (short FMA chains).
+template <int P, int NU4>
+__device__ __forceinline__ void psi_apply_pad2(const double *__restrict__ s, int base,
+                                                const PsiOp &op, double (&out)[P]) {
+  double w[P + NU4 - 1];
+#pragma unroll
+  for (int r = 0; r < P + NU4 - 1; ++r) w[r] = s[pidx<P>(base + r)];
+  double acc0[P], acc1[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) { acc0[p] = 0.0; acc1[p] = 0.0; }
+#pragma unroll
+  for (int q = 0; q < NU4; q += 2) {
+    const double c0 = op.psi[q], c1 = op.psi[q + 1];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      acc0[p] = fma(c0, w[p + q], acc0[p]);
+      acc1[p] = fma(c1, w[p + q + 1], acc1[p]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) out[p] = acc0[p] + acc1[p];
+}
+
+// Register-ring version: each thread prefetches g_i and v_i of its own P points D steps
+// ahead with plain loads and stores u_i directly (no fence anywhere in the loop, so the
+// stores are fire-and-forget).  The halo senders and the halo readers of each side lie in
+// one warp (host-checked), so a __syncwarp -- not the CTA barrier -- orders a warp's
+// reads of B[(i-1)&1] before its sends of x_i: the inter-CTA chain per step is
+// halo wait -> window load -> NU4/2 FMAs -> st.async.
+template <int NT, int P, int CL, int D, int NU4>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
     psi_seq_cluster_kernel(const __grid_constant__ CoarseArgs a) {
-  static_assert(P % 2 == 0, "P even (16-byte vector staging)");
+  static_assert(P % 2 == 0, "P even (16-byte vector loads)");
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  using CS = ClusterSmem<NT, P, D>;
+  using CS = ClusterSmem<NT, P>;
   constexpr int Wc = CS::Wc, HMAX = CS::HMAX, BL = CS::BL;
   extern __shared__ __align__(128) double smem[];
-  double *ring = smem + CS::RING;                  // slot k: g at k*2Wc, v at k*2Wc + Wc
-  double *stage = smem + CS::STAGE;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + CS::BAR);  // [D] loads, [2] halos
-  uint64_t *hb = bar + D;
+  // Halo mbarriers: x_s lands on hb[s % 3].  Three, not two: the boundary warps run
+  // ahead of the CTA barrier, so the neighbours' x_{i+1} can complete while a warp of this
+  // CTA is still waiting for x_{i-1}; with two barriers that phase would alias.
+  uint64_t *hb = reinterpret_cast<uint64_t *>(smem + 2 * BL);
   const uint32_t rank = cluster.block_rank();
   const int tid = threadIdx.x;
   const int N = a.nsteps, o0 = a.op.o0, nu = a.op.nu;
-  const int HL = o0 < 0 ? -o0 : 0;                 // left halo (points before the slice)
-  const int HR = (o0 + nu - 1) > 0 ? (o0 + nu - 1) : 0;
+  // Halo widths, at least one point each way even for a one-sided stencil: the exchange
+  // must be mutual every step, else a CTA could run ahead of the neighbour it feeds (the
+  // ring only bounds the lead by CL steps) and overwrite halos / mbarrier phases that
+  // neighbour has not consumed.  A point past the stencil is read with a zero weight.
+  const int HL = o0 < 0 ? max(-o0, 1) : 1;         // left halo (points before the slice)
+  const int HR = max(o0 + nu - 1, 1);
   const uint32_t hbytes = (uint32_t)(HL + HR) * 8u;
   const int gx0 = rank * Wc + tid * P;             // global index of the thread's first point
-  const double *gb = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)a.nx + rank * Wc;
-  double *ob = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)a.nx + rank * Wc;
+  const double *gb = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)a.nx + gx0;
+  double *ob = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)a.nx + gx0;
   const long long gst = a.g.stride * (long long)a.nx, ost = a.out.stride * (long long)a.nx;
   const uint32_t rprev = (rank + CL - 1) % CL, rnext = (rank + 1) % CL;
   const uint32_t s_base = smem_u32(smem);
   const uint32_t p_base = mapa_shared(s_base, rprev), n_base = mapa_shared(s_base, rnext);
   const uint32_t p_hb = mapa_shared(smem_u32(hb), rprev), n_hb = mapa_shared(smem_u32(hb), rnext);
-  auto fetch = [&](int i) {  // thread 0: g_i, v_i slices -> slot i % D
-    if (i > N) return;
-    double *gs = ring + (size_t)(i % D) * 2 * Wc;
-    mbar_expect_tx(&bar[i % D], (uint32_t)(2 * Wc) * 8u);
-    tma_load_1d(gs, gb + i * gst, (uint32_t)Wc * 8u, &bar[i % D]);
-    tma_load_1d(gs + Wc, ob + i * ost, (uint32_t)Wc * 8u, &bar[i % D]);
-  };
   // local buffer index: HMAX + l for own point l; l < 0 left halo, l >= Wc right halo
   auto publish_local = [&](int k, const double(&x)[P]) {
     double *bk = smem + k * BL;
 #pragma unroll
     for (int p = 0; p < P; ++p) bk[pidx<P>(HMAX + tid * P + p)] = x[p];
   };
-  auto send_halo = [&](int k, const double(&x)[P]) {
+  auto send_halo = [&](int k, int h, const double(&x)[P]) {  // buffer k, mbarrier h
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const int l = tid * P + p;
       if (l < HR)            // prev's right halo
-        st_async_f64(p_base + 8u * (uint32_t)(k * BL + pidx<P>(HMAX + Wc + l)), x[p], p_hb + 8u * k);
+        st_async_f64(p_base + 8u * (uint32_t)(k * BL + pidx<P>(HMAX + Wc + l)), x[p], p_hb + 8u * h);
       if (l >= Wc - HL)      // next's left halo
-        st_async_f64(n_base + 8u * (uint32_t)(k * BL + pidx<P>(HMAX + l - Wc)), x[p], n_hb + 8u * k);
+        st_async_f64(n_base + 8u * (uint32_t)(k * BL + pidx<P>(HMAX + l - Wc)), x[p], n_hb + 8u * h);
     }
   };
   for (int q = tid; q < 2 * BL; q += NT) smem[q] = 0.0;  // over-read slots stay finite
   if (tid == 0) {
-    for (int k = 0; k < D + 2; ++k) mbar_init(&bar[k], 1);
+    for (int k = 0; k < 3; ++k) mbar_init(&hb[k], 1);
     fence_mbar_init();
-    mbar_expect_tx(&hb[0], hbytes);                // halos of x_0 and x_1
-    mbar_expect_tx(&hb[1], hbytes);
+    for (int k = 0; k < 3; ++k) mbar_expect_tx(&hb[k], hbytes);  // halos of x_0, x_1, x_2
   }
   double x[P];
   if (a.state_in) {
@@ -436,77 +457,110 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = 0.0;
   }
-  cluster.sync();  // buffers zeroed, barriers armed everywhere before any remote store
-  if (tid == 0)
-    for (int i = 1; i <= D; ++i) fetch(i);
-  publish_local(0, x);
-  send_halo(0, x);
-  __syncthreads();
-  const int base = HMAX + tid * P + o0;
-#pragma unroll 1
-  for (int i = 1; i <= N; ++i) {
-    const int kp = (i - 1) & 1, kc = i & 1;
-    mbar_wait_cluster(&hb[kp], (uint32_t)(((i - 1) >> 1) & 1));  // halos of x_{i-1}
-    double y[P];
-    psi_apply<P>(smem + kp * BL, base, a.op, y);
-    mbar_wait(&bar[i % D], (uint32_t)(((i - 1) / D) & 1));
-    const double *gs = ring + (size_t)(i % D) * 2 * Wc + tid * P;
-    double *st = stage + (size_t)(i % CS::NSTAGE) * Wc + tid * P;
+  double gq[D][P], vq[D][P];
+  auto load = [&](int d, int i) {
 #pragma unroll
     for (int p = 0; p < P; p += 2) {
-      const double2 g2 = *reinterpret_cast<const double2 *>(gs + p);
-      const double2 v2 = *reinterpret_cast<const double2 *>(gs + Wc + p);
-      x[p] = y[p] + g2.x;                           // x_i = Psi x_{i-1} + g_i
-      x[p + 1] = y[p + 1] + g2.y;
-      *reinterpret_cast<double2 *>(st + p) = make_double2(v2.x + x[p], v2.y + x[p + 1]);  // u_i
+      const double2 g2 = __ldg(reinterpret_cast<const double2 *>(gb + i * gst + p));
+      const double2 v2 = __ldg(reinterpret_cast<const double2 *>(ob + i * ost + p));
+      gq[d][p] = g2.x; gq[d][p + 1] = g2.y;
+      vq[d][p] = v2.x; vq[d][p + 1] = v2.y;
     }
-    publish_local(kc, x);
-    fence_proxy_async();
-    __syncthreads();  // reads of B[kp], the ring slot and the staging row complete
-    send_halo(kc, x);
-    if (tid == 0) {
-      mbar_expect_tx(&hb[kp], hbytes);              // re-arm for the halos of x_{i+1}
-      tma_store_1d(ob + i * ost, stage + (size_t)(i % CS::NSTAGE) * Wc, (uint32_t)Wc * 8u);
-      bulk_commit();
-      bulk_wait_read_all_but1();                    // staging row i-1 read (reused at i+2)
-      fetch(i + D);
+  };
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    if (1 + d <= N) load(d, 1 + d);
+  cluster.sync();  // buffers zeroed, barriers armed everywhere before any remote store
+  publish_local(0, x);
+  send_halo(0, 0, x);
+  __syncthreads();
+  int hp = 0;                                      // (i - 1) % 3
+  const int base = HMAX + tid * P + o0;
+#pragma unroll 1
+  for (int i0 = 1; i0 <= N; i0 += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int i = i0 + d;
+      if (i <= N) {
+        const int kp = (i - 1) & 1, kc = i & 1;
+        mbar_wait_cluster(&hb[hp], (uint32_t)(((i - 1) / 3) & 1));  // halos of x_{i-1}
+        double y[P];
+        psi_apply_pad2<P, NU4>(smem + kp * BL, base, a.op, y);
+#pragma unroll
+        for (int p = 0; p < P; ++p) x[p] = y[p] + gq[d][p];          // x_i = Psi x_{i-1} + g_i
+        __syncwarp();                               // this warp's reads of B[kp] done
+        const int hc = hp == 2 ? 0 : hp + 1;      // i % 3
+        send_halo(kc, hc, x);
+        publish_local(kc, x);
+        double *orow = ob + i * ost;
+#pragma unroll
+        for (int p = 0; p < P; p += 2)              // u_i = v_i + e_i
+          *reinterpret_cast<double2 *>(orow + p) = make_double2(vq[d][p] + x[p], vq[d][p + 1] + x[p + 1]);
+        if (i + D <= N) load(d, i + D);             // refill this ring slot D steps ahead
+        if (tid == 0) mbar_expect_tx(&hb[hp], hbytes);  // re-arm for the halos of x_{i+2}
+        hp = hc;
+        __syncthreads();                            // B[kc] complete; B[kp] reads done
+      }
     }
   }
   if (a.state_out) {
 #pragma unroll
     for (int p = 0; p < P; ++p) a.state_out[gx0 + p] = x[p];
   }
-  if (tid == 0) bulk_wait_all();
-  // the halos of x_N (and the re-armed phase of x_{N+1}) may still be landing here:
-  // wait for x_N's, and keep every CTA's shared memory alive until all have
-  mbar_wait_cluster(&hb[N & 1], (uint32_t)((N >> 1) & 1));
+  // the halos of x_N may still be landing here: wait for them, and keep every CTA's
+  // shared memory alive until all have
+  mbar_wait_cluster(&hb[N % 3], (uint32_t)((N / 3) & 1));
   cluster.sync();
+}
+
+template <int NT, int P, int CL, int NU4>
+static cudaError_t launch_seq_cluster_nu(const CoarseArgs &a, cudaStream_t s) {
+  constexpr int D = 4;
+  const size_t smem = ClusterSmem<NT, P>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, D, NU4>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (CL > 8)
+      cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, D, NU4>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  psi_seq_cluster_kernel<NT, P, CL, D, NU4><<<CL, NT, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 template <int NT, int P, int CL>
 static cudaError_t launch_seq_cluster(const CoarseArgs &a, cudaStream_t s) {
-  constexpr int D = 8;
-  const size_t smem = ClusterSmem<NT, P, D>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, D>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (CL > 8)
-      cudaFuncSetAttribute(psi_seq_cluster_kernel<NT, P, CL, D>,
-                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
-  }
-  psi_seq_cluster_kernel<NT, P, CL, D><<<CL, NT, smem, s>>>(a);
-  return cudaGetLastError();
+  const int nu = a.op.nu;
+  if (nu <= 12) return launch_seq_cluster_nu<NT, P, CL, 12>(a, s);
+  if (nu <= 16) return launch_seq_cluster_nu<NT, P, CL, 16>(a, s);
+  if (nu <= 20) return launch_seq_cluster_nu<NT, P, CL, 20>(a, s);
+  if (nu <= 24) return launch_seq_cluster_nu<NT, P, CL, 24>(a, s);
+  if (nu <= 32) return launch_seq_cluster_nu<NT, P, CL, 32>(a, s);
+  if (nu <= 40) return launch_seq_cluster_nu<NT, P, CL, 40>(a, s);
+  if (nu <= 48) return launch_seq_cluster_nu<NT, P, CL, 48>(a, s);
+  return launch_seq_cluster_nu<NT, P, CL, 64>(a, s);
+}
+
+// Host check for the cluster path: nx == cl*NT*P, halos <= 64 and each side's halo
+// senders and readers inside one warp.
+bool seq_cluster_ok(int cl, SweepCfg c, int nx, int o0, int nu) {
+  if (cl < 2 || cl > 16 || cl * c.nt_threads * c.p != nx) return false;
+  const int hl = std::max(1, -o0), hr = std::max(1, o0 + nu - 1);
+  int nu4 = 64;
+  for (int v : {12, 16, 20, 24, 32, 40, 48})
+    if (nu <= v) { nu4 = v; break; }
+  const int wpts = 32 * c.p;  // points per warp
+  return hl <= 64 && hr <= 64 && hl <= wpts && hr <= wpts && c.nt_threads >= 64 &&
+         nu4 + c.p + 2 + std::max(o0, 0) <= wpts && std::max(-o0, 0) <= wpts;
 }
 
 // nx = CL * NT * P; the halos (-o0, o0+nu-1) must be <= 64 and <= NT*P (host-checked).
 cudaError_t launch_psi_seq_cluster(int cl, SweepCfg c, const CoarseArgs &a, cudaStream_t s) {
   if (a.nsteps <= 0) return cudaSuccess;
   if (cl == 8 && c.nt_threads == 128 && c.p == 4) return launch_seq_cluster<128, 4, 8>(a, s);
-  if (cl == 8 && c.nt_threads == 32 && c.p == 4) return launch_seq_cluster<32, 4, 8>(a, s);
   if (cl == 16 && c.nt_threads == 64 && c.p == 4) return launch_seq_cluster<64, 4, 16>(a, s);
-  if (cl == 16 && c.nt_threads == 32 && c.p == 2) return launch_seq_cluster<32, 2, 16>(a, s);
   if (cl == 8 && c.nt_threads == 64 && c.p == 2) return launch_seq_cluster<64, 2, 8>(a, s);
   return cudaErrorInvalidConfiguration;
 }

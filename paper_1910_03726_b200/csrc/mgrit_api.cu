@@ -534,6 +534,51 @@ int reduce_norm(mgrit_ctx *c, long long n, double *norm2_host) {
 
 // Sequential coarse solve on level l (= levels-1, the coarsest) for steps 1..ntl:
 //   x_n = Psi x_{n-1} + g_n, out_n = v_n + x_n  (stencil Psi: v == out, accumulated).
+// Launch plan of the stencil-Psi sequential solve on level l.  Short chains (the
+// V-cycle's coarsest level): trapezoid tiles, one launch, no inter-CTA communication.
+// Long chains (two-level): the row split over a thread-block cluster (DSMEM halos), else
+// one periodic CTA.
+struct CoarsePlan {
+  enum Kind { NONE, TILES, CLUSTER, SEQ } kind = NONE;
+  SweepCfg cfg = {0, 0};
+  int ntiles = 1, cl = 0;
+};
+static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
+  CoarsePlan pl;
+  const PsiOp &op = c->op[l];
+  const long long cone = c->ntl[l] * (long long)(op.nu - 1);
+  PsiCfg pc;
+  if (cone <= 2048 && c->nx >= 2048 && choose_psi(c->nx, (int)cone, false, pc)) {
+    pl.kind = CoarsePlan::TILES;
+    pl.cfg = pc.cfg;
+    pl.ntiles = pc.ntiles;
+    return pl;
+  }
+  if (!(choose_psi(c->nx, 0, true, pc) && pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx))
+    return pl;
+  int cl = 0;
+  SweepCfg cc = {0, 0};
+  if (c->nx == 4096) { cl = 8; cc = {128, 4}; }
+  else if (c->nx == 1024) { cl = 8; cc = {64, 2}; }
+  if (const char *env = getenv("MGRIT_SEQ_CLUSTER")) {
+    cl = 0;
+    sscanf(env, "%d,%d,%d", &cl, &cc.nt_threads, &cc.p);
+  }
+  if (seq_cluster_ok(cl, cc, c->nx, op.o0, op.nu)) {
+    pl.kind = CoarsePlan::CLUSTER;
+    pl.cfg = cc;
+    pl.cl = cl;
+    return pl;
+  }
+  SweepCfg sc = pc.cfg;  // more threads per row for the latency-bound chain
+  if (c->nx == 4096) sc = {1024, 4};
+  else if (c->nx == 1024) sc = {256, 4};
+  if (const char *env = getenv("MGRIT_SEQ_CFG")) sscanf(env, "%d,%d", &sc.nt_threads, &sc.p);
+  pl.kind = CoarsePlan::SEQ;
+  pl.cfg = sc;
+  return pl;
+}
+
 int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
   const long long N = c->ntl[l];
   if (c->psi_kind != MGRIT_PSI_STENCIL) {
@@ -554,50 +599,28 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
     else return fail(c, MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,256,1024}");
     return run(c, 2, [&] { return launch_rk_coarse(c->scheme, cfg, a, c->stream); });
   }
-  const PsiOp &op = c->op[l];
-  // Short chains (the V-cycle's coarsest level): trapezoid tiles, one launch, no
-  // inter-CTA communication.  Long chains (two-level): one periodic CTA.
-  PsiCfg pc;
-  const long long cone = N * (long long)(op.nu - 1);
-  bool ok = false;
-  if (cone <= 2048 && c->nx >= 2048) ok = choose_psi(c->nx, (int)cone, false, pc);
-  if (!ok) {
-    ok = choose_psi(c->nx, 0, true, pc) && pc.ntiles == 1 &&
-         pc.cfg.nt_threads * pc.cfg.p == c->nx;
-  }
-  if (!ok) return fail(c, MGRIT_EUNSUPPORTED, "no coarse-solve configuration for nx=%d", c->nx);
+  const CoarsePlan pl = plan_coarse(c, l);
+  if (pl.kind == CoarsePlan::NONE)
+    return fail(c, MGRIT_EUNSUPPORTED, "no coarse-solve configuration for nx=%d", c->nx);
   CoarseArgs a;
   std::memset(&a, 0, sizeof(a));
   a.nx = c->nx;
-  a.ntiles = pc.ntiles;
+  a.ntiles = pl.ntiles;
   a.nsteps = (int)N;
   a.n0 = 0;
   a.g = rm(c->g[l], 0, 1);
   a.out = out;
   a.state_in = nullptr;
   a.state_out = nullptr;
-  a.op = op;
-  if (pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx) {
-    // Thread-block cluster: the row split over CL SMs (DSMEM halos).
-    int cl = 0;
-    SweepCfg cc = {0, 0};
-    if (c->nx == 4096) { cl = 8; cc = {128, 4}; }
-    else if (c->nx == 1024) { cl = 8; cc = {64, 2}; }
-    if (const char *env = getenv("MGRIT_SEQ_CLUSTER")) {
-      cl = 0;
-      sscanf(env, "%d,%d,%d", &cl, &cc.nt_threads, &cc.p);
-    }
-    const int hl = std::max(0, -op.o0), hr = std::max(0, op.o0 + op.nu - 1);
-    if (cl > 1 && cl * cc.nt_threads * cc.p == c->nx && hl <= 64 && hr <= 64 &&
-        hl <= cc.nt_threads * cc.p && hr <= cc.nt_threads * cc.p)
-      return run(c, 2, [&] { return launch_psi_seq_cluster(cl, cc, a, c->stream); });
-    SweepCfg sc = pc.cfg;  // more threads per row for the latency-bound chain
-    if (c->nx == 4096) sc = {1024, 4};
-    else if (c->nx == 1024) sc = {256, 4};
-    if (const char *env = getenv("MGRIT_SEQ_CFG")) sscanf(env, "%d,%d", &sc.nt_threads, &sc.p);
-    return run(c, 2, [&] { return launch_psi_seq_periodic(sc, a, c->stream); });
+  a.op = c->op[l];
+  switch (pl.kind) {
+    case CoarsePlan::CLUSTER:
+      return run(c, 2, [&] { return launch_psi_seq_cluster(pl.cl, pl.cfg, a, c->stream); });
+    case CoarsePlan::SEQ:
+      return run(c, 2, [&] { return launch_psi_seq_periodic(pl.cfg, a, c->stream); });
+    default:
+      return run(c, 2, [&] { return launch_psi_coarse(pl.cfg, a, c->stream); });
   }
-  return run(c, 2, [&] { return launch_psi_coarse(pc.cfg, a, c->stream); });
 }
 
 // Level-l (1 <= l <= levels-2) FCF sweep with RHS g_l, zero initial guess:
@@ -1140,8 +1163,23 @@ int mgrit_describe(const mgrit_ctx *c, char *buf, size_t len) {
   const bool ok = choose_fine(c, c->relax == MGRIT_RELAX_FCF ? 2 * m : m, f);
   const bool tma = ok && f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1);
   const char *kern = !ok ? "none" : (tma ? "rk_sweep_tma_kernel" : "rk_sweep_kernel");
-  snprintf(buf, len, "fine=%s<scheme%d,NT=%d,P=%d> tiles=%d halo=%d levels=%d", kern, c->scheme,
-           ok ? f.cfg.nt_threads : 0, ok ? f.cfg.p : 0, ok ? f.ntiles : 0, ok ? f.HL : 0, c->levels);
+  char coarse[96] = "rk_coarse_kernel";
+  if (c->psi_kind == MGRIT_PSI_STENCIL) {
+    const CoarsePlan pl = plan_coarse(c, c->levels - 1);
+    if (pl.kind == CoarsePlan::CLUSTER)
+      snprintf(coarse, sizeof(coarse), "psi_seq_cluster_kernel<NT=%d,P=%d,CL=%d>", pl.cfg.nt_threads,
+               pl.cfg.p, pl.cl);
+    else if (pl.kind == CoarsePlan::SEQ)
+      snprintf(coarse, sizeof(coarse), "psi_seq_periodic_kernel<NT=%d,P=%d>", pl.cfg.nt_threads, pl.cfg.p);
+    else if (pl.kind == CoarsePlan::TILES)
+      snprintf(coarse, sizeof(coarse), "psi_coarse_kernel<NT=%d,P=%d> tiles=%d", pl.cfg.nt_threads,
+               pl.cfg.p, pl.ntiles);
+    else
+      snprintf(coarse, sizeof(coarse), "none");
+  }
+  snprintf(buf, len, "fine=%s<scheme%d,NT=%d,P=%d> tiles=%d halo=%d levels=%d coarse=%s", kern,
+           c->scheme, ok ? f.cfg.nt_threads : 0, ok ? f.cfg.p : 0, ok ? f.ntiles : 0, ok ? f.HL : 0,
+           c->levels, coarse);
   return MGRIT_OK;
 }
 

@@ -167,6 +167,70 @@ def test_coarse_correction_primitive(order, tab, cfl, nx, nt, m, nu):
     assert _rel(Ug.cpu().numpy(), Uo) <= REL
 
 
+@pytest.mark.parametrize("nx,o0,nu,cluster", [
+    (4096, -7, 15, None),            # cfg3-like: default 8 CTAs x 128 threads x 4 points
+    (4096, -4, 9, "16,64,4"),        # 16-CTA (non-portable) cluster
+    (4096, -24, 37, None),           # wide thresholded stencil (cfg4-like)
+    (4096, 0, 11, None),             # one-sided (right halo only)
+    (4096, -12, 12, None),           # one-sided (left halo only)
+    (4096, -14, 15, None),           # cfg3's shape: one-sided, 14-point left halo
+    (1024, -4, 9, None),             # cfg2-like: 8 CTAs x 64 threads x 2 points
+    (1024, -5, 11, "8,64,2"),
+])
+def test_coarse_correction_cluster(nx, o0, nu, cluster, monkeypatch):
+    """Two-level coarse correction through the thread-block-cluster sequential solve
+    (row split over 8/16 SMs, DSMEM halos): e_j = Psi e_{j-1} + r_j, U[jm] += e_j, then
+    F-relaxation vs the oracle, for halo shapes on both / one side."""
+    B = _cuda()
+    if cluster:
+        monkeypatch.setenv("MGRIT_SEQ_CLUSTER", cluster)
+    order, tab, cfl, m = 3, "erk3_kutta", 0.85, 4
+    nt = 2048 if nx == 4096 else 1024   # coarse chain long enough for the cluster path
+    phi = D.make_phi(order, tab, cfl, nx)
+    rng = np.random.default_rng(nu)
+    coeffs = rng.uniform(-1.0, 1.0, nu)
+    coeffs *= 0.9 / np.sum(np.abs(coeffs))           # |Psi| < 1: the chain stays bounded
+    offsets = list(range(o0, o0 + nu))
+    psi = D.StencilPhi(dict(zip(offsets, coeffs)), nx)
+    U = W.initial_iterate(11, nx, nt, W.u0_fourier(nx, 3))
+    M.f_relax(U, phi, m)
+    Uo = U.copy()
+    cpts = np.arange(m, nt + 1, m)
+    gc = np.zeros((nt // m + 1, nx))
+    gc[1:] = M.residual_rows(Uo, phi, cpts)
+    E = M.sequential_rhs(psi, gc)
+    Uo[cpts] += E[1:]
+    M.f_relax(Uo, phi, m)
+    s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2,
+                [{"kind": "stencil", "offsets": offsets, "coeffs": list(coeffs)}], "FCF")
+    assert "coarse=psi_seq_cluster_kernel" in s.describe(), s.describe()
+    Ug = torch.from_numpy(U).cuda()
+    s.coarse_solve_full(Ug)
+    assert _rel(Ug.cpu().numpy(), Uo) <= REL
+
+
+@pytest.mark.parametrize("wname", ["cfg2", "cfg3", "cfg4_literal"])
+def test_coarse_solve_deterministic(wname):
+    """The two-level coarse correction at full size (cluster path, 2048-4096 coarse steps)
+    is bitwise reproducible: any halo / mbarrier race between the cluster's CTAs shows up
+    as run-to-run differences."""
+    B = _cuda()
+    from paper_1910_03726_b200 import problem
+    w = W.ALL[wname]
+    s = problem.make_solver(w)
+    assert "coarse=psi_seq_cluster_kernel" in s.describe(), s.describe()
+    U0 = problem.device_guess(w)
+    s.relax_full(U0, "F")
+    outs = []
+    for _ in range(3):
+        U = U0.clone()
+        s.coarse_solve_full(U)
+        outs.append(U)
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0]), (o - outs[0]).abs().max().item()
+
+
 # ------------------------------------------------------------------ full solves
 def _solve_parity(w, max_iter=None, check_states=True):
     B = _cuda()
