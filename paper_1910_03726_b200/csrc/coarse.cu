@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace mg {
 
@@ -476,6 +477,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
   __syncthreads();
   int hp = 0;                                      // (i - 1) % 3
   const int base = HMAX + tid * P + o0;
+  const bool edge_warp = (tid >> 5) == 0 || (tid >> 5) == NT / 32 - 1;
 #pragma unroll 1
   for (int i0 = 1; i0 <= N; i0 += D) {
 #pragma unroll
@@ -483,7 +485,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
       const int i = i0 + d;
       if (i <= N) {
         const int kp = (i - 1) & 1, kc = i & 1;
-        mbar_wait_cluster(&hb[hp], (uint32_t)(((i - 1) / 3) & 1));  // halos of x_{i-1}
+        // halos of x_{i-1}: only the boundary warps read them (the others read their own
+        // region, ordered by the CTA barrier).  The st.async data lands in this CTA's
+        // shared memory and completes on its own mbarrier, so a CTA-scope acquire (no L1
+        // invalidation) suffices, as for a TMA load.
+        if (edge_warp) mbar_wait(&hb[hp], (uint32_t)(((i - 1) / 3) & 1));
         double y[P];
         psi_apply_pad2<P, NU4>(smem + kp * BL, base, a.op, y);
 #pragma unroll
@@ -513,9 +519,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
   cluster.sync();
 }
 
-template <int NT, int P, int CL, int NU4>
+template <int NT, int P, int CL, int NU4, int D = 4>
 static cudaError_t launch_seq_cluster_nu(const CoarseArgs &a, cudaStream_t s) {
-  constexpr int D = 4;
   const size_t smem = ClusterSmem<NT, P>::BYTES;
   static bool attr = false;
   if (!attr) {
@@ -533,6 +538,8 @@ static cudaError_t launch_seq_cluster_nu(const CoarseArgs &a, cudaStream_t s) {
 template <int NT, int P, int CL>
 static cudaError_t launch_seq_cluster(const CoarseArgs &a, cudaStream_t s) {
   const int nu = a.op.nu;
+  if (NT == 128 && P == 4 && nu <= 16 && getenv("MGRIT_SEQ_D8"))
+    return launch_seq_cluster_nu<NT, P, CL, 16, 8>(a, s);
   if (nu <= 12) return launch_seq_cluster_nu<NT, P, CL, 12>(a, s);
   if (nu <= 16) return launch_seq_cluster_nu<NT, P, CL, 16>(a, s);
   if (nu <= 20) return launch_seq_cluster_nu<NT, P, CL, 20>(a, s);
@@ -562,6 +569,8 @@ cudaError_t launch_psi_seq_cluster(int cl, SweepCfg c, const CoarseArgs &a, cuda
   if (cl == 8 && c.nt_threads == 128 && c.p == 4) return launch_seq_cluster<128, 4, 8>(a, s);
   if (cl == 16 && c.nt_threads == 64 && c.p == 4) return launch_seq_cluster<64, 4, 16>(a, s);
   if (cl == 8 && c.nt_threads == 64 && c.p == 2) return launch_seq_cluster<64, 2, 8>(a, s);
+  if (cl == 16 && c.nt_threads == 128 && c.p == 2) return launch_seq_cluster<128, 2, 16>(a, s);
+  if (cl == 8 && c.nt_threads == 256 && c.p == 2) return launch_seq_cluster<256, 2, 8>(a, s);
   return cudaErrorInvalidConfiguration;
 }
 

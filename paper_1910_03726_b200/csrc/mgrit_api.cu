@@ -558,7 +558,7 @@ static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
     return pl;
   int cl = 0;
   SweepCfg cc = {0, 0};
-  if (c->nx == 4096) { cl = 8; cc = {128, 4}; }
+  if (c->nx == 4096) { cl = 8; cc = {256, 2}; }
   else if (c->nx == 1024) { cl = 8; cc = {64, 2}; }
   if (const char *env = getenv("MGRIT_SEQ_CLUSTER")) {
     cl = 0;
