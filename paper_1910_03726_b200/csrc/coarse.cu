@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 namespace mg {
@@ -561,6 +562,320 @@ bool seq_cluster_ok(int cl, SweepCfg c, int nx, int o0, int nu) {
   const int wpts = 32 * c.p;  // points per warp
   return hl <= 64 && hr <= 64 && hl <= wpts && hr <= wpts && c.nt_threads >= 64 &&
          nu4 + c.p + 2 + std::max(o0, 0) <= wpts && std::max(-o0, 0) <= wpts;
+}
+
+// --------------------------------------------------------------------------
+// Communication-avoiding cluster solve (s-step halos).  Same chain and split as above, but
+// the CTA also keeps an extended halo of EL >= S*HL points on the left and ER >= S*HR on
+// the right and advances the whole extended region S steps between exchanges: after k
+// local steps the values are exact on [-(S-k)HL, Wc+(S-k)HR), so after S steps the own
+// region [0, Wc) is exact and only then are EL / ER boundary points exchanged (st.async
+// into the neighbours' receive buffers, complete_tx on their mbarriers).  The inter-SM
+// latency is paid once per S steps; the price is (EL+ER)/Wc redundant FMAs.
+// Threads: t covers local points l = -EL + t*P + p; own threads are t in [EL/P, EL/P+NT).
+// Per super-step j (steps jS+1..jS+S): halo threads wait for exchange j (x_{jS} of the
+// neighbours' boundary points) and copy it from the receive buffer R[j&1] into the state
+// buffer; then S local steps, each one CTA barrier.  R is separate from the state
+// buffers, so a neighbour that runs ahead cannot overwrite halo values still being read.
+template <int NT, int P> struct CaSmem {
+  static constexpr int EMAX = 256;                  // EL + ER <= EMAX (host-checked)
+  static constexpr int MARG = 64;                   // left over-read (-o0 <= 64), multiple of P
+  static constexpr int MARGR = 160;                 // right over-read (HR + NU4 padding + P)
+  static constexpr int Wc = NT * P;
+  static constexpr int COLS = (MARG + EMAX + Wc + MARGR) / P + 1;
+  static constexpr int BL = COLS * P;               // state buffer, structure of arrays [P][COLS]
+  static constexpr int D = 6;                       // cp.async ring depth (steps)
+  static constexpr int GW = EMAX + Wc;              // g ring row (extended region), v: Wc
+  static constexpr size_t BYTES =
+      sizeof(double) * (2 * (size_t)BL + 2 * EMAX + (size_t)D * (GW + Wc)) + 24;
+};
+
+// Stencil window from a [P][COLS] structure-of-arrays buffer: logical slot q lives at
+// (q % P) * COLS + q / P, so for every window offset the 32 lanes of a warp read 32
+// consecutive doubles (no bank conflicts).  Whole window in registers, two partial sums.
+template <int P, int COLS, int NU4>
+__device__ __forceinline__ void psi_soa_fixed(const double *__restrict__ s, int base,
+                                              const PsiOp &op, double (&out)[P]) {
+  double w[P + NU4 - 1];
+#pragma unroll
+  for (int r = 0; r < P + NU4 - 1; ++r) w[r] = s[((base + r) % P) * COLS + (base + r) / P];
+  double acc0[P], acc1[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) { acc0[p] = 0.0; acc1[p] = 0.0; }
+#pragma unroll
+  for (int q = 0; q < NU4; q += 2) {
+    const double c0 = op.psi[q], c1 = op.psi[q + 1];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      acc0[p] = fma(c0, w[p + q], acc0[p]);
+      acc1[p] = fma(c1, w[p + q + 1], acc1[p]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) out[p] = acc0[p] + acc1[p];
+}
+// Same with the window's phase REM = base % P known at compile time: s0 points at column
+// base / P, every load has an immediate offset (no per-tap index arithmetic).
+template <int P, int COLS, int NU4, int REM>
+__device__ __forceinline__ void psi_soa_rem(const double *__restrict__ s0, const PsiOp &op,
+                                            double (&out)[P]) {
+  double w[P + NU4 - 1];
+#pragma unroll
+  for (int r = 0; r < P + NU4 - 1; ++r) w[r] = s0[((REM + r) % P) * COLS + (REM + r) / P];
+  double acc0[P], acc1[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) { acc0[p] = 0.0; acc1[p] = 0.0; }
+#pragma unroll
+  for (int q = 0; q < NU4; q += 2) {
+    const double c0 = op.psi[q], c1 = op.psi[q + 1];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      acc0[p] = fma(c0, w[p + q], acc0[p]);
+      acc1[p] = fma(c1, w[p + q + 1], acc1[p]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) out[p] = acc0[p] + acc1[p];
+}
+template <int P, int COLS, int NU4>
+__device__ __forceinline__ void psi_soa_dispatch(const double *__restrict__ s, int base,
+                                                 const PsiOp &op, double (&out)[P]) {
+  const int rem = base % P;           // base >= 0
+  const double *s0 = s + base / P;
+  if constexpr (P == 2) {
+    if (rem == 0) psi_soa_rem<P, COLS, NU4, 0>(s0, op, out);
+    else psi_soa_rem<P, COLS, NU4, 1>(s0, op, out);
+  } else if constexpr (P == 4) {
+    if (rem == 0) psi_soa_rem<P, COLS, NU4, 0>(s0, op, out);
+    else if (rem == 1) psi_soa_rem<P, COLS, NU4, 1>(s0, op, out);
+    else if (rem == 2) psi_soa_rem<P, COLS, NU4, 2>(s0, op, out);
+    else psi_soa_rem<P, COLS, NU4, 3>(s0, op, out);
+  } else {
+    psi_soa_fixed<P, COLS, NU4>(s, base, op, out);
+  }
+}
+// Wide stencils: the window streamed through registers four taps at a time.
+template <int P, int COLS>
+__device__ __forceinline__ void psi_soa_chunked(const double *__restrict__ s, int base,
+                                                const PsiOp &op, double (&out)[P]) {
+  auto ld = [&](int q) { return s[(q % P) * COLS + q / P]; };
+  double w[P + 3];
+#pragma unroll
+  for (int r = 0; r < P + 3; ++r) w[r] = ld(base + r);
+#pragma unroll
+  for (int p = 0; p < P; ++p) out[p] = 0.0;
+  const int nu4 = (op.nu + 3) & ~3;
+#pragma unroll 1
+  for (int q0 = 0; q0 < nu4; q0 += 4) {
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const double c = op.psi[q0 + qq];
+#pragma unroll
+      for (int p = 0; p < P; ++p) out[p] = fma(c, w[p + qq], out[p]);
+    }
+#pragma unroll
+    for (int r = 0; r + 4 < P + 3; ++r) w[r] = w[r + 4];
+#pragma unroll
+    for (int r = P - 1; r < P + 3; ++r) w[r] = ld(base + q0 + 4 + r);
+  }
+}
+__device__ __forceinline__ void cp_async16(void *dst_s, const void *src_g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_s)), "l"(src_g)
+               : "memory");
+}
+
+// The g_i / v_i rows come in through a per-thread cp.async ring (D steps deep): unlike
+// register prefetches, cp.async copies are not waited for by the per-step CTA barrier
+// (a plain load in flight must complete before bar.sync releases), so the DRAM latency
+// stays off the step chain.
+template <int NT, int P, int CL, int NU4>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
+    psi_seq_cluster_ca_kernel(const __grid_constant__ CoarseArgs a, int S) {
+  static_assert(P % 2 == 0, "P even (16-byte copies)");
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  using CS = CaSmem<NT, P>;
+  constexpr int Wc = CS::Wc, BL = CS::BL, COLS = CS::COLS, MARG = CS::MARG, D = CS::D, GW = CS::GW;
+  extern __shared__ __align__(128) double smem[];
+  double *R = smem + 2 * BL;                        // receive buffers [2][EL + ER]
+  double *gring = R + 2 * CS::EMAX;                 // [D][GW]
+  double *vring = gring + (size_t)D * GW;           // [D][Wc]
+  uint64_t *hb = reinterpret_cast<uint64_t *>(vring + (size_t)D * Wc);  // exchange j: hb[j % 3]
+  const uint32_t rank = cluster.block_rank();
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int N = a.nsteps, o0 = a.op.o0, nu = a.op.nu;
+  const int HL = o0 < 0 ? max(-o0, 1) : 1, HR = max(o0 + nu - 1, 1);
+  const int EL = ((S * HL + P - 1) / P) * P, ER = ((S * HR + P - 1) / P) * P;
+  const uint32_t hbytes = (uint32_t)(EL + ER) * 8u;
+  const int l0 = -EL + tid * P;                    // first local point of this thread
+  const bool active = l0 < Wc + ER;
+  const bool own = l0 >= 0 && l0 < Wc;
+  const bool lhalo = l0 < 0, rhalo = l0 >= Wc && active;
+  int gx = (int)rank * Wc + l0;                    // global index (periodic)
+  if (gx < 0) gx += a.nx;
+  if (gx >= a.nx) gx -= a.nx;
+  const double *gb = a.g.base + (a.g.off + a.n0 * a.g.stride) * (long long)a.nx + gx;
+  double *ob = const_cast<double *>(a.out.base) + (a.out.off + a.n0 * a.out.stride) * (long long)a.nx + gx;
+  const long long gst = a.g.stride * (long long)a.nx, ost = a.out.stride * (long long)a.nx;
+  const uint32_t rprev = (rank + CL - 1) % CL, rnext = (rank + 1) % CL;
+  const uint32_t r_loc = smem_u32(R), hb_loc = smem_u32(hb);
+  const uint32_t p_R = mapa_shared(r_loc, rprev), n_R = mapa_shared(r_loc, rnext);
+  const uint32_t p_hb = mapa_shared(hb_loc, rprev), n_hb = mapa_shared(hb_loc, rnext);
+  const int q0 = MARG + EL + l0;                   // logical slot of point l0 (multiple of P)
+  const int col = q0 / P;
+  auto put = [&](double *b, const double(&x)[P]) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) b[p * COLS + col] = x[p];
+  };
+  // R layout: [0, EL) = left halo l = -EL + q; [EL, EL+ER) = right halo l = Wc + (q - EL)
+  auto send = [&](int j, const double(&x)[P]) {   // exchange j: own boundary points
+    if (!own) return;
+    const int rb = (j & 1) * CS::EMAX;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int l = l0 + p;
+      if (l < ER)            // prev's right halo, slot EL + l
+        st_async_f64(p_R + 8u * (uint32_t)(rb + EL + l), x[p], p_hb + 8u * (uint32_t)(j % 3));
+      if (l >= Wc - EL)      // next's left halo, slot l - (Wc - EL)
+        st_async_f64(n_R + 8u * (uint32_t)(rb + l - (Wc - EL)), x[p], n_hb + 8u * (uint32_t)(j % 3));
+    }
+  };
+  const double *gpf = gb + gst;                    // rows of the next prefetch (step 1, 2, ...)
+  const double *vpf = ob + ost;
+  auto prefetch = [&](int i) {  // this thread's g_i (and v_i) points -> ring slot i % D
+    if (i <= N && active) {
+      double *gs = gring + (i % D) * GW + tid * P;
+#pragma unroll
+      for (int p = 0; p < P; p += 2) cp_async16(gs + p, gpf + p);
+      if (own) {
+        double *vs = vring + (i % D) * Wc + l0;
+#pragma unroll
+        for (int p = 0; p < P; p += 2) cp_async16(vs + p, vpf + p);
+      }
+    }
+    gpf += gst;
+    vpf += ost;
+    cp_async_commit();
+  };
+  for (int q = tid; q < 2 * BL; q += nthr) smem[q] = 0.0;  // margins stay finite
+  if (tid == 0) {
+    for (int k = 0; k < 3; ++k) mbar_init(&hb[k], 1);
+    fence_mbar_init();
+    for (int k = 0; k < 3; ++k) mbar_expect_tx(&hb[k], hbytes);
+  }
+  double x[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) x[p] = (own && a.state_in) ? a.state_in[gx + p] : 0.0;
+  for (int i = 1; i < D; ++i) prefetch(i);
+  cluster.sync();  // buffers zeroed, barriers armed everywhere before any remote store
+  if (own) put(smem, x);
+  send(0, x);
+  int j = 0, k = 0;                                // super-step j, local step k (1..S)
+#pragma unroll 1
+  for (int i = 1; i <= N; ++i) {
+    double *cur = smem + ((i - 1) & 1) * BL, *nxt = smem + (i & 1) * BL;
+    if (k == 0) {  // start of super-step j: halo threads take x_{jS} from R[j&1]
+      if (lhalo || rhalo) {
+        mbar_wait(&hb[j % 3], (uint32_t)((j / 3) & 1));
+        const double *rj = R + (j & 1) * CS::EMAX + (lhalo ? EL + l0 : EL + (l0 - Wc));
+        double h[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) h[p] = rj[p];
+        put(cur, h);
+      }
+      if (tid == 0) mbar_expect_tx(&hb[j % 3], hbytes);  // re-arm for exchange j + 3
+      __syncthreads();
+    }
+    ++k;
+    prefetch(i + D - 1);
+    cp_async_wait<D - 1>();                        // this thread's rows of step i landed
+    if (active) {
+      double y[P];
+      if constexpr (NU4 <= 32) {
+        psi_soa_dispatch<P, COLS, NU4>(cur, q0 + o0, a.op, y);
+      } else {
+        psi_soa_chunked<P, COLS>(cur, q0 + o0, a.op, y);
+      }
+      const double *gs = gring + (i % D) * GW + tid * P;
+#pragma unroll
+      for (int p = 0; p < P; ++p) x[p] = y[p] + gs[p];   // x_i = Psi x_{i-1} + g_i
+      put(nxt, x);
+      if (own) {
+        if (k == S || i == N) send(j + 1, x);      // exact own values of x_{(j+1)S}
+        const double *vs = vring + (i % D) * Wc + l0;
+        double *orow = ob + (long long)i * ost;
+#pragma unroll
+        for (int p = 0; p < P; p += 2)             // u_i = v_i + e_i
+          *reinterpret_cast<double2 *>(orow + p) = make_double2(vs[p] + x[p], vs[p + 1] + x[p + 1]);
+      }
+    }
+    if (k == S) { k = 0; ++j; }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  if (own && a.state_out) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) a.state_out[gx + p] = x[p];
+  }
+  // the last exchange may still be landing here: wait for it, keep shared memory alive
+  const int jl = k == 0 ? j : j + 1;
+  if (tid == 0) mbar_wait(&hb[jl % 3], (uint32_t)((jl / 3) & 1));
+  cluster.sync();
+}
+
+template <int NT, int P, int CL, int NU4>
+static cudaError_t launch_seq_ca_nu(const CoarseArgs &a, int S, int nthr, cudaStream_t s) {
+  const size_t smem = CaSmem<NT, P>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(psi_seq_cluster_ca_kernel<NT, P, CL, NU4>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (CL > 8)
+      cudaFuncSetAttribute(psi_seq_cluster_ca_kernel<NT, P, CL, NU4>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  psi_seq_cluster_ca_kernel<NT, P, CL, NU4><<<CL, nthr, smem, s>>>(a, S);
+  return cudaGetLastError();
+}
+
+template <int NT, int P, int CL>
+static cudaError_t launch_seq_ca(const CoarseArgs &a, int S, cudaStream_t s) {
+  const int o0 = a.op.o0, nu = a.op.nu;
+  const int HL = o0 < 0 ? std::max(-o0, 1) : 1, HR = std::max(o0 + nu - 1, 1);
+  const int EL = ((S * HL + P - 1) / P) * P, ER = ((S * HR + P - 1) / P) * P;
+  const int nthr = NT + (((EL + ER) / P + 31) / 32) * 32;
+  if (nu <= 12) return launch_seq_ca_nu<NT, P, CL, 12>(a, S, nthr, s);
+  if (nu <= 16) return launch_seq_ca_nu<NT, P, CL, 16>(a, S, nthr, s);
+  if (nu <= 20) return launch_seq_ca_nu<NT, P, CL, 20>(a, S, nthr, s);
+  if (nu <= 24) return launch_seq_ca_nu<NT, P, CL, 24>(a, S, nthr, s);
+  if (nu <= 28) return launch_seq_ca_nu<NT, P, CL, 28>(a, S, nthr, s);
+  if (nu <= 32) return launch_seq_ca_nu<NT, P, CL, 32>(a, S, nthr, s);
+  return launch_seq_ca_nu<NT, P, CL, 64>(a, S, nthr, s);
+}
+
+// Largest s-step depth S <= smax with EL + ER <= 256 (and EL, ER <= Wc); 0: not possible.
+int seq_ca_depth(int cl, SweepCfg c, int nx, int o0, int nu, int smax) {
+  if (cl < 2 || cl > 16 || cl * c.nt_threads * c.p != nx || c.p % 2) return 0;
+  const int HL = o0 < 0 ? std::max(-o0, 1) : 1, HR = std::max(o0 + nu - 1, 1);
+  const int Wc = c.nt_threads * c.p;
+  for (int S = smax; S >= 2; --S) {
+    const int EL = ((S * HL + c.p - 1) / c.p) * c.p, ER = ((S * HR + c.p - 1) / c.p) * c.p;
+    if (EL + ER <= 256 && EL <= Wc && ER <= Wc && (EL + ER) / c.p <= 128) return S;
+  }
+  return 0;
+}
+
+cudaError_t launch_psi_seq_cluster_ca(int cl, SweepCfg c, int S, const CoarseArgs &a, cudaStream_t s) {
+  if (a.nsteps <= 0) return cudaSuccess;
+  if (cl == 8 && c.nt_threads == 64 && c.p == 2) return launch_seq_ca<64, 2, 8>(a, S, s);
+  if (cl == 16 && c.nt_threads == 128 && c.p == 2) return launch_seq_ca<128, 2, 16>(a, S, s);
+  if (cl == 8 && c.nt_threads == 256 && c.p == 2) return launch_seq_ca<256, 2, 8>(a, S, s);
+  if (cl == 16 && c.nt_threads == 32 && c.p == 2) return launch_seq_ca<32, 2, 16>(a, S, s);
+  if (cl == 8 && c.nt_threads == 128 && c.p == 4) return launch_seq_ca<128, 4, 8>(a, S, s);
+  if (cl == 16 && c.nt_threads == 64 && c.p == 4) return launch_seq_ca<64, 4, 16>(a, S, s);
+  if (cl == 8 && c.nt_threads == 32 && c.p == 4) return launch_seq_ca<32, 4, 8>(a, S, s);
+  return cudaErrorInvalidConfiguration;
 }
 
 // nx = CL * NT * P; the halos (-o0, o0+nu-1) must be <= 64 and <= NT*P (host-checked).

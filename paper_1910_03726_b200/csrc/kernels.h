@@ -88,6 +88,9 @@ cudaError_t launch_psi_seq_periodic(SweepCfg cfg, const CoarseArgs &a, cudaStrea
 // barrier per step).  nx == cl * NT * P.
 cudaError_t launch_psi_seq_cluster(int cl, SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);
 bool seq_cluster_ok(int cl, SweepCfg cfg, int nx, int o0, int nu);
+// Communication-avoiding variant: S steps per halo exchange (extended halos S*HL, S*HR).
+cudaError_t launch_psi_seq_cluster_ca(int cl, SweepCfg cfg, int S, const CoarseArgs &a, cudaStream_t s);
+int seq_ca_depth(int cl, SweepCfg cfg, int nx, int o0, int nu, int smax);
 
 // Level-l (l >= 2) relaxation sweep of the V-cycle with Psi_l and RHS g (u = 0 start):
 //   phase 1: x_i = Psi x_{i-1} + g[jm+i], i=1..m, x_0 = u_j (null: 0) -> v_{j+1}

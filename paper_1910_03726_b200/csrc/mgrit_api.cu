@@ -539,9 +539,9 @@ int reduce_norm(mgrit_ctx *c, long long n, double *norm2_host) {
 // Long chains (two-level): the row split over a thread-block cluster (DSMEM halos), else
 // one periodic CTA.
 struct CoarsePlan {
-  enum Kind { NONE, TILES, CLUSTER, SEQ } kind = NONE;
+  enum Kind { NONE, TILES, CLUSTER, CLUSTER_CA, SEQ } kind = NONE;
   SweepCfg cfg = {0, 0};
-  int ntiles = 1, cl = 0;
+  int ntiles = 1, cl = 0, S = 0;
 };
 static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
   CoarsePlan pl;
@@ -556,13 +556,32 @@ static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
   }
   if (!(choose_psi(c->nx, 0, true, pc) && pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx))
     return pl;
-  int cl = 0;
+  // 16-CTA clusters (measured, profiles/README.md): 4 points per thread for narrow
+  // stencils, 2 for wide ones (register window), s-step depth 8 / 4.
+  int cl = 0, smax = 8;
   SweepCfg cc = {0, 0};
-  if (c->nx == 4096) { cl = 8; cc = {256, 2}; }
-  else if (c->nx == 1024) { cl = 8; cc = {64, 2}; }
+  if (c->nx == 4096) {
+    cl = 16;
+    cc = op.nu <= 16 ? SweepCfg{64, 4} : SweepCfg{128, 2};
+    smax = op.nu <= 16 ? 8 : 4;
+  } else if (c->nx == 1024) {
+    cl = 16;
+    cc = {32, 2};
+  }
   if (const char *env = getenv("MGRIT_SEQ_CLUSTER")) {
     cl = 0;
     sscanf(env, "%d,%d,%d", &cl, &cc.nt_threads, &cc.p);
+  }
+  if (const char *env = getenv("MGRIT_SEQ_S")) smax = atoi(env);
+  if (smax >= 2) {
+    const int S = seq_ca_depth(cl, cc, c->nx, op.o0, op.nu, smax);
+    if (S >= 2) {
+      pl.kind = CoarsePlan::CLUSTER_CA;
+      pl.cfg = cc;
+      pl.cl = cl;
+      pl.S = S;
+      return pl;
+    }
   }
   if (seq_cluster_ok(cl, cc, c->nx, op.o0, op.nu)) {
     pl.kind = CoarsePlan::CLUSTER;
@@ -616,6 +635,8 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
   switch (pl.kind) {
     case CoarsePlan::CLUSTER:
       return run(c, 2, [&] { return launch_psi_seq_cluster(pl.cl, pl.cfg, a, c->stream); });
+    case CoarsePlan::CLUSTER_CA:
+      return run(c, 2, [&] { return launch_psi_seq_cluster_ca(pl.cl, pl.cfg, pl.S, a, c->stream); });
     case CoarsePlan::SEQ:
       return run(c, 2, [&] { return launch_psi_seq_periodic(pl.cfg, a, c->stream); });
     default:
@@ -1166,7 +1187,10 @@ int mgrit_describe(const mgrit_ctx *c, char *buf, size_t len) {
   char coarse[96] = "rk_coarse_kernel";
   if (c->psi_kind == MGRIT_PSI_STENCIL) {
     const CoarsePlan pl = plan_coarse(c, c->levels - 1);
-    if (pl.kind == CoarsePlan::CLUSTER)
+    if (pl.kind == CoarsePlan::CLUSTER_CA)
+      snprintf(coarse, sizeof(coarse), "psi_seq_cluster_ca_kernel<NT=%d,P=%d,CL=%d,S=%d>",
+               pl.cfg.nt_threads, pl.cfg.p, pl.cl, pl.S);
+    else if (pl.kind == CoarsePlan::CLUSTER)
       snprintf(coarse, sizeof(coarse), "psi_seq_cluster_kernel<NT=%d,P=%d,CL=%d>", pl.cfg.nt_threads,
                pl.cfg.p, pl.cl);
     else if (pl.kind == CoarsePlan::SEQ)

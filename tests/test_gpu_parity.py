@@ -167,23 +167,26 @@ def test_coarse_correction_primitive(order, tab, cfl, nx, nt, m, nu):
     assert _rel(Ug.cpu().numpy(), Uo) <= REL
 
 
-@pytest.mark.parametrize("nx,o0,nu,cluster", [
-    (4096, -7, 15, None),            # cfg3-like: default 8 CTAs x 128 threads x 4 points
-    (4096, -4, 9, "16,64,4"),        # 16-CTA (non-portable) cluster
-    (4096, -24, 37, None),           # wide thresholded stencil (cfg4-like)
-    (4096, 0, 11, None),             # one-sided (right halo only)
-    (4096, -12, 12, None),           # one-sided (left halo only)
-    (4096, -14, 15, None),           # cfg3's shape: one-sided, 14-point left halo
-    (1024, -4, 9, None),             # cfg2-like: 8 CTAs x 64 threads x 2 points
-    (1024, -5, 11, "8,64,2"),
+@pytest.mark.parametrize("nx,o0,nu,env", [
+    (4096, -7, 15, {}),                                   # default s-step cluster solve
+    (4096, -4, 9, {"MGRIT_SEQ_CLUSTER": "16,128,2"}),     # 16-CTA (non-portable) cluster
+    (4096, -24, 37, {}),                                  # wide stencil (chunked window)
+    (4096, 0, 11, {"MGRIT_SEQ_S": "5"}),                  # one-sided (right), odd depth
+    (4096, -12, 12, {"MGRIT_SEQ_S": "16"}),               # one-sided (left), deep
+    (4096, -14, 15, {}),                                  # cfg3's shape
+    (4096, -14, 15, {"MGRIT_SEQ_S": "0"}),                # step-by-step exchange kernel
+    (4096, -30, 32, {"MGRIT_SEQ_S": "0", "MGRIT_SEQ_CLUSTER": "8,128,4"}),
+    (1024, -4, 9, {}),                                    # cfg2-like: 8 x 64 x 2
+    (1024, -5, 11, {"MGRIT_SEQ_CLUSTER": "16,32,2", "MGRIT_SEQ_S": "3"}),
+    (1024, -5, 11, {"MGRIT_SEQ_S": "2"}),
 ])
-def test_coarse_correction_cluster(nx, o0, nu, cluster, monkeypatch):
+def test_coarse_correction_cluster(nx, o0, nu, env, monkeypatch):
     """Two-level coarse correction through the thread-block-cluster sequential solve
     (row split over 8/16 SMs, DSMEM halos): e_j = Psi e_{j-1} + r_j, U[jm] += e_j, then
     F-relaxation vs the oracle, for halo shapes on both / one side."""
     B = _cuda()
-    if cluster:
-        monkeypatch.setenv("MGRIT_SEQ_CLUSTER", cluster)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     order, tab, cfl, m = 3, "erk3_kutta", 0.85, 4
     nt = 2048 if nx == 4096 else 1024   # coarse chain long enough for the cluster path
     phi = D.make_phi(order, tab, cfl, nx)
@@ -203,7 +206,7 @@ def test_coarse_correction_cluster(nx, o0, nu, cluster, monkeypatch):
     M.f_relax(Uo, phi, m)
     s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2,
                 [{"kind": "stencil", "offsets": offsets, "coeffs": list(coeffs)}], "FCF")
-    assert "coarse=psi_seq_cluster_kernel" in s.describe(), s.describe()
+    assert "coarse=psi_seq_cluster" in s.describe(), s.describe()
     Ug = torch.from_numpy(U).cuda()
     s.coarse_solve_full(Ug)
     assert _rel(Ug.cpu().numpy(), Uo) <= REL
@@ -218,7 +221,7 @@ def test_coarse_solve_deterministic(wname):
     from paper_1910_03726_b200 import problem
     w = W.ALL[wname]
     s = problem.make_solver(w)
-    assert "coarse=psi_seq_cluster_kernel" in s.describe(), s.describe()
+    assert "coarse=psi_seq_cluster" in s.describe(), s.describe()
     U0 = problem.device_guess(w)
     s.relax_full(U0, "F")
     outs = []
