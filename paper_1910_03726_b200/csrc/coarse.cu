@@ -539,8 +539,6 @@ static cudaError_t launch_seq_cluster_nu(const CoarseArgs &a, cudaStream_t s) {
 template <int NT, int P, int CL>
 static cudaError_t launch_seq_cluster(const CoarseArgs &a, cudaStream_t s) {
   const int nu = a.op.nu;
-  if (NT == 128 && P == 4 && nu <= 16 && getenv("MGRIT_SEQ_D8"))
-    return launch_seq_cluster_nu<NT, P, CL, 16, 8>(a, s);
   if (nu <= 12) return launch_seq_cluster_nu<NT, P, CL, 12>(a, s);
   if (nu <= 16) return launch_seq_cluster_nu<NT, P, CL, 16>(a, s);
   if (nu <= 20) return launch_seq_cluster_nu<NT, P, CL, 20>(a, s);
@@ -1266,168 +1264,9 @@ static cudaError_t launch_level_one(const PsiSweepArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Persistent V-cycle level sweep (zero initial guess, no comparison row): the CTA walks
-// items with a grid stride and prefetches the next item's m g-rows into the other of two
-// row sets while the current item steps, so HBM streaming never waits on a CTA start.
-template <int NT, int P, int NU>
-__global__ void __launch_bounds__(NT) psi_level_persist_kernel(const __grid_constant__ PsiSweepArgs a) {
-  static_assert(P % 2 == 1, "contiguous windows need odd P");
-  using L = LevelSmem<NT, P>;
-  constexpr int W = L::W, WB = L::WB;
-  constexpr int MR = 4;                        // rows per set (m <= 4)
-  extern __shared__ __align__(128) double smem[];
-  double *X = smem;
-  double *RB = smem + 2 * L::X;                // [2][MR][WB]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(RB + 2 * MR * WB);
-  const int nx = a.nx, tid = threadIdx.x, m = a.m;
-  const int half = nx >> 1;
-  const int total = a.nitems * a.ntiles;
-  const int o0 = a.op.o0;
-  auto tile_beg = [&](int t) { return 2 * (int)(((long long)t * half) / a.ntiles); };
-  // origin of step i of an item: S_i = abeg + (N - i) o0 (mod nx), N = 2m (m if no phase 2)
-  auto origin = [&](int abeg, int N, int i) { return wrapi((long long)abeg + (long long)(N - i) * o0, nx); };
-  auto issue_item = [&](int w, int set) {      // thread 0: g rows jm+1..jm+m of item w
-    const int item = w / a.ntiles, tile = w - item * a.ntiles;
-    const int abeg = tile_beg(tile);
-    const int N = item < a.p2_items ? 2 * m : m;
-    const long long g0 = a.g.off + (long long)item * a.g.stride;
-    for (int k = 0; k < m; ++k) {
-      const double *row = a.g.base + (g0 + k + 1) * nx;
-      const int S0 = origin(abeg, N, k + 1) & ~1;
-      const int n1 = (S0 + WB <= nx) ? WB : nx - S0;
-      double *dst = RB + (set * MR + k) * WB;
-      uint64_t *b = &bar[set * MR + k];
-      mbar_expect_tx(b, (uint32_t)WB * 8u);
-      tma_load_1d(dst, row + S0, (uint32_t)n1 * 8u, b);
-      if (n1 < WB) tma_load_1d(dst + n1, row, (uint32_t)(WB - n1) * 8u, b);
-    }
-  };
-  if (tid == 0) {
-    for (int k = 0; k < 2 * MR; ++k) mbar_init(&bar[k], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0 && (int)blockIdx.x < total) issue_item(blockIdx.x, 0);
-  int sx = 0, it = 0;
-#pragma unroll 1
-  for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-    const int set = it & 1;
-    const uint32_t par = (uint32_t)((it >> 1) & 1);
-    const int item = w / a.ntiles, tile = w - item * a.ntiles;
-    const int abeg = tile_beg(tile);
-    const int T = tile_beg(tile + 1) - abeg;
-    const bool p2 = item < a.p2_items;
-    const int N = p2 ? 2 * m : m;
-    __syncthreads();                           // item it-1's scalar stores read set^1
-    if (tid == 0) {
-      bulk_wait_read_all();                    // ... and its bulk stores have read it too
-      const int nw = w + gridDim.x;
-      if (nw < total) issue_item(nw, set ^ 1);
-    }
-    auto store = [&](double *row, int S, const double(&v)[P], double *buf) {
-      const int so = S & 1;
-      double *st = buf + so;
-#pragma unroll
-      for (int p = 0; p < P; ++p) st[tid * P + p] = v[p];
-      fence_proxy_async();
-      __syncthreads();
-      int segs[2][2];
-      int ns = 1;
-      if (S + T <= nx) { segs[0][0] = S; segs[0][1] = S + T; }
-      else { segs[0][0] = S; segs[0][1] = nx; segs[1][0] = 0; segs[1][1] = S + T - nx; ns = 2; }
-      int scalar = 0;
-      for (int k = 0; k < ns; ++k) {
-        int ga = segs[k][0], gb = segs[k][1];
-        const int base = so + (k == 0 ? -S : nx - S);
-        if (ga < gb && (ga & 1)) {
-          if (tid == 1 + scalar) row[ga] = buf[base + ga];
-          ++scalar;
-          ++ga;
-        }
-        if (ga < gb && ((gb - ga) & 1)) {
-          if (tid == 1 + scalar) row[gb - 1] = buf[base + gb - 1];
-          ++scalar;
-          --gb;
-        }
-        if (tid == 0 && gb > ga) tma_store_1d(row + ga, buf + base + ga, (uint32_t)(gb - ga) * 8u);
-      }
-      if (tid == 0) bulk_commit();
-    };
-    auto psi_step = [&](double(&y)[P], const double(&xin)[P]) {
-      double *Xb = X + (sx & 1) * L::X;
-      psi_put_c<NT, P>(Xb, xin);
-      __syncthreads();
-      psi_apply_any<P, NU>(Xb, tid * P, a.op, y);
-      ++sx;
-    };
-    double x[P];
-    // step 1 from the zero state: x_1 = g[jm+1]
-    {
-      mbar_wait(&bar[set * MR + 0], par);
-      const double *sg = RB + (set * MR + 0) * WB + (origin(abeg, N, 1) & 1);
-#pragma unroll
-      for (int p = 0; p < P; ++p) x[p] = 0.0 + sg[tid * P + p];
-    }
-#pragma unroll 1
-    for (int i = 2; i <= m; ++i) {
-      double y[P];
-      psi_step(y, x);
-      mbar_wait(&bar[set * MR + i - 1], par);
-      const double *sg = RB + (set * MR + i - 1) * WB + (origin(abeg, N, i) & 1);
-#pragma unroll
-      for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * P + p];
-    }
-    store(const_cast<double *>(a.v.base) + (a.v.off + (long long)item * a.v.stride) * nx,
-          origin(abeg, N, m), x, RB + (set * MR + 0) * WB);   // v_{j+1} (slot of g_1)
-    if (p2) {
-#pragma unroll 1
-      for (int i = m + 1; i <= 2 * m; ++i) {
-        double y[P];
-        psi_step(y, x);
-#pragma unroll
-        for (int p = 0; p < P; ++p) x[p] = y[p];
-      }
-      store(const_cast<double *>(a.r2.base) + (a.r2.off + (long long)item * a.r2.stride) * nx,
-            origin(abeg, N, 2 * m), x, RB + (set * MR + 1) * WB);  // r_{j+2} (slot of g_2)
-    }
-  }
-  if (tid == 0) bulk_wait_all();
-}
-
-template <int NT, int P, int NU>
-static cudaError_t launch_level_persist_one(const PsiSweepArgs &a, cudaStream_t s) {
-  using L = LevelSmem<NT, P>;
-  const size_t smem = sizeof(double) * (2 * L::X + 2 * 4 * (size_t)L::WB + 16) + 64;
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(psi_level_persist_kernel<NT, P, NU>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, psi_level_persist_kernel<NT, P, NU>,
-                                                  NT, smem);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long total = (long long)a.nitems * a.ntiles;
-  if (total <= 0) return cudaSuccess;
-  const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
-  psi_level_persist_kernel<NT, P, NU><<<(unsigned)grid, NT, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_psi_level_tma(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s) {
   if (a.m > 4 || (a.nx & 1)) return cudaErrorInvalidValue;
   if (c.nt_threads != 128 || c.p != 9) return cudaErrorInvalidConfiguration;
-  if (!a.interp && !a.u.base && !a.ucmp.base) {  // coarse-level sweep: persistent variant
-    switch (a.op.nu) {
-      case 9: return launch_level_persist_one<128, 9, 9>(a, s);
-      case 13: return launch_level_persist_one<128, 9, 13>(a, s);
-      case 17: return launch_level_persist_one<128, 9, 17>(a, s);
-      case 21: return launch_level_persist_one<128, 9, 21>(a, s);
-      default: return launch_level_persist_one<128, 9, 0>(a, s);
-    }
-  }
   switch (a.op.nu) {
     case 9: return launch_level_one<128, 9, 9>(a, s);
     case 13: return launch_level_one<128, 9, 13>(a, s);
