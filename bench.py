@@ -207,6 +207,23 @@ def run_ours(args, w):
     avg_ms = ms_f / max(n_f, 1)
     achieved = flops / (avg_ms / 1e3) / 1e12
     shares = {k: round(v[1] / max(ms_total, 1e-9), 4) for k, v in prof.items()}
+    # ---- sequential coarse solve: ns per coarse step vs its FP64 floor ----
+    desc = s.describe()
+    n_c, ms_c = prof["coarse_solve"]
+    nsteps_c = w.nt // (w.m ** (w.levels - 1))
+    coarse = {"kernel": desc.split("coarse=")[-1], "launches": n_c,
+              "steps_per_launch": nsteps_c,
+              "ns_per_step": round(ms_c / max(n_c, 1) / nsteps_c * 1e6, 1) if n_c else None}
+    if w.psi_kind == "stencil" and n_c:
+        ops = psi[-1]
+        nu = ops["offsets"][-1] - ops["offsets"][0] + 1
+        cl = 1
+        if "CL=" in desc:
+            cl = int(desc.split("CL=")[1].split(",")[0].split(">")[0])
+        elif "tiles=" in coarse["kernel"]:
+            cl = min(148, int(coarse["kernel"].split("tiles=")[1].split()[0]))
+        floor = nu * w.nx * 2 / (cl * FP64_PEAK_TFLOPS * 1e12 / 148) * 1e9
+        coarse.update({"taps": nu, "sms": cl, "fp64_floor_ns_per_step": round(floor, 1)})
 
     # ---- end to end through the public API with host buffers -----------------------
     e2e = None
@@ -257,6 +274,8 @@ def run_ours(args, w):
                      "avg_launch_ms": round(avg_ms, 4), "launches": n_f,
                      "flops_per_launch": flops},
         "kernel_time_share": shares,
+        "relax_kernel_rate": round(dof * world / (ms_f / max(args.steps, 1) / 1e3), 1) if ms_f else None,
+        "coarse_solve": coarse,
         "gpu_launches": int(launches),
         "e2e": e2e,
     }
