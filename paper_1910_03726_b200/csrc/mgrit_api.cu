@@ -405,7 +405,8 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
   HL += HL & 1;
   const int HR = steps * S * rk_scheme_reach_right(c->scheme);
   int tcand[][3] = {{128, 15, 0}, {256, 11, 0}};
-  if (const char *env = getenv("MGRIT_FINE_TILE")) {  // experiments: "NT,P[,minBlocks]"
+  const char *env = steps == 2 * c->m ? getenv("MGRIT_FINE_TILE") : nullptr;
+  if (env) {  // experiments on the FCF sweep: "NT,P[,minBlocks]"
     int nt_ = 0, p_ = 0, mb_ = 0;
     if (sscanf(env, "%d,%d,%d", &nt_, &p_, &mb_) >= 2) {
       tcand[0][0] = nt_; tcand[0][1] = p_; tcand[0][2] = mb_;
