@@ -1042,16 +1042,14 @@ __device__ __forceinline__ void psi_apply_c(const double *__restrict__ s, int ba
   }
 }
 
-template <int NT, int P>
-__device__ __forceinline__ void psi_put_c(double *s, const double (&x)[P]) {
-  constexpr int W = NT * P;
-  const int t = threadIdx.x;
+// Publish a thread's P values of a shifted-coordinate window.  No periodic tail: the
+// windows are tiles (W <= nx, T <= W - halo), and the reads past W only feed outputs
+// beyond the valid length, which shrinks by nu-1 per step.
+template <int P>
+__device__ __forceinline__ void psi_put_window(double *s, const double (&x)[P]) {
+  double *st = s + threadIdx.x * P;
 #pragma unroll
-  for (int p = 0; p < P; ++p) {
-    const int l = t * P + p;
-    s[l] = x[p];
-    if (l < PSI_EXT) s[W + l] = x[p];
-  }
+  for (int p = 0; p < P; ++p) st[p] = x[p];
 }
 
 // Compile-time tap count: the thread's whole input window (P + NU - 1 values) is read
@@ -1151,6 +1149,8 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
     mbar_wait(&bar[k], 0);
     return RB + k * WB + (S & 1);
   };
+  // parity of origin(i) (abeg and nx are even): all the step loop needs to find a slot
+  auto opar = [&](int i) { return ((N - i) * o0) & 1; };
   // out[S .. S+T) = v[q]  (or out += v[q] with `acc`: bulk reduce-add at L2), staged in
   // buffer `buf`, a consumed row.  No barrier before staging: each thread overwrites only
   // buffer positions it read itself in this step (same origin), or positions of a row
@@ -1207,7 +1207,7 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
   // buffer written next was last read two steps ago, before the previous barrier.
   auto psi_step = [&](double(&y)[P]) {
     double *Xb = X + (sx & 1) * L::X;
-    psi_put_c<NT, P>(Xb, x);
+    psi_put_window<P>(Xb, x);
     __syncthreads();
     psi_apply_any<P, NU>(Xb, tid * P, a.op, y);
     ++sx;
@@ -1217,7 +1217,7 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
     double y[P];
     psi_step(y);
     const int kg = interp ? i : i - 1;
-    const double *sg = slot(kg, origin(i));
+    const double *sg = slot(kg, opar(i));
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = y[p] + sg[tid * P + p];
     if (interp)  // out[jm+i] += x_i  (staged in place of the consumed g row)
@@ -1229,7 +1229,7 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
     store(const_cast<double *>(rowp(a.v, item)), origin(m), x, false, RB);  // slot of g_1
     if (p2) {
       if (a.ucmp.base) {
-        const double *sc = slot(k_ucmp, origin(m));
+        const double *sc = slot(k_ucmp, opar(m));
 #pragma unroll
         for (int p = 0; p < P; ++p) x[p] -= sc[tid * P + p];
       }
