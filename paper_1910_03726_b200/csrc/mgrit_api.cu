@@ -199,31 +199,40 @@ bool make_sdirk(const double *z, int zlo, int zn, double a, int P, int nx, Sdirk
   const int deg = (int)q.size() - 1;
   const int NL = -zlo;
   auto roots = poly_roots(q);
-  long double gamma_inv = q[deg];
+  std::complex<long double> gamma_inv = q[deg];
+  // real roots -> first-order factors; complex roots come in conjugate pairs -> one complex
+  // factor each (sdirk.cuh), represented by the member with positive imaginary part
+  std::vector<long double> rs;
+  std::vector<std::complex<long double>> cs;
   int nin = 0;
   for (auto &r : roots) {
-    if (std::fabs((double)r.imag()) > 1e-12 * std::max(1.0, (double)std::abs(r))) {
-      why = "complex roots in the SDIRK stage matrix";
-      return false;
+    const bool inside = std::abs(r) < 1.0L;
+    if (inside) ++nin;
+    if (std::fabs((double)r.imag()) <= 1e-12 * std::max(1.0, (double)std::abs(r))) {
+      if (!inside) gamma_inv *= -r.real();
+      rs.push_back(r.real());
+    } else {
+      if (!inside) gamma_inv *= -r;  // the pair contributes |r|^2 (real)
+      if (r.imag() > 0) cs.push_back(r);
     }
-    const long double rr = r.real();
-    if (std::fabs(rr) < 1.0L) ++nin;
-    else gamma_inv *= -rr;
+  }
+  if (2 * cs.size() + rs.size() != roots.size()) {
+    why = "unpaired complex roots in the SDIRK stage matrix";
+    return false;
   }
   if (nin != NL) {
     why = "stage matrix winding number != 0";
     return false;
   }
-  if (deg > MAXREC) {
+  if ((int)rs.size() > MAXREC || (int)cs.size() > MAXCREC) {
     why = "too many stage-matrix factors";
     return false;
   }
-  sd.gamma = (double)(1.0L / gamma_inv);
-  sd.nrec = deg;
+  sd.gamma = (double)(1.0L / gamma_inv.real());
+  sd.nrec = (int)rs.size();
+  sd.ncrec = (int)cs.size();
   int k = 0;
   // forward (inside) factors first, then backward (outside), in increasing |root|
-  std::vector<long double> rs;
-  for (auto &r : roots) rs.push_back(r.real());
   std::sort(rs.begin(), rs.end(), [](long double x, long double y) { return std::fabs(x) < std::fabs(y); });
   for (long double rr : rs) {
     RecCoef &rc = sd.rec[k++];
@@ -242,6 +251,31 @@ bool make_sdirk(const double *z, int zlo, int zn, double a, int P, int nx, Sdirk
       pj *= rP;
     }
     rc.closure = (double)(1.0L / (1.0L - powl(rho, (long double)nx)));
+  }
+  k = 0;
+  for (auto &r : cs) {
+    CRecCoef &rc = sd.crec[k++];
+    const bool bwd = std::abs(r) >= 1.0L;
+    const std::complex<long double> one(1.0L, 0.0L);
+    const std::complex<long double> rho = bwd ? one / r : r;
+    rc.backward = bwd ? 1 : 0;
+    std::complex<long double> pk = one;
+    for (int i = 0; i <= P; ++i) {
+      rc.rpr[i] = (double)pk.real();
+      rc.rpi[i] = (double)pk.imag();
+      pk *= rho;
+    }
+    const std::complex<long double> rP = std::pow(rho, (long double)P);
+    std::complex<long double> pj = one;
+    for (int j = 0; j <= 32; ++j) {
+      rc.rcr[j] = (double)pj.real();
+      rc.rci[j] = (double)pj.imag();
+      pj *= rP;
+    }
+    const std::complex<long double> cl = one / (one - std::pow(rho, (long double)nx));
+    rc.clr = (double)cl.real();
+    rc.cli = (double)cl.imag();
+    rc.ratio = (double)(rho.real() / rho.imag());
   }
   return true;
 }

@@ -11,6 +11,10 @@
 // the CTA: a sequential pass over the thread's P points, a warp-shuffle scan of the
 // chunk carries, a cross-warp pass, and the rank-1 periodic (Sherman-Morrison)
 // closure c_0 = S / (1 - rho^N).  One __syncthreads per bidiagonal solve.
+// A complex-conjugate root pair (SDIRK2+U2, SDIRK4+U4) is one complex recurrence on the
+// real right-hand side: by partial fractions
+//   (1 - rho s)^-1 (1 - conj(rho) s)^-1 f = Im(rho y) / Im(rho),  y = (1 - rho s)^-1 f
+// (s = E^-1 forward, E backward), since (1 - conj(rho) s)^-1 f = conj(y) for real f.
 #pragma once
 #include "device.cuh"
 
@@ -27,11 +31,23 @@ struct RecCoef {
   int pad;
 };
 
+constexpr int MAXCREC = 2;
+
+struct CRecCoef {            // complex rho = (re, im), |rho| < 1
+  double rpr[MAXP + 1], rpi[MAXP + 1];   // rho^k
+  double rcr[33], rci[33];               // (rho^P)^j
+  double clr, cli;                       // 1 / (1 - rho^N)
+  double ratio;                          // Re(rho) / Im(rho)
+  int backward;
+  int pad;
+};
+
 struct SdirkCoef {
   int nrec;
-  int pad;
+  int ncrec;
   double gamma;            // M^-1 = gamma * prod (bidiagonal inverses)
   RecCoef rec[MAXREC];
+  CRecCoef crec[MAXCREC];  // one per complex-conjugate root pair
 };
 
 // In-place periodic first-order recurrence over the CTA's whole row (W == nx).
@@ -93,11 +109,117 @@ __device__ __forceinline__ void periodic_recurrence(double (&f)[P], const RecCoe
   wphase ^= 1;
 }
 
+// Complex multiply-add helpers: (ar + i ai)(br + i bi) + (cr + i ci).
+__device__ __forceinline__ void cfma(double ar, double ai, double br, double bi, double &cr,
+                                     double &ci) {
+  const double r = fma(ar, br, fma(-ai, bi, cr));
+  ci = fma(ar, bi, fma(ai, br, ci));
+  cr = r;
+}
+
+// In-place periodic complex-pair solve over the CTA's whole row: f <- Im(rho y)/Im(rho)
+// with y the periodic solution of y_i = rho y_{i-1} + f_i (backward: y_{i+1}).
+template <int P, int NT>
+__device__ __forceinline__ void periodic_recurrence_cplx(double (&f)[P], const CRecCoef &rc,
+                                                         double *wbuf, int &wphase) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double rr = rc.rpr[1], ri = rc.rpi[1];
+  const double mr = rc.rcr[32], mi = rc.rci[32];
+  double *wb = wbuf + wphase * 2 * NW;            // [NW] re, [NW] im
+  double lr[P], li[P];
+  const bool bwd = rc.backward != 0;
+  if (!bwd) {
+    lr[0] = f[0];
+    li[0] = 0.0;
+#pragma unroll
+    for (int p = 1; p < P; ++p) {
+      lr[p] = f[p];
+      li[p] = 0.0;
+      cfma(rr, ri, lr[p - 1], li[p - 1], lr[p], li[p]);
+    }
+  } else {
+    lr[P - 1] = f[P - 1];
+    li[P - 1] = 0.0;
+#pragma unroll
+    for (int p = P - 2; p >= 0; --p) {
+      lr[p] = f[p];
+      li[p] = 0.0;
+      cfma(rr, ri, lr[p + 1], li[p + 1], lr[p], li[p]);
+    }
+  }
+  // chunk carry of this thread, scanned across the warp
+  double Ar = bwd ? lr[0] : lr[P - 1], Ai = bwd ? li[0] : li[P - 1];
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double vr = bwd ? __shfl_down_sync(FULL, Ar, d) : __shfl_up_sync(FULL, Ar, d);
+    const double vi = bwd ? __shfl_down_sync(FULL, Ai, d) : __shfl_up_sync(FULL, Ai, d);
+    if (bwd ? (lane + d < 32) : (lane >= d)) cfma(rc.rcr[d], rc.rci[d], vr, vi, Ar, Ai);
+  }
+  if (lane == (bwd ? 0 : 31)) {
+    wb[warp] = Ar;
+    wb[NW + warp] = Ai;
+  }
+  __syncthreads();
+  double tr = 0.0, ti = 0.0;
+  if (!bwd) {
+#pragma unroll 1
+    for (int v = 0; v < NW; ++v) {
+      double nr = wb[v], ni = wb[NW + v];
+      cfma(mr, mi, tr, ti, nr, ni);
+      tr = nr; ti = ni;
+    }
+  } else {
+#pragma unroll 1
+    for (int v = NW - 1; v >= 0; --v) {
+      double nr = wb[v], ni = wb[NW + v];
+      cfma(mr, mi, tr, ti, nr, ni);
+      tr = nr; ti = ni;
+    }
+  }
+  double cr = 0.0, ci = 0.0;                       // carry entering the first warp
+  cfma(tr, ti, rc.clr, rc.cli, cr, ci);
+  if (!bwd) {
+#pragma unroll 1
+    for (int v = 0; v < warp; ++v) {
+      double nr = wb[v], ni = wb[NW + v];
+      cfma(mr, mi, cr, ci, nr, ni);
+      cr = nr; ci = ni;
+    }
+  } else {
+#pragma unroll 1
+    for (int v = NW - 1; v > warp; --v) {
+      double nr = wb[v], ni = wb[NW + v];
+      cfma(mr, mi, cr, ci, nr, ni);
+      cr = nr; ci = ni;
+    }
+  }
+  const double Pr = bwd ? __shfl_down_sync(FULL, Ar, 1) : __shfl_up_sync(FULL, Ar, 1);
+  const double Pi = bwd ? __shfl_down_sync(FULL, Ai, 1) : __shfl_up_sync(FULL, Ai, 1);
+  double inr = cr, ini = ci;
+  if (lane != (bwd ? 31 : 0)) {
+    const int k = bwd ? 31 - lane : lane;
+    inr = Pr;
+    ini = Pi;
+    cfma(rc.rcr[k], rc.rci[k], cr, ci, inr, ini);
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int k = bwd ? P - p : p + 1;
+    double yr = lr[p], yi = li[p];
+    cfma(rc.rpr[k], rc.rpi[k], inr, ini, yr, yi);
+    f[p] = fma(rc.ratio, yi, yr);                   // Im(rho y) / Im(rho)
+  }
+  wphase ^= 1;
+}
+
 template <int P, int NT>
 __device__ __forceinline__ void stage_solve(double (&y)[P], const SdirkCoef &sd, double *wbuf,
                                             int &wphase) {
 #pragma unroll 1
   for (int k = 0; k < sd.nrec; ++k) periodic_recurrence<P, NT>(y, sd.rec[k], wbuf, wphase);
+#pragma unroll 1
+  for (int k = 0; k < sd.ncrec; ++k) periodic_recurrence_cplx<P, NT>(y, sd.crec[k], wbuf, wphase);
 #pragma unroll
   for (int p = 0; p < P; ++p) y[p] *= sd.gamma;
 }

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
   double *sB = sA + NT * SP;
   double *edge = sB + NT * SP;
   double *red = edge + 2 * NT * (SC::NL + SC::NR) + 2;
-  double *wbuf = red + NW + 2;  // 2*NW (SDIRK recurrences)
+  double *wbuf = red + NW + 2;  // 4*NW (SDIRK recurrences: 2 phases x complex)
   int wphase = 0;
 
   const int item = blockIdx.x / a.ntiles;
@@ -488,7 +488,7 @@ template <class SC, int NT, int P>
 static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int SP = Pad<P>::SP;
   const size_t smem = sizeof(double) * (2 * NT * SP + 2 * NT * (SC::NL + SC::NR) + 2 +
-                                        NT / 32 + 2 + 2 * (NT / 32) + 2);
+                                        NT / 32 + 2 + 4 * (NT / 32) + 2);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rk_sweep_kernel<SC, NT, P>,

@@ -80,6 +80,10 @@ PRIM = [  # (order, tableau, cfl, nx, nt, m)
     (1, "sdirk1", 4.0, 64, 32, 2),           # SDIRK: periodic banded stage solves
     (3, "sdirk3", 4.0, 256, 32, 4),
     (3, "sdirk3", 4.0, 4096, 16, 4),         # cfg4 width
+    (2, "sdirk2", 4.0, 256, 32, 4),          # complex-conjugate stage-matrix roots
+    (2, "sdirk2", 1.0, 1024, 16, 2),
+    (4, "sdirk4", 4.0, 1024, 32, 4),         # 5 stages, 2 real + 1 complex-pair factors
+    (4, "sdirk4", 8.0, 4096, 16, 4),
 ]
 
 
@@ -106,15 +110,14 @@ def test_relax_primitives(order, tab, cfl, nx, nt, m):
         assert _rel(Ug, Uo) <= REL, (kind, _rel(Ug, Uo))
 
 
-def test_sdirk_complex_roots_unsupported():
-    """SDIRK2+U2 / SDIRK4+U4 stage matrices have complex symbol roots: the library reports
-    EUNSUPPORTED instead of computing anything else."""
-    B = _cuda()
-    for order, tab in [(2, "sdirk2"), (4, "sdirk4")]:
-        with pytest.raises(B.MgritError) as e:
-            B.MGRIT(128, 32, 4, 1.0, 4.0, order, tab, 2,
-                    [{"kind": "stencil", "offsets": [0], "coeffs": [0.5]}], "FCF")
-        assert e.value.code == -5
+@pytest.mark.parametrize("order,tab,cfl", [(2, "sdirk2", 4.0), (4, "sdirk4", 4.0)])
+def test_sdirk_complex_pair_solve(order, tab, cfl):
+    """SDIRK2+U2 / SDIRK4+U4 (stage matrices with a complex-conjugate symbol-root pair,
+    solved as one complex periodic recurrence, sdirk.cuh): a two-level MGRIT solve with a
+    fitted Psi agrees with the oracle (iterates, history, K)."""
+    w = W.CFG4.scaled(256, 1024, order=order, tableau=tab, cfl=cfl)
+    res, rep = _solve_parity(w)
+    assert res["converged"]
 
 
 @pytest.mark.parametrize("order,tab,cfl,nx,nt,m", PRIM[:6])
