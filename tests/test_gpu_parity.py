@@ -314,6 +314,19 @@ def test_solve_cfg5_scaled_vcycle(nx, nt, levels):
     assert res["converged"]
 
 
+@pytest.mark.parametrize("label", ["m2_erk3", "m2_erk1", "m8_erk5", "m4_erk5_4lvl"])
+def test_solve_other_hierarchies(label):
+    """V-cycles beyond cfg5's shape: m = 2 coarsening, m = 8
+    multilevel (ERK5, non-TMA level sweeps), and a 4-level ERK5 hierarchy."""
+    w = {"m2_erk3": W.CFG5.scaled(256, 1024, m=2, levels=4, psi_widths=(7, 9, 11)),
+         "m2_erk1": W.CFG5.scaled(256, 512, order=1, tableau="erk1", m=2, levels=5,
+                                  psi_widths=(3, 5, 7, 9)),
+         "m8_erk5": W.CFG3.scaled(512, 4096, levels=3, psi_widths=(15, 25)),
+         "m4_erk5_4lvl": W.CFG3.scaled(512, 4096, m=4, levels=4, psi_widths=(15, 21, 29))}[label]
+    res, rep = _solve_parity(w)
+    assert res["converged"]
+
+
 def test_solve_cfg5_fullwidth_vcycle():
     """cfg5 at its full width nx = 16384 (the bench launch configurations: halo tiles for
     the fine sweep, tiled level sweeps and tiled coarsest solve), nt reduced to 1024."""
