@@ -157,6 +157,7 @@ def run_ours(args, w):
     torch.cuda.set_stream(stream)
     psi = problem.psi_inputs(w)
     s = problem.make_solver(w, psi, stream=stream)
+    s.set_cycle(args.cycle)
     guess = problem.device_guess(w)
     out = torch.empty_like(guess)
     s.set_guess(guess)
@@ -261,6 +262,7 @@ def run_ours(args, w):
         "config": {"workload": w.name, "nx": w.nx, "nt": w.nt, "scheme": f"{w.tableau}+U{w.order}",
                    "cfl": w.cfl, "m": w.m, "levels": w.levels, "relax": w.relax,
                    "psi_widths": list(w.psi_widths), "tol": w.tol, "iterations": K,
+                   "cycle": args.cycle,
                    "time_to_residual_ms": round(ms, 4),
                    "final_residual": res["history"][-1],
                    "parallelism": f"replicas{world}",
@@ -322,6 +324,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cycle", default="V", choices=["V", "F"],
+                    help="multilevel cycle (DESIGN.md R19); the bench line is the V-cycle")
     args = ap.parse_args()
     w = W.ALL[args.config]
     if args.impl == "reference":

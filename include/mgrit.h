@@ -58,6 +58,10 @@ typedef enum {
 
 typedef enum { MGRIT_RELAX_F = 0, MGRIT_RELAX_C = 1, MGRIT_RELAX_FCF = 2 } mgrit_relax_kind;
 
+/* Multilevel cycle of mgrit_solve: V-cycle (default) or F-cycle, in which
+ * each coarse problem is solved by one F-cycle followed by one V-cycle (R19). */
+typedef enum { MGRIT_CYCLE_V = 0, MGRIT_CYCLE_F = 1 } mgrit_cycle_kind;
+
 /* Coarse-grid time stepper Psi. */
 typedef enum {
   MGRIT_PSI_STENCIL = 0, /* sparse circulant, e.g. the LSQ fit of eq. (LSQ_1D_problem) */
@@ -159,6 +163,14 @@ int mgrit_coarse_solve(mgrit_ctx *ctx, int level, double *U_dev);
  */
 int mgrit_solve(mgrit_ctx *ctx, double tol, int max_iter, double *out_dev, int *iters,
                 double *hist_host, int *converged, double *crows_hist_dev);
+
+/*
+ * mgrit_set_cycle — cycle of mgrit_solve's coarse-grid correction for levels >= 3:
+ * MGRIT_CYCLE_V (default) or MGRIT_CYCLE_F (R19).
+ * Two-level solves are unaffected (the coarse solve is exact).  Host-only setter.
+ * Errors: EINVAL for another value or a null context.
+ */
+int mgrit_set_cycle(mgrit_ctx *ctx, int cycle);
 
 /* C-rows (nt/m+1) x nx of the current iterate after mgrit_solve. */
 int mgrit_get_crows(mgrit_ctx *ctx, double *out_dev);

@@ -109,6 +109,32 @@ def vcycle(level: int, U: np.ndarray, g: Optional[np.ndarray], phis: Sequence[Ca
     f_relax(U, phi, m, g)
 
 
+def fcycle(level: int, U: np.ndarray, g: Optional[np.ndarray], phis: Sequence[Callable],
+           m: int, relax: str) -> None:
+    """F(level, U, g): the multigrid F-cycle (P:622, P:843 name it without defining it;
+    DESIGN.md R19 reading): relaxation and residual injection as in V, but the coarse
+    error equation is solved approximately by one F-cycle followed by one V-cycle on the
+    coarse level, both from e = 0 / the F-cycle's result; then correction + F-relaxation.
+    On the coarsest level it is the sequential solve.  U is modified in place."""
+    phi = phis[level]
+    nt = U.shape[0] - 1
+    if level == len(phis) - 1:
+        U[:] = sequential_rhs(phi, g if g is not None else _fine_rhs(U))
+        return
+    f_relax(U, phi, m, g)
+    if relax == "FCF":
+        c_relax(U, phi, m, g)
+        f_relax(U, phi, m, g)
+    cpts = np.arange(m, nt + 1, m)
+    gc = np.zeros((nt // m + 1, U.shape[1]))
+    gc[1:] = residual_rows(U, phi, cpts, g)
+    E = np.zeros_like(gc)
+    fcycle(level + 1, E, gc, phis, m, relax)
+    vcycle(level + 1, E, gc, phis, m, relax)
+    U[cpts] = U[cpts] + E[1:]
+    f_relax(U, phi, m, g)
+
+
 def _fine_rhs(U):
     g = np.zeros_like(U)
     g[0] = U[0]
@@ -127,13 +153,13 @@ class SolveReport:
 
 def solve(U: np.ndarray, phis: Sequence[Callable], m: int, dx: float, dt: float,
           relax: str = "FCF", tol: float = 1e-10, max_iter: int = 64,
-          keep_states: bool = False) -> SolveReport:
+          keep_states: bool = False, cycle: str = "V") -> SolveReport:
     """MGRIT / Parareal iteration on the fine space-time iterate U (in place).
 
     U[0] holds u0 and is never modified.  The residual is
     measured on the iterate after k complete iterations; K = first k with
     ||r^(k)|| < tol (R2).  No early stop on growth (R15), except
-    for non-finite values."""
+    for non-finite values.  cycle: "V" or "F" (R19)."""
     phi = phis[0]
     hist = [residual_norm(U, phi, dx, dt)]
     states = []
@@ -141,7 +167,7 @@ def solve(U: np.ndarray, phis: Sequence[Callable], m: int, dx: float, dt: float,
     converged = hist[0] < tol
     nonfinite = False
     while not converged and k < max_iter:
-        vcycle(0, U, None, phis, m, relax)
+        (fcycle if cycle == "F" else vcycle)(0, U, None, phis, m, relax)
         k += 1
         r = residual_norm(U, phi, dx, dt)
         hist.append(r)

@@ -59,6 +59,7 @@ _SIGS = [
     ("mgrit_coarse_solve", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     ("mgrit_solve", C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.POINTER(C.c_int),
                               C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p]),
+    ("mgrit_set_cycle", C.c_int, [C.c_void_p, C.c_int]),
     ("mgrit_get_crows", C.c_int, [C.c_void_p, C.c_void_p]),
     ("mgrit_fill_guess", C.c_int, [C.c_void_p, C.c_longlong, C.c_longlong, C.c_int,
                                    C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
@@ -210,6 +211,10 @@ class MGRIT:
         assert tuple(guess.shape) == (self.nt + 1, self.nx)
         self.guess = guess
         self._check(lib().mgrit_set_guess(self.ctx, _dptr(guess)), "mgrit_set_guess")
+
+    def set_cycle(self, cycle: str):
+        """Multilevel cycle of `solve`: "V" (default) or "F" (R19)."""
+        self._check(lib().mgrit_set_cycle(self.ctx, {"V": 0, "F": 1}[cycle]), "mgrit_set_cycle")
 
     def solve(self, tol: float = 1e-10, max_iter: int = 64, out=None, keep_crows: bool = False):
         import torch

@@ -284,7 +284,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Layout of the workspace (doubles unless noted).
 struct Layout {
-  size_t u0, v0, g[MGRIT_MAX_LEVELS], vl[MGRIT_MAX_LEVELS], ul[MGRIT_MAX_LEVELS];
+  size_t u0, v0, g[MGRIT_MAX_LEVELS], u2[MGRIT_MAX_LEVELS], ul[MGRIT_MAX_LEVELS];
   size_t partials, scal, sa, sb, total;
   long long npart;
 };
@@ -307,10 +307,10 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
     ntl /= m;  // nt at level l
     L.g[l] = take((ntl + 1) * row);
     if (l < levels - 1) {
-      L.vl[l] = 0;
       L.ul[l] = take((ntl / m + 1) * row);
+      L.u2[l] = take((ntl / m + 1) * row);   // F-cycle: C-rows of the second (V) visit
     } else {
-      L.vl[l] = L.ul[l] = 0;
+      L.u2[l] = L.ul[l] = 0;
     }
   }
   // partials: largest sweep = all nt rows x up to 64 tiles
@@ -327,6 +327,7 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
 
 struct mgrit_ctx {
   int nx, nt, m, levels, order, tableau, relax, scheme;
+  int cycle = MGRIT_CYCLE_V;
   bool implicit;
   double alpha, cfl, dx, dt;
   cudaStream_t stream;
@@ -341,7 +342,7 @@ struct mgrit_ctx {
   Tab tab;
   Layout lay;
   char *ws;
-  double *u0b, *v0b, *g[MGRIT_MAX_LEVELS], *vl[MGRIT_MAX_LEVELS], *ul[MGRIT_MAX_LEVELS];
+  double *u0b, *v0b, *g[MGRIT_MAX_LEVELS], *u2[MGRIT_MAX_LEVELS], *ul[MGRIT_MAX_LEVELS];
   double *partials, *scal, *sa, *sb;
   double *ucur, *unext;   // fine C-rows: current iterate / next (FCF ping-pong of u0b, v0b)
   const double *guess;
@@ -681,7 +682,9 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
 
 // Level-l (1 <= l <= levels-2) FCF sweep with RHS g_l, zero initial guess:
 // v_l rows 1..nc, g_{l+1} rows 2..nc.
-int level_sweep(mgrit_ctx *c, int l) {
+// uin: C-rows of a nonzero level-l iterate (F-cycle's second visit), null: zero guess;
+// the FCF C-rows v go to vout rows 1..nc, r_{j+2} = Psi^m delta to g_{l+1} rows 2..nc.
+int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout) {
   const PsiOp &op = c->op[l];
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
@@ -696,10 +699,10 @@ int level_sweep(mgrit_ctx *c, int l) {
   a.ntiles = pc.ntiles;
   a.m = m;
   a.interp = 0;
-  a.u = kNone;
-  a.ucmp = kNone;
+  a.u = uin ? rm(uin, 0, 1) : kNone;
+  a.ucmp = uin ? rm(uin, 1, 1) : kNone;
   a.g = rm(c->g[l], 0, m);
-  a.v = rm(c->ul[l], 1, 1);   // v_{j+1} is the uncorrected C-row; the coarse levels add E
+  a.v = rm(vout, 1, 1);   // v_{j+1} is the uncorrected C-row; the coarse levels add E
   a.r2 = rm(c->g[l + 1], 2, 1);
   a.p2_items = (int)nc - 1;
   a.v2 = a.out2 = kNone;
@@ -711,7 +714,7 @@ int level_sweep(mgrit_ctx *c, int l) {
 // Level-l interpolation: from corrected C-rows u_l, F-relax with g_l and add the level-l
 // values to level l-1's C-rows in place: out_{l-1}[n] += U_l[n], n = 0..nt_l (out_{l-1}
 // holds v_{l-1} written by the level-(l-1) sweep; P:212 correction fused).
-int level_interp(mgrit_ctx *c, int l, RowMap out_prev) {
+int level_interp(mgrit_ctx *c, int l, const double *usrc_rows, RowMap out_prev) {
   const PsiOp &op = c->op[l];
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
@@ -727,7 +730,7 @@ int level_interp(mgrit_ctx *c, int l, RowMap out_prev) {
   a.m = m;
   a.interp = 1;
   a.accumulate = 1;
-  a.u = rm(c->ul[l], 0, 1);
+  a.u = rm(usrc_rows, 0, 1);
   a.ucmp = kNone;
   a.g = rm(c->g[l], 0, m);
   a.v = a.r2 = kNone;
@@ -741,30 +744,38 @@ int level_interp(mgrit_ctx *c, int l, RowMap out_prev) {
   const long long ntl = c->ntl[l];
   double *dst = const_cast<double *>(out_prev.base) +
                 (out_prev.off + ntl * out_prev.stride) * (long long)c->nx;
-  const double *usrc = c->ul[l] + nc * (long long)c->nx;
+  const double *usrc = usrc_rows + nc * (long long)c->nx;
   return run(c, 3, [&] { return mg_add_rows(dst, dst, usrc, c->nx, c->stream); });
 }
 
-// Coarse-grid correction below level 0 after the fine sweep (g_1 = r): the fine C-rows
-// `out0` hold v and receive += E (two-level: the sequential solve; V-cycle: level
-// sweeps down, the sequential coarsest solve, interpolations up).
-int coarse_correction(mgrit_ctx *c, RowMap out0) {
+// Level-l coarse cycle with zero initial guess and RHS g_l; the level-l result is ADDED to
+// dst (the C-rows of level l-1, which hold that level's uncorrected v).
+//   V: sweep(l); cycle_V(l+1) -> ul[l]; interp(l) -> dst
+//   F: sweep(l); cycle_F(l+1) -> ul[l]  [= MG_F(l, 0)];
+//      then one V-cycle on level l from that iterate: sweep(l, iterate ul[l]) -> u2[l];
+//      cycle_V(l+1) -> u2[l]; interp(l) from u2[l] -> dst               (R19)
+// The coarsest level is the sequential solve (its F- and V-visits coincide).
+int level_cycle(mgrit_ctx *c, int l, bool fcyc, RowMap dst) {
   const int L = c->levels;
-  if (L == 2) return coarse_solve_level(c, 1, out0, out0);
-  for (int l = 1; l <= L - 2; ++l) {
-    int st = level_sweep(c, l);
-    if (st) return st;
-  }
-  // coarsest: u_{L-2}[n] += x_n, n = 1..nt_{L-1}
-  {
-    int st = coarse_solve_level(c, L - 1, rm(c->ul[L - 2], 0, 1), rm(c->ul[L - 2], 0, 1));
-    if (st) return st;
-  }
-  for (int l = L - 2; l >= 1; --l) {
-    int st = level_interp(c, l, (l == 1) ? out0 : rm(c->ul[l - 1], 0, 1));
-    if (st) return st;
-  }
-  return MGRIT_OK;
+  if (l == L - 1) return coarse_solve_level(c, l, dst, dst);
+  int st = level_sweep(c, l, nullptr, c->ul[l]);
+  if (st) return st;
+  st = level_cycle(c, l + 1, fcyc, rm(c->ul[l], 0, 1));
+  if (st) return st;
+  if (!fcyc) return level_interp(c, l, c->ul[l], dst);
+  st = level_sweep(c, l, c->ul[l], c->u2[l]);
+  if (st) return st;
+  st = level_cycle(c, l + 1, false, rm(c->u2[l], 0, 1));
+  if (st) return st;
+  return level_interp(c, l, c->u2[l], dst);
+}
+
+// Coarse-grid correction below level 0 after the fine sweep (g_1 = r): the fine C-rows
+// `out0` hold v and receive += E (two-level: the sequential solve; multilevel: a V- or
+// F-cycle on level 1).
+int coarse_correction(mgrit_ctx *c, RowMap out0) {
+  if (c->levels == 2) return coarse_solve_level(c, 1, out0, out0);
+  return level_cycle(c, 1, c->cycle == MGRIT_CYCLE_F, out0);
 }
 
 }  // namespace
@@ -884,8 +895,8 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
   c->v0b = (double *)(c->ws + c->lay.v0);
   for (int l = 1; l < levels; ++l) {
     c->g[l] = (double *)(c->ws + c->lay.g[l]);
-    c->vl[l] = nullptr;
     c->ul[l] = (l < levels - 1) ? (double *)(c->ws + c->lay.ul[l]) : nullptr;
+    c->u2[l] = (l < levels - 1) ? (double *)(c->ws + c->lay.u2[l]) : nullptr;
   }
   c->ucur = c->u0b;
   c->unext = c->v0b;
@@ -901,6 +912,7 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
     cudaMemsetAsync(c->g[l], 0, 2 * row, c->stream);
     if (l < levels - 1) {
       cudaMemsetAsync(c->ul[l], 0, row, c->stream);
+      cudaMemsetAsync(c->u2[l], 0, row, c->stream);
     }
   }
   cudaError_t e = cudaGetLastError();
@@ -1036,6 +1048,13 @@ int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, 
   st = reduce_norm(c, partial_count(c, c->nt, 1), norm_host ? &n2 : nullptr);
   if (st) return st;
   if (norm_host) *norm_host = std::sqrt(c->dx * c->dt * n2);
+  return MGRIT_OK;
+}
+
+int mgrit_set_cycle(mgrit_ctx *c, int cycle) {
+  if (!c) return MGRIT_EINVAL;
+  if (cycle != MGRIT_CYCLE_V && cycle != MGRIT_CYCLE_F) return fail(c, MGRIT_EINVAL, "cycle must be V or F");
+  c->cycle = cycle;
   return MGRIT_OK;
 }
 

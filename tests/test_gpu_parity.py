@@ -238,7 +238,7 @@ def test_coarse_solve_deterministic(wname):
 
 
 # ------------------------------------------------------------------ full solves
-def _solve_parity(w, max_iter=None, check_states=True):
+def _solve_parity(w, max_iter=None, check_states=True, cycle="V"):
     B = _cuda()
     phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
     lib_psi, orc_psi = _oracle_psi(w, phi)
@@ -247,8 +247,9 @@ def _solve_parity(w, max_iter=None, check_states=True):
     umax = float(np.max(np.abs(U)))
     Uo = U.copy()
     rep = M.solve(Uo, [phi] + orc_psi, w.m, w.dx, w.dt, w.relax, w.tol, max_iter,
-                  keep_states=check_states)
+                  keep_states=check_states, cycle=cycle)
     s = B.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels, lib_psi, w.relax)
+    s.set_cycle(cycle)
     g = torch.from_numpy(U).cuda()
     s.set_guess(g)
     out = torch.empty_like(g)
@@ -324,6 +325,17 @@ def test_solve_other_hierarchies(label):
          "m8_erk5": W.CFG3.scaled(512, 4096, levels=3, psi_widths=(15, 25)),
          "m4_erk5_4lvl": W.CFG3.scaled(512, 4096, m=4, levels=4, psi_widths=(15, 21, 29))}[label]
     res, rep = _solve_parity(w)
+    assert res["converged"]
+
+
+@pytest.mark.parametrize("nx,nt,levels,m", [(256, 1024, 3, 4), (256, 4096, 5, 4),
+                                             (1024, 4096, 4, 4), (256, 1024, 4, 2)])
+def test_solve_fcycle(nx, nt, levels, m):
+    """F-cycles (R19) on the cfg5 recipe: iterates, history and K
+    vs the oracle's F-cycle (second, nonzero-iterate level sweeps included)."""
+    w = W.CFG5.scaled(nx, nt, levels=levels, m=m,
+                      **({"psi_widths": (7, 9, 11)} if m == 2 else {}))
+    res, rep = _solve_parity(w, cycle="F")
     assert res["converged"]
 
 

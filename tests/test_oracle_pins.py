@@ -260,6 +260,57 @@ def test_multilevel_ideal_hierarchy_one_iteration():
     assert rep.iterations == 1
 
 
+# ---------------------------------------------------------------- F-cycles (R19)
+def test_fcycle_two_level_equals_vcycle():
+    """With two levels the coarse problem is solved exactly, so an F-cycle (exact solve,
+    then a V-cycle = the same exact solve) is the two-level iteration, bitwise."""
+    nx, nt, m = 32, 128, 4
+    phi, U, dx, dt = _setup(3, "erk3_ssp", 0.85, nx, nt)
+    psi = D.StencilPhi({-4: 0.2, -3: 0.5, -2: 0.3}, nx)
+    Uv, Uf = U.copy(), U.copy()
+    for _ in range(3):
+        M.vcycle(0, Uv, None, [phi, psi], m, "FCF")
+        M.fcycle(0, Uf, None, [phi, psi], m, "FCF")
+    assert np.array_equal(Uv, Uf)
+
+
+def test_fcycle_ideal_hierarchy_one_iteration():
+    """Ideal operators on every level: the F-cycle is exact after one iteration."""
+    nx, nt, m = 16, 256, 4
+    phi, U, dx, dt = _setup(3, "erk3_ssp", 0.85, nx, nt)
+    phis = [phi, D.PowerPhi(phi, m), D.PowerPhi(phi, m * m), D.PowerPhi(phi, m ** 3)]
+    rep = M.solve(U, phis, m, dx, dt, "FCF", 1e-10, 4, cycle="F")
+    assert rep.iterations == 1
+
+
+@pytest.mark.parametrize("relax", ["FCF", "F"])
+def test_fcycle_finite_termination(relax):
+    """Finite termination holds for F-cycles too (the fine relaxation makes 2m (m) more
+    steps exact per iteration and the coarse corrections vanish there)."""
+    nx, nt, m = 16, 64, 2
+    phi, U, dx, dt = _setup(3, "erk3_ssp", 0.85, nx, nt)
+    psis = [D.StencilPhi({0: 0.5}, nx), D.StencilPhi({-1: 0.25, 0: 0.25}, nx)]
+    kmax = nt // (2 * m) if relax == "FCF" else nt // m
+    for _ in range(kmax - 1):
+        M.fcycle(0, U, None, [phi] + psis, m, relax)
+    S = D.sequential(phi, U[0], nt)
+    assert np.max(np.abs(U - S)) > 1e-6
+    M.fcycle(0, U, None, [phi] + psis, m, relax)
+    assert np.max(np.abs(U - S)) < 1e-13 * np.max(np.abs(S))
+
+
+def test_fcycle_needs_no_more_iterations_than_vcycle():
+    """"F-cycles require fewer iterations to converge than V-cycles" — on the cfg5
+    recipe at 256 x 4096 with 5 levels: F 6, V 7 iterations."""
+    w = W.CFG5.scaled(256, 4096, levels=5)
+    phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
+    fits = P.fit_hierarchy(phi, w.nx, w.m, w.cfl, w.psi_widths[: w.levels - 1], w.psi_eta)
+    ops = [phi] + [D.StencilPhi(f.stencil, w.nx) for f in fits]
+    kv = M.solve(w.guess(), ops, w.m, w.dx, w.dt, w.relax, w.tol, w.max_iter).iterations
+    kf = M.solve(w.guess(), ops, w.m, w.dx, w.dt, w.relax, w.tol, w.max_iter, cycle="F").iterations
+    assert kf < kv, (kf, kv)
+
+
 # ---------------------------------------------------------------- paper tables
 def _golden_iters():
     rows = []
