@@ -143,6 +143,29 @@ def oracle_sample(w, budget_s: float = 12.0):
                       f"{dt:.1f} s"}
 
 
+def sequential_sample(w, budget_s: float = 6.0):
+    """Plain sequential time-stepping with the oracle's Phi on the host: the
+    other CPU baseline north_star names.  Bounded sample of the workload's steps; the
+    full-length time is extrapolated (nt steps)."""
+    from oracle import discretization as D
+    phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
+    u = w.u0()
+    t0 = time.perf_counter()
+    steps = 0
+    while steps < w.nt:
+        for _ in range(16):
+            u = phi(u)
+        steps += 16
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    rate = steps * w.nx / dt
+    return {"value": rate, "unit": UNIT, "cores": 1, "kind": "sequential time-stepping",
+            "sample": f"{steps} of {w.nt} steps of {w.tableau}+U{w.order} at nx={w.nx} "
+                      f"(oracle Phi, numpy fp64), {dt:.1f} s",
+            "full_run_s_extrapolated": round(w.nt * w.nx / rate, 1)}
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, w):
     import torch
@@ -285,6 +308,7 @@ def run_ours(args, w):
         line["clocks"] = _clock_summary(clk_path, local)
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = oracle_sample(w, args.cpu_budget)
+            line["cpu_sequential"] = sequential_sample(w, args.cpu_budget / 2)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
