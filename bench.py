@@ -181,6 +181,7 @@ def run_ours(args, w):
     psi = problem.psi_inputs(w)
     s = problem.make_solver(w, psi, stream=stream)
     s.set_cycle(args.cycle)
+    s.set_final_sweep(args.final_sweep)
     guess = problem.device_guess(w)
     out = torch.empty_like(guess)
     s.set_guess(guess)
@@ -288,6 +289,8 @@ def run_ours(args, w):
                    "cycle": args.cycle,
                    "time_to_residual_ms": round(ms, 4),
                    "final_residual": res["history"][-1],
+                   "history": [float(f"{h:.4e}") for h in res["history"]],
+                   "final_sweep": args.final_sweep,
                    "parallelism": f"replicas{world}",
                    "l2": "inputs larger than L2 (8 GiB state vs 126 MB L2)"},
         "roofline": {"bound": "alu", "kernel": s.describe() + " (fine FCF sweep)",
@@ -348,6 +351,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--final-sweep", default="predict", choices=["off", "predict", "always"],
+                    help="mgrit_set_final_sweep mode (include/mgrit.h)")
     ap.add_argument("--cycle", default="V", choices=["V", "F"],
                     help="multilevel cycle (DESIGN.md R19); the bench line is the V-cycle")
     args = ap.parse_args()

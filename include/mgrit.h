@@ -172,6 +172,24 @@ int mgrit_solve(mgrit_ctx *ctx, double tol, int max_iter, double *out_dev, int *
  */
 int mgrit_set_cycle(mgrit_ctx *ctx, int cycle);
 
+/*
+ * mgrit_set_final_sweep — how mgrit_solve (with out_dev non-NULL) measures the residual
+ * of the iterate it returns.  The sweep that measures ||r^(k)|| normally also computes
+ * the next coarse right-hand side r = Phi^m delta; if iteration k is the last, that work
+ * is unused and the FULL solution needs a separate F-relaxation pass.  A check sweep
+ * instead writes the F-relaxed iterate (all rows) into out_dev while measuring the norm
+ * (identical partial sums, so identical history and K).  Modes:
+ *   MGRIT_FINAL_OFF      never (always the fused sweep, then a materialisation pass);
+ *   MGRIT_FINAL_PREDICT  (default) when k == max_iter, or when the geometric
+ *                        extrapolation ||r^(k-1)||^2/||r^(k-2)|| of a decreasing history
+ *                        is below tol; if the check does not converge, the fused sweep
+ *                        is run after it (results unchanged, one extra phase-1 pass);
+ *   MGRIT_FINAL_ALWAYS   every iteration (tests the misprediction path).
+ * Host-only setter.  Errors: EINVAL for another value or a null context.
+ */
+enum { MGRIT_FINAL_OFF = 0, MGRIT_FINAL_PREDICT = 1, MGRIT_FINAL_ALWAYS = 2 };
+int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
+
 /* C-rows (nt/m+1) x nx of the current iterate after mgrit_solve. */
 int mgrit_get_crows(mgrit_ctx *ctx, double *out_dev);
 

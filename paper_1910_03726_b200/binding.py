@@ -60,6 +60,7 @@ _SIGS = [
     ("mgrit_solve", C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.POINTER(C.c_int),
                               C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p]),
     ("mgrit_set_cycle", C.c_int, [C.c_void_p, C.c_int]),
+    ("mgrit_set_final_sweep", C.c_int, [C.c_void_p, C.c_int]),
     ("mgrit_get_crows", C.c_int, [C.c_void_p, C.c_void_p]),
     ("mgrit_fill_guess", C.c_int, [C.c_void_p, C.c_longlong, C.c_longlong, C.c_int,
                                    C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
@@ -215,6 +216,11 @@ class MGRIT:
     def set_cycle(self, cycle: str):
         """Multilevel cycle of `solve`: "V" (default) or "F" (R19)."""
         self._check(lib().mgrit_set_cycle(self.ctx, {"V": 0, "F": 1}[cycle]), "mgrit_set_cycle")
+
+    def set_final_sweep(self, mode: str):
+        """mgrit_set_final_sweep: "off", "predict" (default) or "always" (include/mgrit.h)."""
+        self._check(lib().mgrit_set_final_sweep(self.ctx, {"off": 0, "predict": 1, "always": 2}[mode]),
+                    "mgrit_set_final_sweep")
 
     def solve(self, tol: float = 1e-10, max_iter: int = 64, out=None, keep_crows: bool = False):
         import torch

@@ -328,6 +328,7 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
 struct mgrit_ctx {
   int nx, nt, m, levels, order, tableau, relax, scheme;
   int cycle = MGRIT_CYCLE_V;
+  int final_sweep = MGRIT_FINAL_PREDICT;  // mgrit_set_final_sweep
   bool implicit;
   double alpha, cfl, dx, dt;
   cudaStream_t stream;
@@ -538,8 +539,7 @@ int sweep(mgrit_ctx *c, int cls, SweepArgs a, int total_steps) {
   if (a.partials && (long long)a.nitems * a.ntiles > c->lay.npart)
     return fail(c, MGRIT_ENOMEM, "partials buffer too small");
   // halo tiles, even nx, no per-step writes: persistent TMA-pipelined kernel
-  const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1) && a.in.base &&
-                   (a.each_last < a.each_first || !a.cmp.base);
+  const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1) && a.in.base;
   if (a.partials && tma && (long long)a.nitems * a.ntiles * (f.cfg.nt_threads / 32) > c->lay.npart)
     return fail(c, MGRIT_ENOMEM, "partials buffer too small");
   if (tma) return run(c, cls, [&] { return launch_rk_sweep_tma(c->scheme, f.cfg, a, c->stream); });
@@ -1051,6 +1051,14 @@ int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, 
   return MGRIT_OK;
 }
 
+int mgrit_set_final_sweep(mgrit_ctx *c, int mode) {
+  if (!c) return MGRIT_EINVAL;
+  if (mode != MGRIT_FINAL_OFF && mode != MGRIT_FINAL_PREDICT && mode != MGRIT_FINAL_ALWAYS)
+    return fail(c, MGRIT_EINVAL, "final-sweep mode must be OFF, PREDICT or ALWAYS");
+  c->final_sweep = mode;
+  return MGRIT_OK;
+}
+
 int mgrit_set_cycle(mgrit_ctx *c, int cycle) {
   if (!c) return MGRIT_EINVAL;
   if (cycle != MGRIT_CYCLE_V && cycle != MGRIT_CYCLE_F) return fail(c, MGRIT_EINVAL, "cycle must be V or F");
@@ -1135,6 +1143,26 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     }
     return sweep(c, 0, a, fcf ? 2 * m : m);
   };
+  // Check+materialise sweep: phase 1 of the fused sweep (same tiles, so the same norm
+  // partials, bit for bit) with per-step writes of the FULL iterate into out_dev and no
+  // coarse RHS.  Used for the sweep that measures ||r^(k)|| when iteration k is known
+  // (k == max_iter) or predicted to be the last, so a converged solve needs neither the
+  // unused r = Phi^m delta nor a separate materialisation pass.
+  auto check_sweep = [&]() -> int {
+    SweepArgs a = base_sweep(c);
+    a.nitems = (int)nc;
+    a.nsteps1 = m;
+    a.in = rm(c->ucur, 0, 1);
+    a.cmp = rm(c->ucur, 1, 1);
+    a.partials = c->partials;
+    a.each = rm(out_dev, 0, m);
+    a.each_step = 1;
+    a.each_first = 0;
+    a.each_last = m - 1;
+    return sweep(c, 3, a, fcf ? 2 * m : m);
+  };
+  bool materialised = false;
+  std::vector<double> h(1, r0);
   if (!conv && !nonfinite && max_iter > 0) {
     st = do_sweep(true, false);
     if (st) return st;
@@ -1149,17 +1177,30 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       if (crows_hist)
         cudaMemcpyAsync(crows_hist + (size_t)(k - 1) * (nc + 1) * nx, c->ucur, (nc + 1) * row,
                         cudaMemcpyDeviceToDevice, c->stream);
-      // residual of iterate k (computed by the next sweep)
-      st = do_sweep(false, true);
+      // residual of iterate k (computed by the next sweep).  Predicted last: the
+      // previous two residuals extrapolated geometrically fall below tol.
+      bool last = false;
+      if (out_dev && c->final_sweep != MGRIT_FINAL_OFF) {
+        if (k >= max_iter || c->final_sweep == MGRIT_FINAL_ALWAYS) last = true;
+        else if (k >= 2 && h[k - 1] < h[k - 2]) last = h[k - 1] * (h[k - 1] / h[k - 2]) < tol;
+      }
+      st = last ? check_sweep() : do_sweep(false, true);
       if (st) return st;
       double n2;
       st = reduce_norm(c, partial_count(c, nc, fcf ? 2 * m : m), &n2);
       if (st) return st;
       const double rk = std::sqrt(c->dx * c->dt * n2);
       if (hist) hist[k] = rk;
+      h.push_back(rk);
+      const bool stop = !std::isfinite(rk) || rk < tol || k >= max_iter;
+      if (last && stop) materialised = true;
       if (!std::isfinite(rk)) { nonfinite = true; break; }
       if (rk < tol) { conv = true; break; }
       if (k >= max_iter) break;
+      if (last) {  // mispredicted: the fused sweep for the next coarse correction
+        st = do_sweep(false, false);
+        if (st) return st;
+      }
     }
   }
   if (iters) *iters = k;
@@ -1167,6 +1208,9 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   if (out_dev) {
     if (!c->have_iterate) {
       cudaMemcpyAsync(out_dev, c->guess, (size_t)(c->nt + 1) * row, cudaMemcpyDeviceToDevice, c->stream);
+    } else if (materialised) {
+      cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->ucur + (size_t)nc * nx, row,
+                      cudaMemcpyDeviceToDevice, c->stream);
     } else {
       SweepArgs a = base_sweep(c);
       a.nitems = (int)nc;

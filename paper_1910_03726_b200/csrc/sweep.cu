@@ -232,14 +232,18 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
     double x[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = IN(b)[tid * P + p];
-    // per-step writes (F-relaxation / materialisation): alternate the two CM buffers
-    // as staging (no comparison rows in this mode)
+    // per-step writes (F-relaxation / materialisation): alternate IN(b) and CM as staging.
+    // With comparison rows (the final check+materialise sweep) CM is taken, so every store
+    // stages in IN(b) after the previous one has finished reading it.
     auto each_store = [&](int i) {
-      if (tid == 0 && nstage >= 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if (tid == 0 && nstage >= 1) {
+        if (a.cmp.base) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      }
       double *row = const_cast<double *>(a.each.base) +
                     (a.each.off + (long long)item * a.each.stride + (long long)i * a.each_step) *
                         (long long)nx;
-      store(row, (nstage & 1) ? CM : IN(b), x, abeg, T, true);
+      store(row, (!a.cmp.base && (nstage & 1)) ? CM : IN(b), x, abeg, T, true);
       ++nstage;
     };
     // Step 1 is peeled so the thread-0 prefetch does not sit inside the step loop (a

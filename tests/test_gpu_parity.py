@@ -437,3 +437,34 @@ def test_fullsize_solve_properties(wname):
             assert math.sqrt(dxdt * np.sum(r * r)) <= res["history"][-1] * (1 + 1e-9) + 1e-16
     again = s.residual_full(out)
     assert abs(again - res["history"][-1]) <= 1e-6 * res["history"][-1] + 1e-15
+
+
+# ------------------------------------------------------------------ final check sweep
+@pytest.mark.parametrize("label", ["tiles_vcycle", "whole_rows", "parareal", "cap"])
+def test_final_sweep_modes_identical(label):
+    """mgrit_set_final_sweep: the check+materialise sweep (predicted, forced every
+    iteration = the misprediction path, or off) yields the same history, K and FULL
+    solution bit for bit (it is phase 1 of the fused sweep on the same tiles)."""
+    from paper_1910_03726_b200 import problem
+    B = _cuda()
+    w = {"tiles_vcycle": W.CFG5.scaled(4096, 1024, levels=4),
+         "whole_rows": W.CFG2.scaled(1024, 1024),
+         "parareal": W.CFG2.scaled(256, 1024, relax="F", max_iter=40),
+         "cap": W.CFG4_LITERAL.scaled(256, 1024, max_iter=6)}[label]
+    g = torch.from_numpy(w.guess()).cuda()
+    runs = {}
+    for mode in ("off", "predict", "always"):
+        s = problem.make_solver(w)
+        s.set_final_sweep(mode)
+        s.set_guess(g)
+        out = torch.full_like(g, float("nan"))
+        res = s.solve(w.tol, w.max_iter, out=out)
+        runs[mode] = (res, out)
+    r0, o0 = runs["off"]
+    for mode in ("predict", "always"):
+        r, o = runs[mode]
+        assert r["iterations"] == r0["iterations"] and r["converged"] == r0["converged"]
+        assert r["history"] == r0["history"], mode
+        assert torch.equal(o, o0), (mode, (o - o0).abs().max().item())
+    if label == "cap":
+        assert r0["iterations"] == w.max_iter and not r0["converged"]
