@@ -186,8 +186,115 @@ std::vector<std::complex<long double>> poly_roots(const std::vector<long double>
 // Factor M = I - a Z (periodic, stencil z_d at d = zlo..zlo+zn-1) into first-order periodic
 // recurrences for the device stage solve (sdirk.cuh).  Returns false if the factorisation is
 // not supported (complex roots, or winding number != 0).
+// Partial-fraction (fused) form of the stage-matrix inverse (sdirk.cuh,
+// fused_stage_solve).  With inside roots a_k (forward factors 1/(1 - a_k z^-1)) and
+// b_l = 1/r_l for the outside roots r_l (backward factors 1/(1 - b_l z)):
+//   A_k = prod_{j!=k} 1/(1 - a_j/a_k) prod_l 1/(1 - b_l a_k)   (residue at z = a_k)
+//   B_l = prod_{j!=l} 1/(1 - b_j/b_l) prod_k 1/(1 - a_k b_l)   (residue at z = 1/b_l)
+//   const = F(inf) - sum_k A_k,  F(inf) = 1 if there is no outside root, else 0.
+// Used only when the weights are well conditioned (sum of |weights| <= 64), so the
+// rounding of the sum stays within a few ulps of the product form's.
+void make_sdirk_fused(const std::vector<std::complex<long double>> &roots, long double gamma,
+                      int NL, int P, int nx, SdirkCoef &sd) {
+  typedef std::complex<long double> C;
+  const C one(1.0L, 0.0L);
+  std::vector<C> a, b;
+  for (auto &r : roots) {
+    if (std::abs(r) < 1.0L) a.push_back(r);
+    else b.push_back(one / r);
+  }
+  const int NR = (int)b.size();
+  std::vector<C> A(a.size()), B(b.size());
+  long double cond = 0.0L;
+  C cst = (NR == 0) ? one : C(0.0L, 0.0L);
+  for (size_t k = 0; k < a.size(); ++k) {
+    C w = one;
+    for (size_t j = 0; j < a.size(); ++j)
+      if (j != k) w /= (one - a[j] / a[k]);
+    for (auto &bl : b) w /= (one - bl * a[k]);
+    A[k] = w;
+    cst -= w;
+    cond += std::abs(w);
+  }
+  for (size_t l = 0; l < b.size(); ++l) {
+    C w = one;
+    for (size_t j = 0; j < b.size(); ++j)
+      if (j != l) w /= (one - b[j] / b[l]);
+    for (auto &ak : a) w /= (one - ak * b[l]);
+    B[l] = w;
+    cond += std::abs(w);
+  }
+  cond += std::abs(cst);
+  sd.fused = 0;
+  if (!(cond <= 64.0L) || NR > 1 || (int)a.size() != NL || NL + NR > MAXREC) return;
+  // slots: rec[0..NL) forward real (then zero dummies), rec[NL..NL+NR) backward real,
+  // crec[0] the complex pair (member with Im > 0)
+  SdirkCoef f = sd;
+  for (int k = 0; k < MAXREC; ++k) std::memset(&f.rec[k], 0, sizeof(RecCoef));
+  for (int k = 0; k < MAXCREC; ++k) std::memset(&f.crec[k], 0, sizeof(CRecCoef));
+  auto fill_real = [&](RecCoef &rc, long double rho, long double alpha, bool bwd) {
+    long double pk = 1.0L;
+    for (int i = 0; i <= MAXP; ++i) {
+      rc.rpow[i] = (i <= P) ? (double)pk : 0.0;
+      pk *= rho;
+    }
+    const long double rP = powl(rho, (long double)P);
+    long double pj = 1.0L;
+    for (int j = 0; j <= 32; ++j) { rc.rchunk[j] = (double)pj; pj *= rP; }
+    const long double mu = powl(rho, (long double)(32 * P));
+    long double pw = 1.0L;
+    for (int w = 0; w <= 16; ++w) { rc.rwarp[w] = (double)pw; pw *= mu; }
+    rc.closure = (double)(1.0L / (1.0L - powl(rho, (long double)nx)));
+    rc.alpha = (double)alpha;
+    rc.backward = bwd ? 1 : 0;
+  };
+  int nrf = 0, npair = 0;
+  std::vector<std::pair<long double, long double>> fr;  // (rho, alpha) forward real
+  for (size_t k = 0; k < a.size(); ++k) {
+    const long double im = a[k].imag();
+    if (std::fabs((double)im) <= 1e-12 * std::max(1.0, (double)std::abs(a[k]))) {
+      fr.push_back({a[k].real(), (gamma * A[k]).real()});
+    } else if (im > 0) {
+      if (npair >= 1) return;
+      CRecCoef &rc = f.crec[npair++];
+      const C rho = a[k];
+      C pk = one;
+      for (int i = 0; i <= MAXP; ++i) {
+        rc.rpr[i] = (i <= P) ? (double)pk.real() : 0.0;
+        rc.rpi[i] = (i <= P) ? (double)pk.imag() : 0.0;
+        pk *= rho;
+      }
+      const C rP = std::pow(rho, (long double)P);
+      C pj = one;
+      for (int j = 0; j <= 32; ++j) { rc.rcr[j] = (double)pj.real(); rc.rci[j] = (double)pj.imag(); pj *= rP; }
+      const C mu = std::pow(rho, (long double)(32 * P));
+      C pw = one;
+      for (int w = 0; w <= 16; ++w) { rc.rwr[w] = (double)pw.real(); rc.rwi[w] = (double)pw.imag(); pw *= mu; }
+      const C cl = one / (one - std::pow(rho, (long double)nx));
+      rc.clr = (double)cl.real();
+      rc.cli = (double)cl.imag();
+      const C w2 = 2.0L * gamma * A[k];
+      rc.ar = (double)w2.real();
+      rc.ai = (double)w2.imag();
+    }
+  }
+  std::sort(fr.begin(), fr.end(), [](const std::pair<long double, long double> &x,
+                                     const std::pair<long double, long double> &y) {
+    return std::fabs(x.first) < std::fabs(y.first);
+  });
+  for (auto &pr : fr) fill_real(f.rec[nrf++], pr.first, pr.second, false);
+  for (int k = nrf; k < NL; ++k) fill_real(f.rec[k], 0.0L, 0.0L, false);  // dummies
+  for (int l = 0; l < NR; ++l) fill_real(f.rec[NL + l], b[l].real(), (gamma * B[l]).real(), true);
+  f.nrf = nrf;
+  f.ncrec = npair;
+  f.nrec = NL + NR;
+  f.beta = (double)(gamma * cst).real();
+  f.fused = 1;
+  sd = f;
+}
+
 bool make_sdirk(const double *z, int zlo, int zn, double a, int P, int nx, SdirkCoef &sd,
-                std::string &why) {
+                std::string &why, bool allow_fused) {
   std::memset(&sd, 0, sizeof(sd));
   // m_d = delta_d0 - a z_d; polynomial q(x) = sum_d m_d x^(d - zlo)
   std::vector<long double> q(zn);
@@ -277,6 +384,7 @@ bool make_sdirk(const double *z, int zlo, int zn, double a, int P, int nx, Sdirk
     rc.cli = (double)cl.imag();
     rc.ratio = (double)(rho.real() / rho.imag());
   }
+  if (allow_fused) make_sdirk_fused(roots, 1.0L / gamma_inv.real(), NL, P, nx, sd);
   return true;
 }
 
@@ -524,6 +632,8 @@ SweepArgs base_sweep(const mgrit_ctx *c) {
   a.each_first = 1;
   a.each_last = 0;  // none
   a.d_every = 1;
+  a.load_after = 1;
+  if (const char *e = getenv("MGRIT_LOAD_AFTER")) a.load_after = atoi(e);  // experiments
   a.co = c->fine;
   a.sd = c->sd;
   a.in = a.cmp = a.endw = a.each = a.dstore = a.r2 = kNone;
@@ -850,8 +960,11 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
     FineCfg f;
     if (!choose_fine(c, 1, f)) return bad(MGRIT_EUNSUPPORTED, "SDIRK needs nx in {64,128,256,...,4096} (whole-row CTAs)");
     std::string why;
-    if (!make_sdirk(c->fine.z, c->zlo, c->zn, c->tab.A[0][0], f.cfg.p, nx, c->sd, why))
+    const char *prod = getenv("MGRIT_SDIRK_PRODUCT");  // experiments/tests: product form only
+    if (!make_sdirk(c->fine.z, c->zlo, c->zn, c->tab.A[0][0], f.cfg.p, nx, c->sd, why,
+                    !(prod && atoi(prod))))
       return bad(MGRIT_EUNSUPPORTED, why.c_str());
+
   }
   // coarse operators
   c->psi_kind = psi[0].kind;

@@ -26,7 +26,9 @@ constexpr int MAXREC = 4;
 struct RecCoef {
   double rpow[MAXP + 1];   // rho^k, k = 0..P
   double rchunk[33];       // (rho^P)^j, j = 0..32
+  double rwarp[17];        // (rho^(32P))^w, w = 0..16 (fused form: cross-warp scan)
   double closure;          // 1 / (1 - rho^N), N = nx
+  double alpha;            // fused form: gamma * partial-fraction weight of this factor
   int backward;            // 0: x_i = rho x_{i-1} + f_i ; 1: x_i = rho x_{i+1} + f_i
   int pad;
 };
@@ -36,8 +38,10 @@ constexpr int MAXCREC = 2;
 struct CRecCoef {            // complex rho = (re, im), |rho| < 1
   double rpr[MAXP + 1], rpi[MAXP + 1];   // rho^k
   double rcr[33], rci[33];               // (rho^P)^j
+  double rwr[17], rwi[17];               // (rho^(32P))^w (fused form)
   double clr, cli;                       // 1 / (1 - rho^N)
   double ratio;                          // Re(rho) / Im(rho)
+  double ar, ai;                         // fused form: 2 * gamma * weight (complex)
   int backward;
   int pad;
 };
@@ -45,7 +49,10 @@ struct CRecCoef {            // complex rho = (re, im), |rho| < 1
 struct SdirkCoef {
   int nrec;
   int ncrec;
+  int fused;               // 1: partial-fraction form (fused_stage_solve), 0: product form
+  int nrf;                 // fused form: forward real factors in rec[0..nrf), backward after
   double gamma;            // M^-1 = gamma * prod (bidiagonal inverses)
+  double beta;             // fused form: gamma * constant term of the partial fractions
   RecCoef rec[MAXREC];
   CRecCoef crec[MAXCREC];  // one per complex-conjugate root pair
 };
@@ -213,6 +220,200 @@ __device__ __forceinline__ void periodic_recurrence_cplx(double (&f)[P], const C
   wphase ^= 1;
 }
 
+// ---------------------------------------------------------------------------
+// Fused (partial-fraction) stage solve.  The inverse symbol of the stage matrix,
+//   1/m(z) = gamma prod_k 1/(1 - a_k z^-1) prod_l 1/(1 - b_l z)     (|a_k|, |b_l| < 1),
+// is, for distinct roots, beta + sum_k A_k/(1 - a_k z^-1) + sum_l B_l/(1 - b_l z), so
+// M^-1 f = beta f + sum of INDEPENDENT first-order periodic recurrences on the same f
+// (weights computed on the host, mgrit_api.cu make_sdirk; used only when they are well
+// conditioned).  All recurrences run in one pass: interleaved local chains, interleaved
+// warp scans, ONE barrier, a shuffle scan of the warp carries (log2 NW steps instead of
+// a serial loop), and the carry fix-up accumulates straight into y.
+// Slots in wbuf (per phase): NL forward real (absent ones have rho = alpha = 0), then
+// 2 per complex pair, then NR backward real.
+// ---------------------------------------------------------------------------
+template <int NW>
+__device__ __forceinline__ double warp_carry_fwd(double t, const double *mu, double closure,
+                                                 int warp, int lane) {
+  // t = this lane's warp total (lane v < NW holds warp v's); returns the carry entering
+  // `warp`: mu^warp * tot * closure + sum_{v<warp} mu^(warp-1-v) t_v
+  double S = (lane < NW) ? t : 0.0;
+#pragma unroll
+  for (int d = 1; d < NW; d <<= 1) {
+    const double v = __shfl_up_sync(FULL, S, d);
+    if (lane >= d) S = fma(mu[d], v, S);
+  }
+  const double tot = __shfl_sync(FULL, S, NW - 1);
+  const double prev = __shfl_sync(FULL, S, (warp + 31) & 31);
+  return fma(mu[warp], tot * closure, warp ? prev : 0.0);
+}
+
+template <int NW>
+__device__ __forceinline__ double warp_carry_bwd(double t, const double *mu, double closure,
+                                                 int warp, int lane) {
+  // carry entering `warp` from the right: mu^(NW-1-warp) * tot * closure
+  //   + sum_{v>warp} mu^(v-warp-1) t_v,   tot = sum_v mu^v t_v
+  double S = (lane < NW) ? t : 0.0;
+#pragma unroll
+  for (int d = 1; d < NW; d <<= 1) {
+    const double v = __shfl_down_sync(FULL, S, d);
+    if (lane + d < NW) S = fma(mu[d], v, S);
+  }
+  const double tot = __shfl_sync(FULL, S, 0);
+  const double next = __shfl_sync(FULL, S, (warp + 1) & 31);
+  return fma(mu[NW - 1 - warp], tot * closure, warp < NW - 1 ? next : 0.0);
+}
+
+template <int NW>
+__device__ __forceinline__ void warp_carry_cplx(double tr, double ti, const CRecCoef &rc,
+                                                int warp, int lane, double &cr, double &ci) {
+  double Sr = (lane < NW) ? tr : 0.0, Si = (lane < NW) ? ti : 0.0;
+#pragma unroll
+  for (int d = 1; d < NW; d <<= 1) {
+    const double vr = __shfl_up_sync(FULL, Sr, d);
+    const double vi = __shfl_up_sync(FULL, Si, d);
+    if (lane >= d) cfma(rc.rwr[d], rc.rwi[d], vr, vi, Sr, Si);
+  }
+  const double totr = __shfl_sync(FULL, Sr, NW - 1), toti = __shfl_sync(FULL, Si, NW - 1);
+  const double pr = __shfl_sync(FULL, Sr, (warp + 31) & 31);
+  const double pi = __shfl_sync(FULL, Si, (warp + 31) & 31);
+  double c0r = 0.0, c0i = 0.0;
+  cfma(totr, toti, rc.clr, rc.cli, c0r, c0i);
+  cr = warp ? pr : 0.0;
+  ci = warp ? pi : 0.0;
+  cfma(rc.rwr[warp], rc.rwi[warp], c0r, c0i, cr, ci);
+}
+
+template <int NL, int NR, int P, int NT>
+__device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoef &sd,
+                                                  double *wbuf, int &wphase) {
+  constexpr int NW = NT / 32;
+  constexpr int NSLOT = NL + 2 * (NL / 2) + NR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool pair = (NL >= 2) && sd.ncrec > 0;   // warp-uniform
+  double *wb = wbuf + wphase * NSLOT * NW;
+  double y[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) y[p] = sd.beta * f[p];
+  // ---- local chains (interleaved) -------------------------------------------------
+  double A[NL], Br[NR > 0 ? NR : 1];
+  double Cr = 0.0, Ci = 0.0;
+#pragma unroll
+  for (int k = 0; k < NL; ++k) A[k] = f[0];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      if (p > 0) A[k] = fma(sd.rec[k].rpow[1], A[k], f[p]);
+      y[p] = fma(sd.rec[k].alpha, A[k], y[p]);
+    }
+  }
+  if constexpr (NL >= 2) {
+    if (pair) {
+      const CRecCoef &rc = sd.crec[0];
+      Cr = f[0];
+      Ci = 0.0;
+      y[0] = fma(rc.ar, Cr, y[0]);
+#pragma unroll
+      for (int p = 1; p < P; ++p) {
+        double nr = f[p], ni = 0.0;
+        cfma(rc.rpr[1], rc.rpi[1], Cr, Ci, nr, ni);
+        Cr = nr;
+        Ci = ni;
+        y[p] = fma(rc.ar, Cr, fma(-rc.ai, Ci, y[p]));
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const RecCoef &rc = sd.rec[NL + k];
+    Br[k] = f[P - 1];
+    y[P - 1] = fma(rc.alpha, Br[k], y[P - 1]);
+#pragma unroll
+    for (int p = P - 2; p >= 0; --p) {
+      Br[k] = fma(rc.rpow[1], Br[k], f[p]);
+      y[p] = fma(rc.alpha, Br[k], y[p]);
+    }
+  }
+  // ---- warp scans of the chunk totals (interleaved) --------------------------------
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const double v = __shfl_up_sync(FULL, A[k], d);
+      if (lane >= d) A[k] = fma(sd.rec[k].rchunk[d], v, A[k]);
+    }
+    if constexpr (NL >= 2) {
+      if (pair) {
+        const double vr = __shfl_up_sync(FULL, Cr, d), vi = __shfl_up_sync(FULL, Ci, d);
+        if (lane >= d) cfma(sd.crec[0].rcr[d], sd.crec[0].rci[d], vr, vi, Cr, Ci);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      const double v = __shfl_down_sync(FULL, Br[k], d);
+      if (lane + d < 32) Br[k] = fma(sd.rec[NL + k].rchunk[d], v, Br[k]);
+    }
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) wb[k * NW + warp] = A[k];
+    if constexpr (NL >= 2) {
+      wb[NL * NW + warp] = Cr;
+      wb[(NL + 1) * NW + warp] = Ci;
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) wb[(NL + 2 * (NL / 2) + k) * NW + warp] = Br[k];
+  }
+  __syncthreads();
+  const int ld = lane < NW ? lane : 0;
+  // ---- carries entering the warp, then entering the lane; fix-up into y ------------
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    const RecCoef &rc = sd.rec[k];
+    const double cw = warp_carry_fwd<NW>(wb[k * NW + ld], rc.rwarp, rc.closure, warp, lane);
+    const double Ap = __shfl_up_sync(FULL, A[k], 1);
+    const double cin = (lane == 0) ? cw : fma(rc.rchunk[lane], cw, Ap);
+    const double ac = rc.alpha * cin;
+#pragma unroll
+    for (int p = 0; p < P; ++p) y[p] = fma(rc.rpow[p + 1], ac, y[p]);
+  }
+  if constexpr (NL >= 2) {
+    if (pair) {
+      const CRecCoef &rc = sd.crec[0];
+      double cr, ci;
+      warp_carry_cplx<NW>(wb[NL * NW + ld], wb[(NL + 1) * NW + ld], rc, warp, lane, cr, ci);
+      const double Pr = __shfl_up_sync(FULL, Cr, 1), Pi = __shfl_up_sync(FULL, Ci, 1);
+      double inr = cr, ini = ci;
+      if (lane != 0) {
+        inr = Pr;
+        ini = Pi;
+        cfma(rc.rcr[lane], rc.rci[lane], cr, ci, inr, ini);
+      }
+      double acr = 0.0, aci = 0.0;                   // (2 gamma A) * cin
+      cfma(rc.ar, rc.ai, inr, ini, acr, aci);
+#pragma unroll
+      for (int p = 0; p < P; ++p) y[p] = fma(rc.rpr[p + 1], acr, fma(-rc.rpi[p + 1], aci, y[p]));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const RecCoef &rc = sd.rec[NL + k];
+    const int slot = NL + 2 * (NL / 2) + k;
+    const double cw = warp_carry_bwd<NW>(wb[slot * NW + ld], rc.rwarp, rc.closure, warp, lane);
+    const double Bn = __shfl_down_sync(FULL, Br[k], 1);
+    const double cin = (lane == 31) ? cw : fma(rc.rchunk[31 - lane], cw, Bn);
+    const double ac = rc.alpha * cin;
+#pragma unroll
+    for (int p = 0; p < P; ++p) y[p] = fma(rc.rpow[P - p], ac, y[p]);
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) f[p] = y[p];
+  wphase ^= 1;
+}
+
 template <int P, int NT>
 __device__ __forceinline__ void stage_solve(double (&y)[P], const SdirkCoef &sd, double *wbuf,
                                             int &wphase) {
@@ -240,7 +441,10 @@ __device__ __forceinline__ void dirk_step(double (&x)[P], const RKCoeffs &c, con
   }
 #pragma unroll
   for (int i = 0; i < S; ++i) {
-    stage_solve<P, NT>(acc[i], sd, wbuf, wphase);
+    if (sd.fused)
+      fused_stage_solve<SC::NL, SC::NR, P, NT>(acc[i], sd, wbuf, wphase);
+    else
+      stage_solve<P, NT>(acc[i], sd, wbuf, wphase);
     double k[P];
     apply_Z<SC::NL, SC::NR, P, NT>(acc[i], k, c.z, edge, phase);
 #pragma unroll

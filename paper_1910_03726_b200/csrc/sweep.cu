@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
   double *sB = sA + NT * SP;
   double *edge = sB + NT * SP;
   double *red = edge + 2 * NT * (SC::NL + SC::NR) + 2;
-  double *wbuf = red + NW + 2;  // 4*NW (SDIRK recurrences: 2 phases x complex)
+  double *wbuf = red + NW + 2;  // 16*NW (SDIRK recurrences: 2 phases x <= 8 slots)
   int wphase = 0;
 
   const int item = blockIdx.x / a.ntiles;
@@ -246,24 +246,29 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
       store(row, (!a.cmp.base && (nstage & 1)) ? CM : IN(b), x, abeg, T, true);
       ++nstage;
     };
-    // Step 1 is peeled so the thread-0 prefetch does not sit inside the step loop (a
-    // divergent region there costs a reconvergence point per step); per-step writes get
-    // their own loop for the same reason.
+    // The steps before and after the thread-0 prefetch run in separate loops so the
+    // divergent issue region does not sit inside a step loop (a reconvergence point per
+    // step); per-step writes get their own loops for the same reason.
     if (a.each_first == 0 && a.each_last >= 0) each_store(0);
-    if (a.nsteps1 >= 1) {
-      erk_step<SC, P, NT>(x, a.co, edge, phase);
-      if (!early) issue_loads();
-      if (1 >= a.each_first && 1 <= a.each_last) each_store(1);
-    }
+    const int la = early ? 0 : min(max(a.load_after, 1), a.nsteps1);
     if (a.each_last >= a.each_first) {
 #pragma unroll 1
-      for (int i = 2; i <= a.nsteps1; ++i) {
+      for (int i = 1; i <= la; ++i) {
+        erk_step<SC, P, NT>(x, a.co, edge, phase);
+        if (i >= a.each_first && i <= a.each_last) each_store(i);
+      }
+      if (!early) issue_loads();
+#pragma unroll 1
+      for (int i = la + 1; i <= a.nsteps1; ++i) {
         erk_step<SC, P, NT>(x, a.co, edge, phase);
         if (i >= a.each_first && i <= a.each_last) each_store(i);
       }
     } else {
 #pragma unroll 1
-      for (int i = 2; i <= a.nsteps1; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
+      for (int i = 1; i <= la; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
+      if (!early) issue_loads();
+#pragma unroll 1
+      for (int i = la + 1; i <= a.nsteps1; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
     }
     if (a.endw.base) store(const_cast<double *>(rowp(a.endw, item)), IN(b), x, abeg, T, false);
     if (a.cmp.base) {
@@ -492,7 +497,7 @@ template <class SC, int NT, int P>
 static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int SP = Pad<P>::SP;
   const size_t smem = sizeof(double) * (2 * NT * SP + 2 * NT * (SC::NL + SC::NR) + 2 +
-                                        NT / 32 + 2 + 4 * (NT / 32) + 2);
+                                        NT / 32 + 2 + 16 * (NT / 32) + 2);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rk_sweep_kernel<SC, NT, P>,

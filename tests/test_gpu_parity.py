@@ -110,6 +110,36 @@ def test_relax_primitives(order, tab, cfl, nx, nt, m):
         assert _rel(Ug, Uo) <= REL, (kind, _rel(Ug, Uo))
 
 
+SDIRK_FORMS = [  # (order, tableau, cfl, nx): real, complex-pair and mixed root sets
+    (1, "sdirk1", 4.0, 64), (1, "sdirk1", 1.0, 512), (2, "sdirk2", 1.0, 256),
+    (2, "sdirk2", 4.0, 1024), (3, "sdirk3", 1.0, 256), (3, "sdirk3", 4.0, 4096),
+    (4, "sdirk4", 1.0, 128), (4, "sdirk4", 4.0, 2048), (4, "sdirk4", 8.0, 4096),
+]
+
+
+@pytest.mark.parametrize("order,tab,cfl,nx", SDIRK_FORMS)
+def test_sdirk_fused_vs_product_form(order, tab, cfl, nx, monkeypatch):
+    """The partial-fraction (fused, one barrier) stage solve and the product of
+    first-order periodic solves (MGRIT_SDIRK_PRODUCT=1) are the same operator (sdirk.cuh):
+    F-relaxation of the FULL state agrees with the oracle for both and between them."""
+    B = _cuda()
+    nt, m = 16, 4
+    phi = D.make_phi(order, tab, cfl, nx)
+    U0 = W.initial_iterate(9, nx, nt, W.u0_fourier(nx, 2))
+    Uo = U0.copy()
+    M.f_relax(Uo, phi, m)
+    psi = [{"kind": "stencil", "offsets": [-1, 0], "coeffs": [0.5, 0.5]}]
+    outs = []
+    for prod in ("0", "1"):
+        monkeypatch.setenv("MGRIT_SDIRK_PRODUCT", prod)
+        s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2, psi, "FCF")
+        Ug = torch.from_numpy(U0).cuda()
+        s.relax_full(Ug, "F")
+        outs.append(Ug.cpu().numpy())
+        assert _rel(outs[-1], Uo) <= REL, (prod, _rel(outs[-1], Uo))
+    assert _rel(outs[0], outs[1]) <= 1e-13
+
+
 @pytest.mark.parametrize("order,tab,cfl", [(2, "sdirk2", 4.0), (4, "sdirk4", 4.0)])
 def test_sdirk_complex_pair_solve(order, tab, cfl):
     """SDIRK2+U2 / SDIRK4+U4 (stage matrices with a complex-conjugate symbol-root pair,
