@@ -289,6 +289,15 @@ void make_sdirk_fused(const std::vector<std::complex<long double>> &roots, long 
   f.ncrec = npair;
   f.nrec = NL + NR;
   f.beta = (double)(gamma * cst).real();
+  // scan truncation: weights (rho^P)^d below 2^-70 are beyond fp64 resolution
+  long double rmax = 0.0L;
+  for (auto &x : a) rmax = std::max(rmax, (long double)std::abs(x));
+  for (auto &x : b) rmax = std::max(rmax, (long double)std::abs(x));
+  const long double tiny = ldexpl(1.0L, -70);
+  f.dmax = 32;
+  for (int d = 1; d < 32; d <<= 1)
+    if (powl(rmax, (long double)(P * d)) < tiny) { f.dmax = d; break; }
+  f.warp_local = powl(rmax, (long double)(32 * P)) < tiny ? 1 : 0;
   f.fused = 1;
   sd = f;
 }

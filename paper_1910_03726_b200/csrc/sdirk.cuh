@@ -53,6 +53,10 @@ struct SdirkCoef {
   int nrf;                 // fused form: forward real factors in rec[0..nrf), backward after
   double gamma;            // M^-1 = gamma * prod (bidiagonal inverses)
   double beta;             // fused form: gamma * constant term of the partial fractions
+  int dmax;                // fused form: warp-scan distances d < dmax (farther lanes' weights
+                           //   (rho^P)^d < 2^-70 are below fp64 resolution), power of 2
+  int warp_local;          // fused form: 1 if (rho^(32P)) < 2^-70 for every factor, so the
+                           //   carry entering a warp is the previous warp's total alone
   RecCoef rec[MAXREC];
   CRecCoef crec[MAXCREC];  // one per complex-conjugate root pair
 };
@@ -284,6 +288,25 @@ __device__ __forceinline__ void warp_carry_cplx(double tr, double ti, const CRec
   cfma(rc.rwr[warp], rc.rwi[warp], c0r, c0i, cr, ci);
 }
 
+// Per-lane carry multipliers of the fused solve, built once per CTA in shared memory
+// (lane-indexed constant-bank loads would serialise across the warp): slot k < NL:
+// (rho_k^P)^lane; pair slots NL, NL+1: Re/Im (rho^P)^lane; backward slots:
+// (rho^P)^(31-lane).  Layout [slot][32] at wbuf + 16*NW.
+template <int NL, int NR, int NT>
+__device__ __forceinline__ void fused_lane_tables(const SdirkCoef &sd, double *wbuf) {
+  constexpr int NW = NT / 32;
+  constexpr int NSLOT = NL + 2 * (NL / 2) + NR;
+  double *lt = wbuf + 2 * 8 * NW;
+  for (int t = threadIdx.x; t < NSLOT * 32; t += NT) {
+    const int slot = t >> 5, l = t & 31;
+    double v;
+    if (slot < NL) v = sd.rec[slot].rchunk[l];
+    else if (slot < NL + 2 * (NL / 2)) v = (slot == NL) ? sd.crec[0].rcr[l] : sd.crec[0].rci[l];
+    else v = sd.rec[NL + (slot - NL - 2 * (NL / 2))].rchunk[31 - l];
+    lt[t] = v;
+  }
+}
+
 template <int NL, int NR, int P, int NT>
 __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoef &sd,
                                                   double *wbuf, int &wphase) {
@@ -292,6 +315,7 @@ __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoe
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool pair = (NL >= 2) && sd.ncrec > 0;   // warp-uniform
   double *wb = wbuf + wphase * NSLOT * NW;
+  const double *lt = wbuf + 2 * 8 * NW;            // lane tables (fused_lane_tables)
   double y[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) y[p] = sd.beta * f[p];
@@ -338,6 +362,7 @@ __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoe
   // ---- warp scans of the chunk totals (interleaved) --------------------------------
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
+    if (d >= sd.dmax) break;  // warp-uniform
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
       const double v = __shfl_up_sync(FULL, A[k], d);
@@ -369,13 +394,16 @@ __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoe
   }
   __syncthreads();
   const int ld = lane < NW ? lane : 0;
+  const bool wl = sd.warp_local != 0;
+  const int wprev = (warp + NW - 1) % NW, wnext = (warp + 1) % NW;
   // ---- carries entering the warp, then entering the lane; fix-up into y ------------
 #pragma unroll
   for (int k = 0; k < NL; ++k) {
     const RecCoef &rc = sd.rec[k];
-    const double cw = warp_carry_fwd<NW>(wb[k * NW + ld], rc.rwarp, rc.closure, warp, lane);
+    const double cw = wl ? wb[k * NW + wprev] * (warp ? 1.0 : rc.closure)
+                         : warp_carry_fwd<NW>(wb[k * NW + ld], rc.rwarp, rc.closure, warp, lane);
     const double Ap = __shfl_up_sync(FULL, A[k], 1);
-    const double cin = (lane == 0) ? cw : fma(rc.rchunk[lane], cw, Ap);
+    const double cin = (lane == 0) ? cw : fma(lt[k * 32 + lane], cw, Ap);
     const double ac = rc.alpha * cin;
 #pragma unroll
     for (int p = 0; p < P; ++p) y[p] = fma(rc.rpow[p + 1], ac, y[p]);
@@ -384,13 +412,24 @@ __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoe
     if (pair) {
       const CRecCoef &rc = sd.crec[0];
       double cr, ci;
-      warp_carry_cplx<NW>(wb[NL * NW + ld], wb[(NL + 1) * NW + ld], rc, warp, lane, cr, ci);
+      if (wl) {
+        const double tr = wb[NL * NW + wprev], ti = wb[(NL + 1) * NW + wprev];
+        cr = tr;
+        ci = ti;
+        if (!warp) {
+          cr = 0.0;
+          ci = 0.0;
+          cfma(tr, ti, rc.clr, rc.cli, cr, ci);
+        }
+      } else {
+        warp_carry_cplx<NW>(wb[NL * NW + ld], wb[(NL + 1) * NW + ld], rc, warp, lane, cr, ci);
+      }
       const double Pr = __shfl_up_sync(FULL, Cr, 1), Pi = __shfl_up_sync(FULL, Ci, 1);
       double inr = cr, ini = ci;
       if (lane != 0) {
         inr = Pr;
         ini = Pi;
-        cfma(rc.rcr[lane], rc.rci[lane], cr, ci, inr, ini);
+        cfma(lt[NL * 32 + lane], lt[(NL + 1) * 32 + lane], cr, ci, inr, ini);
       }
       double acr = 0.0, aci = 0.0;                   // (2 gamma A) * cin
       cfma(rc.ar, rc.ai, inr, ini, acr, aci);
@@ -402,9 +441,10 @@ __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoe
   for (int k = 0; k < NR; ++k) {
     const RecCoef &rc = sd.rec[NL + k];
     const int slot = NL + 2 * (NL / 2) + k;
-    const double cw = warp_carry_bwd<NW>(wb[slot * NW + ld], rc.rwarp, rc.closure, warp, lane);
+    const double cw = wl ? wb[slot * NW + wnext] * (warp < NW - 1 ? 1.0 : rc.closure)
+                         : warp_carry_bwd<NW>(wb[slot * NW + ld], rc.rwarp, rc.closure, warp, lane);
     const double Bn = __shfl_down_sync(FULL, Br[k], 1);
-    const double cin = (lane == 31) ? cw : fma(rc.rchunk[31 - lane], cw, Bn);
+    const double cin = (lane == 31) ? cw : fma(lt[slot * 32 + lane], cw, Bn);
     const double ac = rc.alpha * cin;
 #pragma unroll
     for (int p = 0; p < P; ++p) y[p] = fma(rc.rpow[P - p], ac, y[p]);

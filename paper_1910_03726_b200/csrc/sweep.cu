@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
   double *sB = sA + NT * SP;
   double *edge = sB + NT * SP;
   double *red = edge + 2 * NT * (SC::NL + SC::NR) + 2;
-  double *wbuf = red + NW + 2;  // 16*NW (SDIRK recurrences: 2 phases x <= 8 slots)
+  double *wbuf = red + NW + 2;  // 16*NW (SDIRK recurrences: 2 phases x <= 8 slots) + lane tables
   int wphase = 0;
 
   const int item = blockIdx.x / a.ntiles;
@@ -73,6 +73,8 @@ __global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ Sw
     for (int q = tid; q < T; q += NT) row[abeg + q] = sA[pidx<P>(a.HL + q)];
   };
 
+  if constexpr (SC::implicit)
+    if (a.sd.fused) fused_lane_tables<SC::NL, SC::NR, NT>(a.sd, wbuf);
   if (a.in.base) load_window(rowp(a.in, item), sA);
   if (a.cmp.base) load_window(rowp(a.cmp, item), sB);
   __syncthreads();
@@ -497,7 +499,7 @@ template <class SC, int NT, int P>
 static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int SP = Pad<P>::SP;
   const size_t smem = sizeof(double) * (2 * NT * SP + 2 * NT * (SC::NL + SC::NR) + 2 +
-                                        NT / 32 + 2 + 16 * (NT / 32) + 2);
+                                        NT / 32 + 2 + 16 * (NT / 32) + 8 * 32 + 2);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rk_sweep_kernel<SC, NT, P>,
