@@ -91,7 +91,8 @@ def _profile_traffic():
     """dram bytes per fine-sweep launch from the committed ncu summary, if present."""
     p = os.path.join(ROOT, "profiles", "fine_sweep_ncu.json")
     try:
-        return json.load(open(p)).get("dram_bytes_per_launch")
+        d = json.load(open(p))
+        return (d[0] if isinstance(d, list) else d).get("dram_bytes_per_launch")
     except Exception:
         return None
 
