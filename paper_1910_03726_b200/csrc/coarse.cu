@@ -773,7 +773,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
   for (int i = 1; i <= N; ++i) {
     double *cur = smem + ((i - 1) & 1) * BL, *nxt = smem + (i & 1) * BL;
     if (k == 0) {  // start of super-step j: halo threads take x_{jS} from R[j&1]
-      if (lhalo || rhalo) {
+      if ((lhalo || rhalo) && !(a.dbg & 1)) {
         mbar_wait(&hb[j % 3], (uint32_t)((j / 3) & 1));
         const double *rj = R + (j & 1) * CS::EMAX + (lhalo ? EL + l0 : EL + (l0 - Wc));
         double h[P];
@@ -781,12 +781,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
         for (int p = 0; p < P; ++p) h[p] = rj[p];
         put(cur, h);
       }
-      if (tid == 0) mbar_expect_tx(&hb[j % 3], hbytes);  // re-arm for exchange j + 3
+      if (tid == 0 && !(a.dbg & 1)) mbar_expect_tx(&hb[j % 3], hbytes);  // re-arm for j + 3
       __syncthreads();
     }
     ++k;
-    prefetch(i + D - 1);
-    cp_async_wait<D - 1>();                        // this thread's rows of step i landed
+    if (!(a.dbg & 2)) {
+      prefetch(i + D - 1);
+      cp_async_wait<D - 1>();                      // this thread's rows of step i landed
+    }
     if (active) {
       double y[P];
       if constexpr (NU4 <= 32) {
@@ -799,12 +801,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
       for (int p = 0; p < P; ++p) x[p] = y[p] + gs[p];   // x_i = Psi x_{i-1} + g_i
       put(nxt, x);
       if (own) {
-        if (k == S || i == N) send(j + 1, x);      // exact own values of x_{(j+1)S}
+        if ((k == S || i == N) && !(a.dbg & 1)) send(j + 1, x);  // exact own x_{(j+1)S}
         const double *vs = vring + (i % D) * Wc + l0;
         double *orow = ob + (long long)i * ost;
+        if (!(a.dbg & 2)) {
 #pragma unroll
-        for (int p = 0; p < P; p += 2)             // u_i = v_i + e_i
-          *reinterpret_cast<double2 *>(orow + p) = make_double2(vs[p] + x[p], vs[p + 1] + x[p + 1]);
+          for (int p = 0; p < P; p += 2)           // u_i = v_i + e_i
+            *reinterpret_cast<double2 *>(orow + p) = make_double2(vs[p] + x[p], vs[p + 1] + x[p + 1]);
+        }
       }
     }
     if (k == S) { k = 0; ++j; }
@@ -817,7 +821,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
   }
   // the last exchange may still be landing here: wait for it, keep shared memory alive
   const int jl = k == 0 ? j : j + 1;
-  if (tid == 0) mbar_wait(&hb[jl % 3], (uint32_t)((jl / 3) & 1));
+  if (tid == 0 && !(a.dbg & 1)) mbar_wait(&hb[jl % 3], (uint32_t)((jl / 3) & 1));
   cluster.sync();
 }
 
@@ -873,6 +877,266 @@ cudaError_t launch_psi_seq_cluster_ca(int cl, SweepCfg c, int S, const CoarseArg
   if (cl == 8 && c.nt_threads == 128 && c.p == 4) return launch_seq_ca<128, 4, 8>(a, S, s);
   if (cl == 16 && c.nt_threads == 64 && c.p == 4) return launch_seq_ca<64, 4, 16>(a, S, s);
   if (cl == 8 && c.nt_threads == 32 && c.p == 4) return launch_seq_ca<32, 4, 8>(a, S, s);
+  return cudaErrorInvalidConfiguration;
+}
+
+// --------------------------------------------------------------------------
+// Communication-avoiding cluster solve, warp-specialised ("lean step").  Same split,
+// s-step halos and point-to-point DSMEM exchange as psi_seq_cluster_ca_kernel, but the
+// compute warps' per-step instruction stream -- which sets the step latency of this
+// sequential chain -- carries no global-memory work at all:
+//  * a producer warp streams the g rows into a ring of 3 sets x 4 rows (extended region
+//    EL+Wc+ER per row) with bulk copies, up to 12 steps ahead;
+//  * the correction u_n = v_n + e_n is a bulk reduce-add of the own slice of e_n
+//    into the C-row (which holds v_n): compute threads stage e_n in a 3 x 4-row ring, the
+//    producer issues the reduce-adds and frees the set once they have read it;
+//  * compute warps synchronise with a named barrier (the producer never joins it) and
+//    meet the producer through mbarriers once per 4 steps: g set full / free, staging set
+//    full / free;
+//  * the stencil window's phase (o0 mod P) is a template parameter, fixed for the launch.
+// Per step: window loads, NU4*P FMAs (2 partial sums), + g, publish, one named barrier.
+template <int NT, int P> struct TbSmem {
+  using CS = CaSmem<NT, P>;
+  static constexpr int Wc = NT * P, GW = CS::EMAX + Wc, NS = 12;
+  static constexpr size_t BYTES =
+      sizeof(double) * (2 * (size_t)CS::BL + 2 * CS::EMAX + (size_t)NS * (GW + Wc)) + 128;
+};
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int NT, int P, int CL, int NU4, int REM>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160)
+    psi_seq_cluster_tb_kernel(const __grid_constant__ CoarseArgs a, int S) {
+  static_assert(P % 2 == 0, "P even (16-byte rows)");
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  using CS = CaSmem<NT, P>;
+  using TS = TbSmem<NT, P>;
+  constexpr int Wc = CS::Wc, BL = CS::BL, COLS = CS::COLS, MARG = CS::MARG, GW = TS::GW;
+  extern __shared__ __align__(128) double smem[];
+  double *R = smem + 2 * BL;                        // receive buffers [2][EMAX]
+  double *gring = R + 2 * CS::EMAX;                 // [12][GW]
+  double *oring = gring + (size_t)TS::NS * GW;      // [12][Wc]
+  uint64_t *hb = reinterpret_cast<uint64_t *>(oring + (size_t)TS::NS * Wc);  // [3] exchange
+  uint64_t *gfull = hb + 3, *gfree = hb + 6, *ofull = hb + 9, *ofree = hb + 12;
+  const uint32_t rank = cluster.block_rank();
+  const int tid = threadIdx.x, nthr = blockDim.x, ncomp = nthr - 32;
+  const bool producer = tid >= ncomp;
+  const int N = a.nsteps, nx = a.nx, o0 = a.op.o0, nu = a.op.nu;
+  const int H = (N + 3) / 4;                        // halves of 4 steps
+  const int HL = o0 < 0 ? max(-o0, 1) : 1, HR = max(o0 + nu - 1, 1);
+  const int EL = ((S * HL + P - 1) / P) * P, ER = ((S * HR + P - 1) / P) * P;
+  const int GWa = EL + Wc + ER;                     // extended row length (even)
+  const uint32_t hbytes = (uint32_t)(EL + ER) * 8u;
+  const int l0 = -EL + tid * P;
+  const bool active = !producer && l0 < Wc + ER;
+  const bool own = !producer && l0 >= 0 && l0 < Wc;
+  const bool lhalo = !producer && l0 < 0, rhalo = !producer && l0 >= Wc && active;
+  const int own0 = (int)rank * Wc;                  // global index of local point 0
+  int gx = own0 + l0;
+  if (gx < 0) gx += nx;
+  if (gx >= nx) gx -= nx;
+  int seg0 = own0 - EL;                             // extended segment start (periodic)
+  if (seg0 < 0) seg0 += nx;
+  const uint32_t rprev = (rank + CL - 1) % CL, rnext = (rank + 1) % CL;
+  const uint32_t r_loc = smem_u32(R), hb_loc = smem_u32(hb);
+  const uint32_t p_R = mapa_shared(r_loc, rprev), n_R = mapa_shared(r_loc, rnext);
+  const uint32_t p_hb = mapa_shared(hb_loc, rprev), n_hb = mapa_shared(hb_loc, rnext);
+  const int col = (MARG + tid * P) / P;             // SoA column of point l0
+  const int wcol = (MARG + tid * P + o0 - REM) / P; // window column (phase REM = o0 mod P)
+  auto put = [&](double *b, const double(&x)[P]) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) b[p * COLS + col] = x[p];
+  };
+  auto send = [&](int j, const double(&x)[P]) {
+    if (!own) return;
+    const int rb = (j & 1) * CS::EMAX;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int l = l0 + p;
+      if (l < ER)
+        st_async_f64(p_R + 8u * (uint32_t)(rb + EL + l), x[p], p_hb + 8u * (uint32_t)(j % 3));
+      if (l >= Wc - EL)
+        st_async_f64(n_R + 8u * (uint32_t)(rb + l - (Wc - EL)), x[p], n_hb + 8u * (uint32_t)(j % 3));
+    }
+  };
+  for (int q = tid; q < 2 * BL; q += nthr) smem[q] = 0.0;  // margins stay finite
+  if (tid == 0) {
+    for (int k = 0; k < 15; ++k) mbar_init(&hb[k], 1);
+    fence_mbar_init();
+    for (int k = 0; k < 3; ++k) mbar_expect_tx(&hb[k], hbytes);
+  }
+  double x[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) x[p] = (own && a.state_in) ? a.state_in[gx + p] : 0.0;
+  cluster.sync();  // buffers zeroed, barriers armed everywhere before any remote store
+
+  if (producer) {
+    // ---- producer warp: lanes q = 0..3 handle row 4t+1+q of half t --------------------
+    const int q = tid - ncomp;
+    const int n1g = (seg0 + GWa <= nx) ? GWa : nx - seg0;
+    auto issue_g = [&](int t) {  // half t -> set t % 3
+      if (q == 0) mbar_expect_tx(&gfull[t % 3], (uint32_t)((min(N, 4 * t + 4) - 4 * t) * GWa) * 8u);
+      __syncwarp();
+      const int r = 4 * t + 1 + q;
+      if (q < 4 && r <= N) {
+        double *dst = gring + (size_t)((r - 1) % TS::NS) * GW;
+        const double *src = a.g.base + (a.g.off + (a.n0 + r) * a.g.stride) * (long long)nx;
+        tma_load_1d(dst, src + seg0, (uint32_t)n1g * 8u, &gfull[t % 3]);
+        if (n1g < GWa) tma_load_1d(dst + n1g, src, (uint32_t)(GWa - n1g) * 8u, &gfull[t % 3]);
+      }
+    };
+    for (int t = 0; t < 3 && t < H; ++t) issue_g(t);
+    for (int t = 0; t < H; ++t) {
+      // staging set of half t full -> reduce-add into out, free the set once read
+      mbar_wait(&ofull[t % 3], (uint32_t)((t / 3) & 1));
+      const int r = 4 * t + 1 + q;
+      if (q < 4 && r <= N) {
+        double *dst = const_cast<double *>(a.out.base) +
+                      (a.out.off + (a.n0 + r) * a.out.stride) * (long long)nx + own0;
+        tma_reduce_add_1d(dst, oring + (size_t)((r - 1) % TS::NS) * Wc, (uint32_t)Wc * 8u);
+      }
+      bulk_commit();
+      bulk_wait_read_all();
+      __syncwarp();
+      if (q == 0) mbar_arrive(&ofree[t % 3]);
+      // g set of half t read by every compute thread -> reload it with half t + 3
+      if (t + 3 < H) {
+        mbar_wait(&gfree[t % 3], (uint32_t)((t / 3) & 1));
+        issue_g(t + 3);
+      }
+    }
+    bulk_wait_all();
+  } else {
+    // ---- compute warps ---------------------------------------------------------------
+    if (own) put(smem, x);
+    send(0, x);
+    int j = 0, k = 0;                              // super-step j, local step k (1..S)
+    int h = 0, kh = 0, slot = 0;                   // half h, step in the half, (i-1) % 12
+#pragma unroll 1
+    for (int i = 1; i <= N; ++i) {
+      double *cur = smem + ((i - 1) & 1) * BL, *nxt = smem + (i & 1) * BL;
+      if (k == 0) {  // start of super-step j: halo threads take x_{jS} from R[j&1]
+        if (lhalo || rhalo) {
+          mbar_wait(&hb[j % 3], (uint32_t)((j / 3) & 1));
+          const double *rj = R + (j & 1) * CS::EMAX + (lhalo ? EL + l0 : EL + (l0 - Wc));
+          double hv[P];
+#pragma unroll
+          for (int p = 0; p < P; ++p) hv[p] = rj[p];
+          put(cur, hv);
+        }
+        if (tid == 0) mbar_expect_tx(&hb[j % 3], hbytes);  // re-arm for exchange j + 3
+        named_bar(1, ncomp);
+      }
+      ++k;
+      if (kh == 0) {  // start of half h: hand half h-1's sets back, take half h's
+        if (tid == 0 && h > 0) {
+          mbar_arrive(&gfree[(h - 1) % 3]);
+          mbar_arrive(&ofull[(h - 1) % 3]);
+        }
+        mbar_wait(&gfull[h % 3], (uint32_t)((h / 3) & 1));
+        if (own && h >= 3) mbar_wait(&ofree[h % 3], (uint32_t)(((h - 3) / 3) & 1));
+      }
+      if (active) {
+        double w[P + NU4 - 1];
+        const double *s0 = cur + wcol;
+#pragma unroll
+        for (int r = 0; r < P + NU4 - 1; ++r) w[r] = s0[((REM + r) % P) * COLS + (REM + r) / P];
+        double acc0[P], acc1[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) { acc0[p] = 0.0; acc1[p] = 0.0; }
+#pragma unroll
+        for (int qq = 0; qq < NU4; qq += 2) {
+          const double c0 = a.op.psi[qq], c1 = a.op.psi[qq + 1];
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            acc0[p] = fma(c0, w[p + qq], acc0[p]);
+            acc1[p] = fma(c1, w[p + qq + 1], acc1[p]);
+          }
+        }
+        const double *gs = gring + (size_t)slot * GW + tid * P;
+#pragma unroll
+        for (int p = 0; p < P; ++p) x[p] = (acc0[p] + acc1[p]) + gs[p];  // x_i = Psi x_{i-1} + g_i
+        put(nxt, x);
+        if (own) {
+          double *os = oring + (size_t)slot * Wc + l0;
+#pragma unroll
+          for (int p = 0; p < P; ++p) os[p] = x[p];
+          if (kh == 3 || i == N) fence_proxy_async();  // the half's staged rows -> async proxy
+          if (k == S || i == N) send(j + 1, x);        // exact own values of x_{(j+1)S}
+        }
+      }
+      if (k == S) { k = 0; ++j; }
+      if (++kh == 4) { kh = 0; ++h; }
+      if (++slot == TS::NS) slot = 0;
+      named_bar(1, ncomp);
+    }
+    if (tid == 0) mbar_arrive(&ofull[(H - 1) % 3]);  // the last half is staged
+    if (own && a.state_out) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) a.state_out[gx + p] = x[p];
+    }
+    const int jl = k == 0 ? j : j + 1;
+    if (tid == 0) mbar_wait(&hb[jl % 3], (uint32_t)((jl / 3) & 1));
+  }
+  cluster.sync();
+}
+
+template <int NT, int P, int CL, int NU4, int REM>
+static cudaError_t launch_seq_tb_rem(const CoarseArgs &a, int S, int nthr, cudaStream_t s) {
+  const size_t smem = TbSmem<NT, P>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(psi_seq_cluster_tb_kernel<NT, P, CL, NU4, REM>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (CL > 8)
+      cudaFuncSetAttribute(psi_seq_cluster_tb_kernel<NT, P, CL, NU4, REM>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  psi_seq_cluster_tb_kernel<NT, P, CL, NU4, REM><<<CL, nthr, smem, s>>>(a, S);
+  return cudaGetLastError();
+}
+
+template <int NT, int P, int CL, int NU4>
+static cudaError_t launch_seq_tb_nu(const CoarseArgs &a, int S, int nthr, cudaStream_t s) {
+  const int rem = ((a.op.o0 % P) + P) % P;
+  if constexpr (P == 2) {
+    if (rem == 0) return launch_seq_tb_rem<NT, P, CL, NU4, 0>(a, S, nthr, s);
+    return launch_seq_tb_rem<NT, P, CL, NU4, 1>(a, S, nthr, s);
+  } else {
+    if (rem == 0) return launch_seq_tb_rem<NT, P, CL, NU4, 0>(a, S, nthr, s);
+    if (rem == 1) return launch_seq_tb_rem<NT, P, CL, NU4, 1>(a, S, nthr, s);
+    if (rem == 2) return launch_seq_tb_rem<NT, P, CL, NU4, 2>(a, S, nthr, s);
+    return launch_seq_tb_rem<NT, P, CL, NU4, 3>(a, S, nthr, s);
+  }
+}
+
+template <int NT, int P, int CL>
+static cudaError_t launch_seq_tb(const CoarseArgs &a, int S, cudaStream_t s) {
+  const int o0 = a.op.o0, nu = a.op.nu;
+  const int HL = o0 < 0 ? std::max(-o0, 1) : 1, HR = std::max(o0 + nu - 1, 1);
+  const int EL = ((S * HL + P - 1) / P) * P, ER = ((S * HR + P - 1) / P) * P;
+  const int nthr = NT + (((EL + ER) / P + 31) / 32) * 32 + 32;  // + producer warp
+  if (nu <= 10) return launch_seq_tb_nu<NT, P, CL, 10>(a, S, nthr, s);
+  if (nu <= 12) return launch_seq_tb_nu<NT, P, CL, 12>(a, S, nthr, s);
+  if (nu <= 16) return launch_seq_tb_nu<NT, P, CL, 16>(a, S, nthr, s);
+  if (nu <= 32) return launch_seq_tb_nu<NT, P, CL, 32>(a, S, nthr, s);
+  return cudaErrorInvalidValue;
+}
+
+// Same configurations / depth rule as the CA kernel (seq_ca_depth); windows up to 32 taps.
+cudaError_t launch_psi_seq_cluster_tb(int cl, SweepCfg c, int S, const CoarseArgs &a, cudaStream_t s) {
+  if (a.nsteps <= 0) return cudaSuccess;
+  if (a.op.nu > 32) return cudaErrorInvalidValue;
+  if (cl == 16 && c.nt_threads == 128 && c.p == 2) return launch_seq_tb<128, 2, 16>(a, S, s);
+  if (cl == 16 && c.nt_threads == 32 && c.p == 2) return launch_seq_tb<32, 2, 16>(a, S, s);
+  if (cl == 16 && c.nt_threads == 64 && c.p == 4) return launch_seq_tb<64, 4, 16>(a, S, s);
   return cudaErrorInvalidConfiguration;
 }
 

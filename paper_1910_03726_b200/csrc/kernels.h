@@ -80,6 +80,7 @@ struct CoarseArgs {
   const double *state_in;  // x_{n0} (nx), null: zero
   double *state_out;       // x_{n0+nsteps} (nx), null: not stored
   PsiOp op;
+  int dbg;                 // experiments only (MGRIT_COARSE_DBG): 1 no halo exchange, 2 no I/O
 };
 cudaError_t launch_psi_coarse(SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);
 // Periodic whole-row single-CTA variant (NT*P == nx), fixed coordinates, per-thread
@@ -92,6 +93,9 @@ bool seq_cluster_ok(int cl, SweepCfg cfg, int nx, int o0, int nu);
 // Communication-avoiding variant: S steps per halo exchange (extended halos S*HL, S*HR).
 cudaError_t launch_psi_seq_cluster_ca(int cl, SweepCfg cfg, int S, const CoarseArgs &a, cudaStream_t s);
 int seq_ca_depth(int cl, SweepCfg cfg, int nx, int o0, int nu, int smax);
+// Same split and s-step halos with batched TMA I/O (g ring, reduce-add correction), the
+// launch's window phase as a template parameter; nu <= 32.
+cudaError_t launch_psi_seq_cluster_tb(int cl, SweepCfg cfg, int S, const CoarseArgs &a, cudaStream_t s);
 
 // Level-l (l >= 2) relaxation sweep of the V-cycle with Psi_l and RHS g (u = 0 start):
 //   phase 1: x_i = Psi x_{i-1} + g[jm+i], i=1..m, x_0 = u_j (null: 0) -> v_{j+1}

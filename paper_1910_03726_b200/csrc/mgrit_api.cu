@@ -698,6 +698,16 @@ struct CoarsePlan {
   SweepCfg cfg = {0, 0};
   int ntiles = 1, cl = 0, S = 0;
 };
+// The warp-specialised variant of the CA cluster solve (psi_seq_cluster_tb_kernel)
+// applies when the window fits its register form (nu <= 32); the correction always
+// accumulates into the C-rows that hold v.  MGRIT_COARSE_KERNEL=ca selects the
+// per-thread cp.async variant (experiments).
+static bool coarse_tb(const mgrit_ctx *c, int l) {
+  const char *e = getenv("MGRIT_COARSE_KERNEL");
+  if (e && std::string(e) == "ca") return false;
+  return c->op[l].nu <= 32;
+}
+
 static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
   CoarsePlan pl;
   const PsiOp &op = c->op[l];
@@ -711,17 +721,21 @@ static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
   }
   if (!(choose_psi(c->nx, 0, true, pc) && pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx))
     return pl;
-  // 16-CTA clusters (measured, profiles/README.md): 4 points per thread for narrow
-  // stencils, 2 for wide ones (register window), s-step depth 8 / 4.
+  // 16-CTA clusters (measured with tools/probe_cfgs.sh): the warp-
+  // specialised kernel (nu <= 32) prefers 4 points per thread at nx = 4096 (half the
+  // shared-memory window loads per output) and deeper s-steps; the cp.async variant
+  // (wider stencils) keeps 2 points per thread and depth 4 for wide stencils.
+  const bool tb = coarse_tb(c, l);
   int cl = 0, smax = 8;
   SweepCfg cc = {0, 0};
   if (c->nx == 4096) {
     cl = 16;
-    cc = op.nu <= 16 ? SweepCfg{64, 4} : SweepCfg{128, 2};
-    smax = op.nu <= 16 ? 8 : 4;
+    cc = (op.nu <= 16 || tb) ? SweepCfg{64, 4} : SweepCfg{128, 2};
+    smax = op.nu <= 16 ? 8 : (tb ? 6 : 4);
   } else if (c->nx == 1024) {
     cl = 16;
     cc = {32, 2};
+    smax = tb ? 12 : 8;
   }
   if (const char *env = getenv("MGRIT_SEQ_CLUSTER")) {
     cl = 0;
@@ -791,6 +805,9 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
     case CoarsePlan::CLUSTER:
       return run(c, 2, [&] { return launch_psi_seq_cluster(pl.cl, pl.cfg, a, c->stream); });
     case CoarsePlan::CLUSTER_CA:
+      if (const char *e = getenv("MGRIT_COARSE_DBG")) a.dbg = atoi(e);  // experiments only
+      if (coarse_tb(c, l))
+        return run(c, 2, [&] { return launch_psi_seq_cluster_tb(pl.cl, pl.cfg, pl.S, a, c->stream); });
       return run(c, 2, [&] { return launch_psi_seq_cluster_ca(pl.cl, pl.cfg, pl.S, a, c->stream); });
     case CoarsePlan::SEQ:
       return run(c, 2, [&] { return launch_psi_seq_periodic(pl.cfg, a, c->stream); });
@@ -1408,7 +1425,8 @@ int mgrit_describe(const mgrit_ctx *c, char *buf, size_t len) {
   if (c->psi_kind == MGRIT_PSI_STENCIL) {
     const CoarsePlan pl = plan_coarse(c, c->levels - 1);
     if (pl.kind == CoarsePlan::CLUSTER_CA)
-      snprintf(coarse, sizeof(coarse), "psi_seq_cluster_ca_kernel<NT=%d,P=%d,CL=%d,S=%d>",
+      snprintf(coarse, sizeof(coarse), "%s<NT=%d,P=%d,CL=%d,S=%d>",
+               coarse_tb(c, c->levels - 1) ? "psi_seq_cluster_tb_kernel" : "psi_seq_cluster_ca_kernel",
                pl.cfg.nt_threads, pl.cfg.p, pl.cl, pl.S);
     else if (pl.kind == CoarsePlan::CLUSTER)
       snprintf(coarse, sizeof(coarse), "psi_seq_cluster_kernel<NT=%d,P=%d,CL=%d>", pl.cfg.nt_threads,
