@@ -212,6 +212,12 @@ def test_coarse_correction_primitive(order, tab, cfl, nx, nt, m, nu):
     (1024, -4, 9, {}),                                    # cfg2-like: 8 x 64 x 2
     (1024, -5, 11, {"MGRIT_SEQ_CLUSTER": "16,32,2", "MGRIT_SEQ_S": "3"}),
     (1024, -5, 11, {"MGRIT_SEQ_S": "2"}),
+    (4096, -30, 32, {}),                                  # cfg4's shape (warp-specialised)
+    (4096, -30, 32, {"_nt": "2044"}),                     # ragged: N = 511 = 4*127 + 3
+    (1024, -4, 9, {"_nt": "1000"}),                       # ragged: N = 250 = 4*62 + 2
+    (1024, -7, 9, {"_nt": "20"}),                         # N = 5: shorter than the g ring
+    (4096, -14, 15, {"MGRIT_COARSE_KERNEL": "ca"}),       # per-thread cp.async variant
+    (1024, -4, 9, {"MGRIT_COARSE_KERNEL": "ca", "_nt": "1000"}),
 ])
 def test_coarse_correction_cluster(nx, o0, nu, env, monkeypatch):
     """Two-level coarse correction through the thread-block-cluster sequential solve
@@ -219,9 +225,11 @@ def test_coarse_correction_cluster(nx, o0, nu, env, monkeypatch):
     F-relaxation vs the oracle, for halo shapes on both / one side."""
     B = _cuda()
     for k, v in env.items():
-        monkeypatch.setenv(k, v)
+        if not k.startswith("_"):
+            monkeypatch.setenv(k, v)
     order, tab, cfl, m = 3, "erk3_kutta", 0.85, 4
     nt = 2048 if nx == 4096 else 1024   # coarse chain long enough for the cluster path
+    nt = int(env.get("_nt", nt))
     phi = D.make_phi(order, tab, cfl, nx)
     rng = np.random.default_rng(nu)
     coeffs = rng.uniform(-1.0, 1.0, nu)
@@ -245,7 +253,7 @@ def test_coarse_correction_cluster(nx, o0, nu, env, monkeypatch):
     assert _rel(Ug.cpu().numpy(), Uo) <= REL
 
 
-@pytest.mark.parametrize("wname", ["cfg2", "cfg3", "cfg4_literal"])
+@pytest.mark.parametrize("wname", ["cfg2", "cfg3", "cfg4", "cfg4_literal"])
 def test_coarse_solve_deterministic(wname):
     """The two-level coarse correction at full size (cluster path, 2048-4096 coarse steps)
     is bitwise reproducible: any halo / mbarrier race between the cluster's CTAs shows up

@@ -4,17 +4,15 @@
 // nvcc -arch=sm_100a -O3 -o step_bench step_bench.cu
 #include <cstdio>
 
+struct Coef { double c[32]; };
 template <int P, int NU, int NS, int MODE>
-__global__ void __launch_bounds__(512) step(long long *out, int iters, double *sink, const double *coef) {
+__global__ void __launch_bounds__(512) step(long long *out, int iters, double *sink, const __grid_constant__ Coef cf) {
   constexpr int COLS = 320;
   __shared__ double S[2][P * COLS];
   __shared__ double G[4][512];
   const int t = threadIdx.x;
   for (int q = t; q < 2 * P * COLS; q += blockDim.x) (&S[0][0])[q] = 1e-3 * q;
   for (int q = t; q < 4 * 512; q += blockDim.x) (&G[0][0])[q] = 1e-4 * q;
-  double c[NU];
-#pragma unroll
-  for (int q = 0; q < NU; ++q) c[q] = coef[q];
   __syncthreads();
   double x[P];
 #pragma unroll
@@ -35,7 +33,7 @@ __global__ void __launch_bounds__(512) step(long long *out, int iters, double *s
 #pragma unroll
     for (int q = 0; q < NU; ++q)
 #pragma unroll
-      for (int p = 0; p < P; ++p) acc[q % NS][p] = fma(c[q], w[p + q], acc[q % NS][p]);
+      for (int p = 0; p < P; ++p) acc[q % NS][p] = fma(cf.c[q], w[p + q], acc[q % NS][p]);
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       double y = acc[0][p];
@@ -57,7 +55,9 @@ __global__ void __launch_bounds__(512) step(long long *out, int iters, double *s
 }
 
 template <int P, int NU, int NS, int MODE>
-void run(int nt, long long *d, double *sink, const double *coef) {
+void run(int nt, long long *d, double *sink, const double *) {
+  Coef coef;
+  for (int q = 0; q < 32; ++q) coef.c[q] = 0.01 * q;
   long long h[16];
   const int iters = 20000;
   step<P, NU, NS, MODE><<<16, nt>>>(d, iters, sink, coef);
@@ -74,15 +74,14 @@ int main() {
   cudaMalloc(&sink, 1 << 16);
   cudaMalloc(&coef, 64 * 8);
   cudaMemset(coef, 0, 64 * 8);
-  for (int nt : {32, 64, 192, 288}) {
-    run<2, 12, 2, 0>(nt, d, sink, coef);
-    run<2, 12, 4, 0>(nt, d, sink, coef);
-    run<2, 12, 2, 1>(nt, d, sink, coef);
+  for (int nt : {64, 128, 192}) {
+    run<2, 10, 2, 0>(nt, d, sink, coef);
     run<2, 32, 2, 0>(nt, d, sink, coef);
     run<2, 32, 4, 0>(nt, d, sink, coef);
     run<4, 16, 2, 0>(nt, d, sink, coef);
-    run<4, 16, 4, 0>(nt, d, sink, coef);
-    if (nt == 32) { run<2, 12, 2, 2>(nt, d, sink, coef); run<2, 12, 4, 2>(nt, d, sink, coef); }
+    run<4, 32, 2, 0>(nt, d, sink, coef);
+    run<4, 32, 4, 0>(nt, d, sink, coef);
+    run<4, 32, 2, 1>(nt, d, sink, coef);
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
