@@ -78,16 +78,6 @@ template <int NT, int P> struct PsiSmem {
   static constexpr int TOTAL = 2 * X + 2 * G;   // ping-pong state + ping-pong g/staging
 };
 
-// --------------------------------------------------------------------------
-// cp.async (LDGSTS) 8-byte copy global -> shared, per-thread groups.
-__device__ __forceinline__ void cp_async8(void *dst_s, const void *src_g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_s)), "l"(src_g)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 // fp64 add at L2, no return (fire-and-forget RED).
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
