@@ -553,7 +553,7 @@ static cudaError_t dispatch_cfg(SweepCfg c, const SweepArgs &a, cudaStream_t s) 
   return cudaErrorInvalidConfiguration;
 }
 
-#define MG_IMPL_CFGS(X) X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8)
+#define MG_IMPL_CFGS(X) X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8) X(256, 16)
 template <class SC>
 static cudaError_t dispatch_implicit(SweepCfg c, const SweepArgs &a, cudaStream_t s) {
 #define MG_CASE(NT_, P_) \
@@ -566,6 +566,7 @@ static cudaError_t dispatch_implicit(SweepCfg c, const SweepArgs &a, cudaStream_
 bool rk_sweep_supported(int scheme, SweepCfg c) {
   if (scheme < 0 || scheme > 8) return false;
   if (scheme >= 5 && c.p == 11) return false;  // implicit: whole periodic rows only
+  if (c.nt_threads == 256 && c.p == 16) return scheme >= 5;  // implicit-only configuration
 #define MG_CASE(NT_, P_) \
   if (c.nt_threads == NT_ && c.p == P_) return true;
   MG_CFGS(MG_CASE)
