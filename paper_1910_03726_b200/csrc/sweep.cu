@@ -198,14 +198,25 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
     tma_load_1d(IN(b), row + start, (uint32_t)n1 * 8u, &bar[b]);
     if (n1 < W) tma_load_1d(IN(b) + n1, row, (uint32_t)(W - n1) * 8u, &bar[b]);
   };
-  auto issue_cmp = [&](int w) {
+  auto issue_cmp = [&](int w, double *dst) {
     int start, n1;
     window(w, start, n1);
     mbar_expect_tx(&bar[2], (uint32_t)W * 8u);
     const double *row = rowp(a.cmp, w / a.ntiles);
-    tma_load_1d(CM, row + start, (uint32_t)n1 * 8u, &bar[2]);
-    if (n1 < W) tma_load_1d(CM + n1, row, (uint32_t)(W - n1) * 8u, &bar[2]);
+    tma_load_1d(dst, row + start, (uint32_t)n1 * 8u, &bar[2]);
+    if (n1 < W) tma_load_1d(dst + n1, row, (uint32_t)(W - n1) * 8u, &bar[2]);
   };
+  // wait until at most n of this thread's bulk groups are still reading shared memory
+  auto wait_read_upto = [&](int n) {
+    if (n <= 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    else if (n == 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    else if (n == 2) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+  };
+  // check sweep (per-step writes AND comparison rows): IN(b) and CM alternate as staging,
+  // and the comparison row is loaded after the last per-step store, into the buffer the
+  // store before it used (phase-1's last step covers the load)
+  const bool chk = a.cmp.base && a.each_last >= a.each_first;
   // stage x into buf, then bulk-store the owned slice [HL, HL+T) to row[abeg..].  The
   // leading barrier is needed only when buf was read by other threads since the last
   // barrier (per-step staging after thread 0's read-completion wait); the production
@@ -237,6 +248,8 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
     const int b = it & 1;
     const uint32_t par = (uint32_t)((it >> 1) & 1);
     const int nw = w + gridDim.x;
+    const int nstage0 = nstage;
+    double *CMP = CM;                               // where the comparison row lands
     // Prefetch of item it+1 into IN(b^1) and the comparison row of item it into CM: both
     // buffers held the staged stores of item it-1, so thread 0 must first wait for those
     // bulk stores to finish reading shared memory.  Doing that at item start would hold
@@ -244,9 +257,9 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
     // the first RK step unless the item has a single step.
     auto issue_loads = [&]() {
       if (tid == 0) {
-        bulk_wait_read_all();
+        wait_read_upto(nstage - nstage0);          // only this item's own stores may still read
         if (nw < total) issue_in(nw, b ^ 1);
-        if (a.cmp.base) issue_cmp(w);
+        if (a.cmp.base && !chk) issue_cmp(w, CM);
       }
     };
     const bool early = a.nsteps1 < 2;
@@ -258,19 +271,22 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
     double x[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) x[p] = IN(b)[tid * P + p];
-    // per-step writes (F-relaxation / materialisation): alternate IN(b) and CM as staging.
-    // With comparison rows (the final check+materialise sweep) CM is taken, so every store
-    // stages in IN(b) after the previous one has finished reading it.
+    // per-step writes (F-relaxation / materialisation / check sweep): IN(b) and CM
+    // alternate as staging; a buffer is reused once the store before last has read it.
     auto each_store = [&](int i) {
-      if (tid == 0 && nstage >= 1) {
-        if (a.cmp.base) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      }
+      if (tid == 0 && nstage >= 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       double *row = const_cast<double *>(a.each.base) +
                     (a.each.off + (long long)item * a.each.stride + (long long)i * a.each_step) *
                         (long long)nx;
-      store(row, (!a.cmp.base && (nstage & 1)) ? CM : IN(b), x, abeg, T, true);
+      store(row, (nstage & 1) ? CM : IN(b), x, abeg, T, true);
       ++nstage;
+      if (chk && i == a.each_last) {
+        CMP = (nstage & 1) ? CM : IN(b);           // the buffer of the store before last
+        if (tid == 0) {
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          issue_cmp(w, CMP);
+        }
+      }
     };
     // The steps before and after the thread-0 prefetch run in separate loops so the
     // divergent issue region does not sit inside a step loop (a reconvergence point per
@@ -301,7 +317,7 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
       mbar_wait(&bar[2], (uint32_t)(it & 1));
       double d[P];
 #pragma unroll
-      for (int p = 0; p < P; ++p) d[p] = x[p] - CM[tid * P + p];
+      for (int p = 0; p < P; ++p) d[p] = x[p] - CMP[tid * P + p];
       if (a.partials) {
         double sacc = 0.0;
 #pragma unroll
