@@ -763,7 +763,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
   for (int i = 1; i <= N; ++i) {
     double *cur = smem + ((i - 1) & 1) * BL, *nxt = smem + (i & 1) * BL;
     if (k == 0) {  // start of super-step j: halo threads take x_{jS} from R[j&1]
-      if ((lhalo || rhalo) && !(a.dbg & 1)) {
+      if (lhalo || rhalo) {
         mbar_wait(&hb[j % 3], (uint32_t)((j / 3) & 1));
         const double *rj = R + (j & 1) * CS::EMAX + (lhalo ? EL + l0 : EL + (l0 - Wc));
         double h[P];
@@ -771,14 +771,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
         for (int p = 0; p < P; ++p) h[p] = rj[p];
         put(cur, h);
       }
-      if (tid == 0 && !(a.dbg & 1)) mbar_expect_tx(&hb[j % 3], hbytes);  // re-arm for j + 3
+      if (tid == 0) mbar_expect_tx(&hb[j % 3], hbytes);  // re-arm for exchange j + 3
       __syncthreads();
     }
     ++k;
-    if (!(a.dbg & 2)) {
-      prefetch(i + D - 1);
-      cp_async_wait<D - 1>();                      // this thread's rows of step i landed
-    }
+    prefetch(i + D - 1);
+    cp_async_wait<D - 1>();                        // this thread's rows of step i landed
     if (active) {
       double y[P];
       if constexpr (NU4 <= 32) {
@@ -791,14 +789,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
       for (int p = 0; p < P; ++p) x[p] = y[p] + gs[p];   // x_i = Psi x_{i-1} + g_i
       put(nxt, x);
       if (own) {
-        if ((k == S || i == N) && !(a.dbg & 1)) send(j + 1, x);  // exact own x_{(j+1)S}
+        if (k == S || i == N) send(j + 1, x);      // exact own values of x_{(j+1)S}
         const double *vs = vring + (i % D) * Wc + l0;
         double *orow = ob + (long long)i * ost;
-        if (!(a.dbg & 2)) {
 #pragma unroll
-          for (int p = 0; p < P; p += 2)           // u_i = v_i + e_i
-            *reinterpret_cast<double2 *>(orow + p) = make_double2(vs[p] + x[p], vs[p + 1] + x[p + 1]);
-        }
+        for (int p = 0; p < P; p += 2)             // u_i = v_i + e_i
+          *reinterpret_cast<double2 *>(orow + p) = make_double2(vs[p] + x[p], vs[p + 1] + x[p + 1]);
       }
     }
     if (k == S) { k = 0; ++j; }
@@ -811,7 +807,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
   }
   // the last exchange may still be landing here: wait for it, keep shared memory alive
   const int jl = k == 0 ? j : j + 1;
-  if (tid == 0 && !(a.dbg & 1)) mbar_wait(&hb[jl % 3], (uint32_t)((jl / 3) & 1));
+  if (tid == 0) mbar_wait(&hb[jl % 3], (uint32_t)((jl / 3) & 1));
   cluster.sync();
 }
 

@@ -80,7 +80,6 @@ struct CoarseArgs {
   const double *state_in;  // x_{n0} (nx), null: zero
   double *state_out;       // x_{n0+nsteps} (nx), null: not stored
   PsiOp op;
-  int dbg;                 // experiments only (MGRIT_COARSE_DBG): 1 no halo exchange, 2 no I/O
 };
 cudaError_t launch_psi_coarse(SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);
 // Periodic whole-row single-CTA variant (NT*P == nx), fixed coordinates, per-thread

@@ -809,7 +809,6 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
     case CoarsePlan::CLUSTER:
       return run(c, 2, [&] { return launch_psi_seq_cluster(pl.cl, pl.cfg, a, c->stream); });
     case CoarsePlan::CLUSTER_CA:
-      if (const char *e = getenv("MGRIT_COARSE_DBG")) a.dbg = atoi(e);  // experiments only
       if (coarse_tb(c, l))
         return run(c, 2, [&] { return launch_psi_seq_cluster_tb(pl.cl, pl.cfg, pl.S, a, c->stream); });
       return run(c, 2, [&] { return launch_psi_seq_cluster_ca(pl.cl, pl.cfg, pl.S, a, c->stream); });

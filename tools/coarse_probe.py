@@ -1,6 +1,6 @@
 """Time the two-level sequential coarse solve alone (class coarse_solve) on a workload's
 shape: ns per coarse step.  usage: python tools/coarse_probe.py cfg2 [reps]
-(experiments: MGRIT_COARSE_DBG / plan overrides are read by the library)."""
+(experiments: the plan overrides MGRIT_SEQ_CLUSTER, MGRIT_SEQ_S, MGRIT_COARSE_KERNEL)."""
 import os
 import sys
 
@@ -24,4 +24,4 @@ prof = s.profile_read()
 n, ms = prof["coarse_solve"]
 steps = w.nt // w.m
 print(f"{w.name} {s.describe().split('coarse=')[-1]} ns/step {ms / n / steps * 1e6:.1f} "
-      f"dbg={os.environ.get('MGRIT_COARSE_DBG', '0')}")
+      f"")
