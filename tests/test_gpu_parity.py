@@ -506,3 +506,25 @@ def test_final_sweep_modes_identical(label):
         assert torch.equal(o, o0), (mode, (o - o0).abs().max().item())
     if label == "cap":
         assert r0["iterations"] == w.max_iter and not r0["converged"]
+
+
+@pytest.mark.parametrize("wname", ["cfg5", "cfg3"])
+def test_fullsize_solve_deterministic(wname):
+    """Two full-size solves in the bench configuration give bit-identical histories and
+    solutions: the persistent sweeps, TMA pipelines, cluster exchanges and the reductions
+    (fixed-order partial sums) have no order- or race-dependent result."""
+    from paper_1910_03726_b200 import problem
+    _cuda()
+    w = W.ALL[wname]
+    s = problem.make_solver(w)
+    g = problem.device_guess(w)
+    s.set_guess(g)
+    outs, hists = [], []
+    for _ in range(2):
+        out = torch.empty_like(g)
+        res = s.solve(w.tol, w.max_iter, out=out)
+        hists.append(res["history"])
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert hists[0] == hists[1]
+    assert torch.equal(outs[0], outs[1])
