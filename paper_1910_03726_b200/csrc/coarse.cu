@@ -1379,14 +1379,16 @@ __global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ P
     if (k == 0) { row = rowp(a.u, item); S = origin(0); }
     else { row = a.g.base + (g0 + k) * nx; S = origin(k); }
   };
-  if (tid == 0) {
-    for (int k = 0; k < nrow; ++k) mbar_init(&bar[k], 1);
+  // lane k of warp 0 requests row k (in parallel: a serial issue loop by one thread held
+  // every warp of the CTA at the barrier below for ~15 % of the kernel's time)
+  if (tid < nrow) {
+    const int k = tid;
+    mbar_init(&bar[k], 1);
     fence_mbar_init();
-    for (int k = 0; k < nrow; ++k) {
-      const double *row;
-      int S;
-      slot_row(k, row, S);
-      if (!interp && !p2 && a.ucmp.base && k == k_ucmp) continue;  // not needed
+    const double *row;
+    int S;
+    slot_row(k, row, S);
+    if (interp || p2 || !a.ucmp.base || k != k_ucmp) {  // else: not needed
       const int S0 = S & ~1;
       const int n1 = (S0 + WB <= nx) ? WB : nx - S0;
       mbar_expect_tx(&bar[k], (uint32_t)WB * 8u);
