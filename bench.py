@@ -299,7 +299,8 @@ def run_ours(args, w):
                      "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
                      "peak_note": "FP64 pipe: 64 DFMA/clk/SM x 148 x 1.965 GHz (derived); "
                                   f"measured DFMA probe {FP64_PEAK_MEASURED} TF/s",
-                     "traffic": _profile_traffic(),
+                     # ncu DRAM bytes per launch of this kernel, captured on cfg5 only
+                     "traffic": _profile_traffic() if w.name == "cfg5" else None,
                      "avg_launch_ms": round(avg_ms, 4), "launches": n_f,
                      "flops_per_launch": flops},
         "kernel_time_share": shares,
