@@ -1539,18 +1539,33 @@ __global__ void __launch_bounds__(NT) rk_coarse_kernel(const __grid_constant__ R
   double x[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) x[p] = 0.0;
-#pragma unroll 1
-  for (int n = 1; n <= a.nsteps; ++n) {
-#pragma unroll 1
-    for (int r = 0; r < a.q; ++r) erk_step<SC, P, NT>(x, a.co, edge, phase);
+  // g_n and v_n do not depend on the chain: they are loaded one step ahead, so their
+  // latency overlaps the RK steps (one-warp rows exchange by shuffles, no barrier)
+  auto load = [&](int n, double(&gv)[P], double(&vv)[P]) {
+    if (n > a.nsteps) return;
     const double *g = a.g.base + (a.g.off + (long long)n * a.g.stride) * nx;
     const double *v = a.v.base ? a.v.base + (a.v.off + (long long)n * a.v.stride) * nx : nullptr;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      gv[p] = g[tid * P + p];
+      vv[p] = v ? v[tid * P + p] : 0.0;
+    }
+  };
+  double gn[P], vn[P];
+  load(1, gn, vn);
+#pragma unroll 1
+  for (int n = 1; n <= a.nsteps; ++n) {
+    double gc[P], vc[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) { gc[p] = gn[p]; vc[p] = vn[p]; }
+    load(n + 1, gn, vn);
+#pragma unroll 1
+    for (int r = 0; r < a.q; ++r) erk_step<SC, P, NT>(x, a.co, edge, phase);
     double *o = const_cast<double *>(a.out.base) + (a.out.off + (long long)n * a.out.stride) * nx;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      const int i = tid * P + p;
-      x[p] = x[p] + g[i];
-      o[i] = v ? v[i] + x[p] : x[p];
+      x[p] = x[p] + gc[p];
+      o[tid * P + p] = a.v.base ? vc[p] + x[p] : x[p];
     }
   }
 }

@@ -73,6 +73,13 @@ __device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<N
   constexpr int NW = NT / 32;
   constexpr int E = NL + NR;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (NW == 1) {  // one warp holds the whole window: the wrap is a shuffle too
+#pragma unroll
+    for (int k = 0; k < NL; ++k) L.v[k] = __shfl_sync(FULL, y[P - NL + k], (lane + 31) & 31);
+#pragma unroll
+    for (int k = 0; k < NR; ++k) R.v[k] = __shfl_sync(FULL, y[k], (lane + 1) & 31);
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < NL; ++k) L.v[k] = __shfl_up_sync(FULL, y[P - NL + k], 1);
 #pragma unroll
