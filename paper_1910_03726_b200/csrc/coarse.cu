@@ -1587,24 +1587,26 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
+// One CTA per row chunk: blockIdx.y strides over rows, threads over the row's points (two
+// per thread, 16-byte stores), so there is no per-element 64-bit division.
 __global__ void fill_guess_kernel(double *dst, long long row0, long long rows, int nx,
                                   uint64_t seed, int lo_kind, const double *u0) {
-  const long long total = rows * (long long)nx;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long r = t / nx;
-    const int i = (int)(t - r * nx);
+  auto value = [&](long long n, int i) {
+    if (n == 0 && u0) return u0[i];
+    const uint64_t idx = (uint64_t)n * (uint64_t)nx + (uint64_t)i;
+    const uint64_t k = splitmix64(idx + seed * 0x632BE59BD9B4E019ull) >> 11;
+    return lo_kind == 0 ? (double)((long long)k - (1ll << 52)) * 0x1p-52 : (double)k * 0x1p-53;
+  };
+  const bool pairs = (nx & 1) == 0;
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
     const long long n = row0 + r;
-    double val;
-    if (n == 0 && u0) {
-      val = u0[i];
+    double *row = dst + r * (long long)nx;
+    if (pairs) {
+      for (int i = 2 * threadIdx.x; i < nx; i += 2 * blockDim.x)
+        *reinterpret_cast<double2 *>(row + i) = make_double2(value(n, i), value(n, i + 1));
     } else {
-      const uint64_t idx = (uint64_t)n * (uint64_t)nx + (uint64_t)i;
-      const uint64_t k = splitmix64(idx + seed * 0x632BE59BD9B4E019ull) >> 11;
-      val = lo_kind == 0 ? (double)((long long)k - (1ll << 52)) * 0x1p-52
-                         : (double)k * 0x1p-53;
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) row[i] = value(n, i);
     }
-    dst[t] = val;
   }
 }
 
@@ -1723,10 +1725,8 @@ cudaError_t launch_reduce(const double *partials, long long n, double *out, cuda
 
 cudaError_t launch_fill_guess(double *dst, long long row0, long long rows, int nx, uint64_t seed,
                               int lo_kind, const double *u0, cudaStream_t s) {
-  const long long total = rows * (long long)nx;
-  if (total <= 0) return cudaSuccess;
-  long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (rows <= 0 || nx <= 0) return cudaSuccess;
+  long long blocks = rows < 148 * 32 ? rows : 148 * 32;
   fill_guess_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, row0, rows, nx, seed, lo_kind, u0);
   return cudaGetLastError();
 }
