@@ -194,6 +194,25 @@ std::vector<std::complex<long double>> poly_roots(const std::vector<long double>
 //   const = F(inf) - sum_k A_k,  F(inf) = 1 if there is no outside root, else 0.
 // Used only when the weights are well conditioned (sum of |weights| <= 64), so the
 // rounding of the sum stays within a few ulps of the product form's.
+// Power tables of one real first-order factor of the fused form (host only).
+static void fill_real_factor(RecCoef &rc, long double rho, long double alpha, bool bwd, int P,
+                             int nx) {
+  long double pk = 1.0L;
+  for (int i = 0; i <= MAXP; ++i) {
+    rc.rpow[i] = (i <= P) ? (double)pk : 0.0;
+    pk *= rho;
+  }
+  const long double rP = powl(rho, (long double)P);
+  long double pj = 1.0L;
+  for (int j = 0; j <= 32; ++j) { rc.rchunk[j] = (double)pj; pj *= rP; }
+  const long double mu = powl(rho, (long double)(32 * P));
+  long double pw = 1.0L;
+  for (int w = 0; w <= 16; ++w) { rc.rwarp[w] = (double)pw; pw *= mu; }
+  rc.closure = (double)(1.0L / (1.0L - powl(rho, (long double)nx)));
+  rc.alpha = (double)alpha;
+  rc.backward = bwd ? 1 : 0;
+}
+
 void make_sdirk_fused(const std::vector<std::complex<long double>> &roots, long double gamma,
                       int NL, int P, int nx, SdirkCoef &sd) {
   typedef std::complex<long double> C;
@@ -233,20 +252,7 @@ void make_sdirk_fused(const std::vector<std::complex<long double>> &roots, long 
   for (int k = 0; k < MAXREC; ++k) std::memset(&f.rec[k], 0, sizeof(RecCoef));
   for (int k = 0; k < MAXCREC; ++k) std::memset(&f.crec[k], 0, sizeof(CRecCoef));
   auto fill_real = [&](RecCoef &rc, long double rho, long double alpha, bool bwd) {
-    long double pk = 1.0L;
-    for (int i = 0; i <= MAXP; ++i) {
-      rc.rpow[i] = (i <= P) ? (double)pk : 0.0;
-      pk *= rho;
-    }
-    const long double rP = powl(rho, (long double)P);
-    long double pj = 1.0L;
-    for (int j = 0; j <= 32; ++j) { rc.rchunk[j] = (double)pj; pj *= rP; }
-    const long double mu = powl(rho, (long double)(32 * P));
-    long double pw = 1.0L;
-    for (int w = 0; w <= 16; ++w) { rc.rwarp[w] = (double)pw; pw *= mu; }
-    rc.closure = (double)(1.0L / (1.0L - powl(rho, (long double)nx)));
-    rc.alpha = (double)alpha;
-    rc.backward = bwd ? 1 : 0;
+    fill_real_factor(rc, rho, alpha, bwd, P, nx);
   };
   int nrf = 0, npair = 0;
   std::vector<std::pair<long double, long double>> fr;  // (rho, alpha) forward real
