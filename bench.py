@@ -278,6 +278,34 @@ def run_ours(args, w):
                "ms_per_step": round(ms_e2e, 3),
                "note": "H2D u0 (pinned), device-generated random iterate (R4), solve, "
                        "D2H of the full (nt+1) x nx solution"}
+        if world == 1:
+            # the same with the initial iterate uploaded from pinned host memory as well
+            # (the whole (nt+1) x nx guess, not just u0, crosses PCIe every step)
+            binding.fill_guess(guess, w.guess_seed, w.guess_lo, u0=u0_dev, stream=stream)
+            guess_host = torch.empty((w.nt + 1, w.nx), dtype=torch.float64).pin_memory()
+            guess_host.copy_(guess)
+            torch.cuda.synchronize()
+            th = []
+            for it in range(args.warmup + args.steps):
+                torch.cuda.synchronize()
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                guess.copy_(guess_host, non_blocking=True)
+                step()
+                out_host.copy_(out, non_blocking=True)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                if it >= args.warmup:
+                    th.append(a0.elapsed_time(a1))
+            ms_h = sum(th) / len(th)
+            e2e["host_guess"] = {"value": dof / (ms_h / 1e3), "unit": UNIT,
+                                 "h2d_bytes_per_step": int(guess_host.numel() * 8),
+                                 "d2h_bytes_per_step": int(out_host.numel() * 8),
+                                 "ms_per_step": round(ms_h, 3),
+                                 "note": "H2D of the whole initial iterate (pinned), solve, "
+                                         "D2H of the full solution"}
+            del guess_host
         del out_host
 
     line = {
