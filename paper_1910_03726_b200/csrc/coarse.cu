@@ -1534,8 +1534,19 @@ template <class SC, int NT, int P>
 __global__ void __launch_bounds__(NT) rk_coarse_kernel(const __grid_constant__ RKCoarseArgs a) {
   extern __shared__ double smem[];
   double *edge = smem;
+  double *wbuf = edge + 2 * NT * (SC::NL + SC::NR) + 2;  // SDIRK recurrences + lane tables
+  int wphase = 0;
   const int tid = threadIdx.x, nx = a.nx;
   int phase = 0;
+  if constexpr (SC::implicit) {
+    if (a.sd.fused) fused_lane_tables<SC::NL, SC::NR, NT>(a.sd, wbuf);
+    __syncthreads();
+  }
+  // one coarse step = q steps of the (explicit or SDIRK) Runge-Kutta propagator
+  auto rk = [&](double(&x)[P]) {
+    if constexpr (SC::implicit) dirk_step<SC, P, NT>(x, a.co, a.sd, edge, phase, wbuf, wphase);
+    else erk_step<SC, P, NT>(x, a.co, edge, phase);
+  };
   double x[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) x[p] = 0.0;
@@ -1560,7 +1571,7 @@ __global__ void __launch_bounds__(NT) rk_coarse_kernel(const __grid_constant__ R
     for (int p = 0; p < P; ++p) { gc[p] = gn[p]; vc[p] = vn[p]; }
     load(n + 1, gn, vn);
 #pragma unroll 1
-    for (int r = 0; r < a.q; ++r) erk_step<SC, P, NT>(x, a.co, edge, phase);
+    for (int r = 0; r < a.q; ++r) rk(x);
     double *o = const_cast<double *>(a.out.base) + (a.out.off + (long long)n * a.out.stride) * nx;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -1670,7 +1681,8 @@ cudaError_t launch_psi_sweep(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s) 
 
 template <class SC>
 static cudaError_t launch_rkc(SweepCfg c, const RKCoarseArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (2 * c.nt_threads * (SC::NL + SC::NR) + 4);
+  const size_t smem = sizeof(double) * (2 * c.nt_threads * (SC::NL + SC::NR) + 4 +
+                                        16 * (c.nt_threads / 32) + 8 * 32 + 2);
   if (c.nt_threads == 32 && c.p == 2) {
     rk_coarse_kernel<SC, 32, 2><<<1, 32, smem, s>>>(a);
   } else if (c.nt_threads == 32 && c.p == 4) {
@@ -1692,6 +1704,10 @@ cudaError_t launch_rk_coarse(int scheme, SweepCfg c, const RKCoarseArgs &a, cuda
     case 2: return launch_rkc<ERK3U3>(c, a, s);
     case 3: return launch_rkc<ERK4U4>(c, a, s);
     case 4: return launch_rkc<ERK5U5>(c, a, s);
+    case 5: return launch_rkc<SDIRK1U1>(c, a, s);
+    case 6: return launch_rkc<SDIRK2U2>(c, a, s);
+    case 7: return launch_rkc<SDIRK3U3>(c, a, s);
+    case 8: return launch_rkc<SDIRK4U4>(c, a, s);
     default: return cudaErrorInvalidValue;
   }
 }

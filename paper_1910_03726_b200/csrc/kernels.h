@@ -125,6 +125,7 @@ struct RKCoarseArgs {
   int nx, nsteps, q;
   RowMap g, v, out;
   RKCoeffs co;
+  SdirkCoef sd;      // implicit schemes: the coarse step's factored stage solve
 };
 cudaError_t launch_rk_coarse(int scheme, SweepCfg cfg, const RKCoarseArgs &a, cudaStream_t s);
 

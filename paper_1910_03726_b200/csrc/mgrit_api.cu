@@ -405,6 +405,16 @@ bool make_sdirk(const double *z, int zlo, int zn, double a, int P, int nx, Sdirk
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Whole-row configuration of the RK-form coarse solve (rk_coarse_kernel): one CTA per row.
+bool rk_coarse_cfg(int nx, SweepCfg &cfg) {
+  if (nx == 64) cfg = {32, 2};
+  else if (nx == 128) cfg = {32, 4};
+  else if (nx == 256) cfg = {32, 8};
+  else if (nx == 1024) cfg = {128, 8};
+  else return false;
+  return true;
+}
+
 // Layout of the workspace (doubles unless noted).
 struct Layout {
   size_t u0, v0, g[MGRIT_MAX_LEVELS], u2[MGRIT_MAX_LEVELS], ul[MGRIT_MAX_LEVELS];
@@ -461,6 +471,7 @@ struct mgrit_ctx {
   double redisc_cfl;
   RKCoeffs fine, coarse_rk;
   SdirkCoef sd;
+  SdirkCoef coarse_sd;              // RK-form Psi of an SDIRK scheme: the coarse stage solve
   int coarse_q;
   int zlo, zn;
   Tab tab;
@@ -789,12 +800,10 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
     a.v = v;
     a.out = out;
     a.co = c->coarse_rk;
+    a.sd = c->coarse_sd;
     SweepCfg cfg;
-    if (c->nx == 64) cfg = {32, 2};
-    else if (c->nx == 128) cfg = {32, 4};
-    else if (c->nx == 256) cfg = {32, 8};
-    else if (c->nx == 1024) cfg = {128, 8};
-    else return fail(c, MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,256,1024}");
+    if (!rk_coarse_cfg(c->nx, cfg))
+      return fail(c, MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,256,1024}");
     return run(c, 2, [&] { return launch_rk_coarse(c->scheme, cfg, a, c->stream); });
   }
   const CoarsePlan pl = plan_coarse(c, l);
@@ -1022,7 +1031,6 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
       }
     } else {
       if (levels != 2) return bad(MGRIT_EINVAL, "IDEAL/REDISC Psi only for two levels");
-      if (c->implicit) return bad(MGRIT_EUNSUPPORTED, "RK-form Psi is explicit-only");
       std::memset(&c->coarse_rk, 0, sizeof(c->coarse_rk));
       c->coarse_rk = c->fine;
       if (p.kind == MGRIT_PSI_IDEAL) {
@@ -1034,6 +1042,15 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
         c->redisc_cfl = p.redisc_cfl;
       } else {
         return bad(MGRIT_EINVAL, "unknown Psi kind");
+      }
+      if (c->implicit) {  // the coarse SDIRK step's stage solve (Phi at CFL m*c or Phi^m)
+        SweepCfg rc;
+        if (!rk_coarse_cfg(nx, rc)) return bad(MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,256,1024}");
+        std::string why;
+        const char *prod = getenv("MGRIT_SDIRK_PRODUCT");
+        if (!make_sdirk(c->coarse_rk.z, c->zlo, c->zn, c->tab.A[0][0], rc.p, nx, c->coarse_sd, why,
+                        !(prod && atoi(prod))))
+          return bad(MGRIT_EUNSUPPORTED, why.c_str());
       }
     }
   }
