@@ -94,14 +94,18 @@ size_t mgrit_workspace_bytes(int nx, int nt, int m, int levels);
  *   order       p of the upwind stencil U_p, 1..5.
  *   tableau     mgrit_tableau; explicit tableaux need ERK, implicit SDIRK.
  *   levels      2 = two-level MGRIT/Parareal; > 2 = multilevel V-cycle.
- *   psi         host array of levels-1 coarse operators Psi_2..Psi_L (copied).  IDEAL and
- *               REDISC are only valid for levels == 2.
+ *   psi         host array of levels-1 coarse operators Psi_2..Psi_L (copied).  IDEAL
+ *               (Phi^m) and REDISC (Phi at CFL redisc_cfl) are only valid for
+ *               levels == 2 and nx in {64, 128, 256, 1024}; with an SDIRK tableau the coarse
+ *               step solves its own stages (factored as for the fine step).
  *   relax       production relaxation of mgrit_solve: MGRIT_RELAX_F (Parareal) or
  *               MGRIT_RELAX_FCF.
  *   workspace_dev / workspace_bytes   caller-owned device memory, >= mgrit_workspace_bytes.
  *   stream      cudaStream_t (NULL = legacy default stream).
  * Errors: EINVAL (sizes, divisibility, tableau/order mismatch, nx too small for a stencil),
- *         ENOMEM (workspace), EUNSUPPORTED.
+ *         ENOMEM (workspace), EUNSUPPORTED (SDIRK needs whole periodic rows: nx in
+ *         {64, 128, ..., 4096}; RK-form Psi outside the sizes above; a Psi stencil wider
+ *         than MGRIT_MAX_PSI_TAPS or nx/2).
  */
 int mgrit_setup(mgrit_ctx **ctx, int nx, int nt, int m, double alpha, double cfl, int order,
                 int tableau, int levels, const mgrit_psi *psi, int relax,
