@@ -662,8 +662,7 @@ SweepArgs base_sweep(const mgrit_ctx *c) {
   a.each_first = 1;
   a.each_last = 0;  // none
   a.d_every = 1;
-  a.load_after = 1;
-  if (const char *e = getenv("MGRIT_LOAD_AFTER")) a.load_after = atoi(e);  // experiments
+  a.load_after = 1;  // issue the next item's prefetch after phase-1 step 1 (DESIGN 6.6)
   a.co = c->fine;
   a.sd = c->sd;
   a.in = a.cmp = a.endw = a.each = a.dstore = a.r2 = kNone;
