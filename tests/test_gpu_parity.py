@@ -599,3 +599,13 @@ def test_sdirk_ideal_psi_one_iteration_gpu(order, tab, cfl):
     res = s.solve(1e-10, 8, out=out)
     assert res["iterations"] == rep.iterations == 1 and res["converged"]
     assert _rel(out.cpu().numpy(), Uo) <= REL
+
+
+@pytest.mark.parametrize("cycle", ["V", "F"])
+def test_solve_sdirk_multilevel(cycle):
+    """SDIRK3+U3 (c = 4) fine propagator under a 3-level V- / F-cycle: the whole-row SDIRK
+    sweep feeds the stencil level kernels (windows of 31 and 61 taps centred on -m^l c,
+    R8); iterates, history and K vs the oracle (5 iterations)."""
+    w = W.CFG4.scaled(256, 1024, levels=3, psi_eta=None, psi_widths=(31, 61), max_iter=30)
+    res, rep = _solve_parity(w, cycle=cycle)
+    assert res["converged"]
