@@ -609,3 +609,41 @@ def test_solve_sdirk_multilevel(cycle):
     w = W.CFG4.scaled(256, 1024, levels=3, psi_eta=None, psi_widths=(31, 61), max_iter=30)
     res, rep = _solve_parity(w, cycle=cycle)
     assert res["converged"]
+
+
+# ------------------------------------------------------------------ degenerate cases
+def test_degenerate_max_iter_zero_and_exact_guess():
+    """max_iter = 0: K = 0, hist = [r0], the output is the guess.  A guess equal to the
+    sequential solution (the fixed point) has r0 at rounding level: K = 0 and the
+    output is returned unchanged."""
+    B = _cuda()
+    w = W.CFG2.scaled(256, 256)
+    phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
+    lib_psi, orc_psi = _oracle_psi(w, phi)
+    U = w.guess()
+    s = B.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels, lib_psi, w.relax)
+    g = torch.from_numpy(U).cuda()
+    s.set_guess(g)
+    out = torch.empty_like(g)
+    res = s.solve(w.tol, 0, out=out)
+    assert res["iterations"] == 0 and len(res["history"]) == 1
+    r0 = M.residual_norm(U, phi, w.dx, w.dt)
+    assert abs(res["history"][0] - r0) <= 1e-13 * r0
+    assert torch.equal(out, g)
+    S = D.sequential(phi, U[0], w.nt)
+    gs = torch.from_numpy(S).cuda()
+    s.set_guess(gs)
+    res = s.solve(w.tol, 10, out=out)
+    assert res["iterations"] == 0 and res["converged"] and res["history"][0] < 1e-13
+    assert torch.equal(out, gs)
+
+
+@pytest.mark.parametrize("nx,nt,m,levels,relax", [(256, 4, 4, 2, "FCF"), (256, 8, 4, 2, "F"),
+                                                   (256, 16, 4, 3, "FCF"), (4096, 8, 4, 2, "FCF")])
+def test_degenerate_few_intervals(nx, nt, m, levels, relax):
+    """One or two coarse intervals (nt = m, 2m) and a 3-level hierarchy whose coarsest
+    level has a single step: iterates, history and K vs the oracle (finite termination
+    makes K small)."""
+    w = W.CFG2.scaled(nx, nt, m=m, levels=levels, relax=relax, psi_widths=(9, 9), max_iter=16)
+    res, rep = _solve_parity(w)
+    assert res["converged"]
