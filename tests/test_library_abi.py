@@ -81,3 +81,30 @@ def test_product_threshold_pattern_matches_oracle(B):
     col = OP.ideal_first_column(phi, nx, 4)
     lam = ppsi.phi_eigenvalues(3, "sdirk3", 4.0, nx)
     assert ppsi.threshold(lam ** 4, 0.01) == OP.threshold_pattern(col, 0.01)
+
+
+def test_setup_rejections_host_only(B):
+    """mgrit_setup validates before touching the device: every rejected combination
+    returns its status code and leaves *ctx NULL (include/mgrit.h)."""
+    import ctypes as C
+    lib = B.lib()
+    ctx = C.c_void_p(123)
+    one = (B._Psi * 1)()
+    dummy = C.c_void_p(1 << 20)        # never dereferenced: validation fails first
+    big = 1 << 40
+    cases = [
+        (64, 64, 2, -1.0, 0.85, 1, 0, 2, one, 2, dummy, big),    # alpha <= 0
+        (64, 64, 2, 1.0, 0.0, 1, 0, 2, one, 2, dummy, big),      # cfl <= 0
+        (64, 64, 2, 1.0, 0.85, 6, 0, 2, one, 2, dummy, big),     # order outside 1..5
+        (64, 64, 2, 1.0, 0.85, 1, 0, 2, one, 1, dummy, big),     # relax C is not a solve mode
+        (64, 63, 2, 1.0, 0.85, 1, 0, 2, one, 2, dummy, big),     # nt % m != 0
+        (64, 64, 2, 1.0, 0.85, 1, 0, 2, None, 2, dummy, big),    # psi NULL
+        (4, 64, 2, 1.0, 0.85, 1, 0, 2, one, 2, dummy, big),      # nx too small for U1
+    ]
+    for args in cases:
+        st = lib.mgrit_setup(C.byref(ctx), *args, None)
+        assert st == -1, (args, st)
+        assert not ctx.value
+    # the host-only setters reject a NULL context
+    assert lib.mgrit_set_cycle(None, 0) == -1
+    assert lib.mgrit_set_final_sweep(None, 1) == -1
