@@ -404,7 +404,7 @@ cudaError_t launch_rk_sweep_tma(int scheme, SweepCfg cfg, const SweepArgs &a, cu
 // comparison row and then as the next input.  Per-warp partial sums of r^2.
 // ---------------------------------------------------------------------------
 template <class SC, int NT, int P>
-__global__ void __launch_bounds__(NT) rk_residual_tma_kernel(const __grid_constant__ SweepArgs a,
+__global__ void __launch_bounds__(NT, 4) rk_residual_tma_kernel(const __grid_constant__ SweepArgs a,
                                                              int chunk) {
   static_assert(P % 2 == 1, "contiguous windows need odd P");
   constexpr int W = NT * P;
