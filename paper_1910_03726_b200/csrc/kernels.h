@@ -25,6 +25,7 @@ struct SweepArgs {
   int nsteps2;     // phase-2 steps (applied to delta), 0 = none
   int p2_items;    // phase 2 only for items j < p2_items
   int load_after;  // TMA kernel: issue the next item's prefetch after this phase-1 step
+  int defer_v;     // TMA kernel: store v_{j+1} together with r_{j+2} (one fence per item)
   int each_first;  // write phase-1 states i = each_first..each_last into `each` rows
   int each_last;   //   (each_last < each_first: none); i = 0 is the input state
   long long each_step;  // row(j,i) = each.base + (each.off + j*each.stride + i*each_step)*nx

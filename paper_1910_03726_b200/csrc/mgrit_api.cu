@@ -663,6 +663,7 @@ SweepArgs base_sweep(const mgrit_ctx *c) {
   a.each_last = 0;  // none
   a.d_every = 1;
   a.load_after = 1;  // issue the next item's prefetch after phase-1 step 1 (DESIGN 6.6)
+  a.defer_v = 1;     // v_{j+1} stored with r_{j+2} (measured: -0.3 % per cfg5 solve)
   a.co = c->fine;
   a.sd = c->sd;
   a.in = a.cmp = a.endw = a.each = a.dstore = a.r2 = kNone;

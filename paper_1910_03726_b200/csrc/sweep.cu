@@ -312,7 +312,16 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
 #pragma unroll 1
       for (int i = la + 1; i <= a.nsteps1; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
     }
-    if (a.endw.base) store(const_cast<double *>(rowp(a.endw, item)), IN(b), x, abeg, T, false);
+    // v_{j+1}: with a phase 2 to follow, staged in place now and stored together with
+    // r_{j+2} (one fence and one barrier per item); otherwise stored right away
+    const bool defer_v = a.endw.base && a.cmp.base && a.nsteps2 > 0 && item < a.p2_items &&
+                         a.defer_v;
+    if (defer_v) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) IN(b)[tid * P + p] = x[p];
+    } else if (a.endw.base) {
+      store(const_cast<double *>(rowp(a.endw, item)), IN(b), x, abeg, T, false);
+    }
     if (a.cmp.base) {
       mbar_wait(&bar[2], (uint32_t)(it & 1));
       double d[P];
@@ -339,7 +348,19 @@ __global__ void __launch_bounds__(NT, MINB) rk_sweep_tma_kernel(const __grid_con
         for (int p = 0; p < P; ++p) x[p] = d[p];
 #pragma unroll 1
         for (int i = 1; i <= a.nsteps2; ++i) erk_step<SC, P, NT>(x, a.co, edge, phase);
-        store(const_cast<double *>(rowp(a.r2, item)), CM, x, abeg, T, false);
+        if (defer_v) {
+#pragma unroll
+          for (int p = 0; p < P; ++p) CM[tid * P + p] = x[p];
+          fence_proxy_async();
+          __syncthreads();
+          if (tid == 0) {
+            tma_store_1d(const_cast<double *>(rowp(a.endw, item)) + abeg, IN(b) + a.HL, (uint32_t)T * 8u);
+            tma_store_1d(const_cast<double *>(rowp(a.r2, item)) + abeg, CM + a.HL, (uint32_t)T * 8u);
+            bulk_commit();
+          }
+        } else {
+          store(const_cast<double *>(rowp(a.r2, item)), CM, x, abeg, T, false);
+        }
       }
     }
   }
