@@ -1550,8 +1550,10 @@ __global__ void __launch_bounds__(NT) rk_coarse_kernel(const __grid_constant__ R
   double x[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) x[p] = 0.0;
-  // g_n and v_n do not depend on the chain: they are loaded one step ahead, so their
-  // latency overlaps the RK steps (one-warp rows exchange by shuffles, no barrier)
+  // g_n and v_n do not depend on the chain: a register ring loads them D steps ahead, so
+  // their latency (~1 us) overlaps D coarse steps (one-warp rows exchange by shuffles, no
+  // barrier).  The ring is indexed at compile time: steps run in blocks of D.
+  constexpr int D = SC::implicit ? 2 : ((16 / P) < 2 ? 2 : (16 / P));
   auto load = [&](int n, double(&gv)[P], double(&vv)[P]) {
     if (n > a.nsteps) return;
     const double *g = a.g.base + (a.g.off + (long long)n * a.g.stride) * nx;
@@ -1562,21 +1564,24 @@ __global__ void __launch_bounds__(NT) rk_coarse_kernel(const __grid_constant__ R
       vv[p] = v ? v[tid * P + p] : 0.0;
     }
   };
-  double gn[P], vn[P];
-  load(1, gn, vn);
-#pragma unroll 1
-  for (int n = 1; n <= a.nsteps; ++n) {
-    double gc[P], vc[P];
+  double gr[D][P], vr[D][P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) { gc[p] = gn[p]; vc[p] = vn[p]; }
-    load(n + 1, gn, vn);
+  for (int d = 0; d < D; ++d) load(1 + d, gr[d], vr[d]);
 #pragma unroll 1
-    for (int r = 0; r < a.q; ++r) rk(x);
-    double *o = const_cast<double *>(a.out.base) + (a.out.off + (long long)n * a.out.stride) * nx;
+  for (int n0 = 1; n0 <= a.nsteps; n0 += D) {
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      x[p] = x[p] + gc[p];
-      o[tid * P + p] = a.v.base ? vc[p] + x[p] : x[p];
+    for (int d = 0; d < D; ++d) {
+      const int n = n0 + d;
+      if (n > a.nsteps) break;
+#pragma unroll 1
+      for (int r = 0; r < a.q; ++r) rk(x);
+      double *o = const_cast<double *>(a.out.base) + (a.out.off + (long long)n * a.out.stride) * nx;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        x[p] = x[p] + gr[d][p];
+        o[tid * P + p] = a.v.base ? vr[d][p] + x[p] : x[p];
+      }
+      load(n + D, gr[d], vr[d]);                  // slot d: D - 1 steps of lead
     }
   }
 }
