@@ -18,7 +18,6 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     "-I", os.path.join(ROOT, "include"),
     "--expt-relaxed-constexpr",
-] + (["-DMGRIT_TB_TRACE"] if os.environ.get("MGRIT_TB_TRACE") else []) + [
 ]
 
 

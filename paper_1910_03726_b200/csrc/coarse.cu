@@ -1004,16 +1004,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
     send(0, x);
     int j = 0, k = 0;                              // super-step j, local step k (1..S)
     int h = 0, kh = 0, slot = 0;                   // half h, step in the half, (i-1) % 12
-#ifdef MGRIT_TB_TRACE
-    __shared__ long long trc[48][5];
-    const bool tr = (tid == 0 || tid == ncomp - 1);
-#define TR(s) if (tr && i <= 48 && i >= 1) trc[i - 1][s] = clock64();
-#else
-#define TR(s)
-#endif
 #pragma unroll 1
     for (int i = 1; i <= N; ++i) {
-      TR(0)
       double *cur = smem + ((i - 1) & 1) * BL, *nxt = smem + (i & 1) * BL;
       if (k == 0) {  // start of super-step j: halo threads take x_{jS} from R[j&1]
         if (lhalo || rhalo) {
@@ -1027,7 +1019,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
         if (tid == 0) mbar_expect_tx(&hb[j % 3], hbytes);  // re-arm for exchange j + 3
         named_bar(1, ncomp);
       }
-      TR(1)
       ++k;
       if (kh == 0) {  // start of half h: hand half h-1's sets back, take half h's
         if (tid == 0 && h > 0) {
@@ -1037,7 +1028,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
         mbar_wait(&gfull[h % 3], (uint32_t)((h / 3) & 1));
         if (own && h >= 3) mbar_wait(&ofree[h % 3], (uint32_t)(((h - 3) / 3) & 1));
       }
-      TR(2)
       if (active) {
         double w[P + NU4 - 1];
         const double *s0 = cur + wcol;
@@ -1067,22 +1057,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
           if (k == S || i == N) send(j + 1, x);        // exact own values of x_{(j+1)S}
         }
       }
-      TR(3)
       if (k == S) { k = 0; ++j; }
       if (++kh == 4) { kh = 0; ++h; }
       if (++slot == TS::NS) slot = 0;
       named_bar(1, ncomp);
-      TR(4)
     }
-#ifdef MGRIT_TB_TRACE
-    if (tr && rank < 2 && N >= 48) {
-      for (int q = 0; q < 48; ++q)
-        printf("TBTRACE rank %u tid %d step %d exch %lld wait %lld comp %lld bar %lld total %lld\n", rank, tid, q + 1,
-               trc[q][1] - trc[q][0], trc[q][2] - trc[q][1], trc[q][3] - trc[q][2], trc[q][4] - trc[q][3],
-               trc[q][4] - trc[q][0]);
-    }
-#endif
-#undef TR
     if (tid == 0) mbar_arrive(&ofull[(H - 1) % 3]);  // the last half is staged
     if (own && a.state_out) {
 #pragma unroll
