@@ -99,7 +99,7 @@ struct CoarseSmem {
 };
 
 template <int NT, int P, int R>
-__global__ void __launch_bounds__(NT) psi_coarse_kernel(const __grid_constant__ CoarseArgs a) {
+__global__ void __launch_bounds__(NT, 1) psi_coarse_kernel(const __grid_constant__ CoarseArgs a) {
   using CS = CoarseSmem<NT, P, R>;
   constexpr int W = NT * P, WB = CS::WB;
   extern __shared__ __align__(128) double smem[];
@@ -677,7 +677,7 @@ __device__ __forceinline__ void cp_async16(void *dst_s, const void *src_g) {
 // (a plain load in flight must complete before bar.sync releases), so the DRAM latency
 // stays off the step chain.
 template <int NT, int P, int CL, int NU4>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128)
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 128, 1)
     psi_seq_cluster_ca_kernel(const __grid_constant__ CoarseArgs a, int S) {
   static_assert(P % 2 == 0, "P even (16-byte copies)");
   namespace cg = cooperative_groups;
@@ -1344,7 +1344,7 @@ template <int NT, int P> struct LevelSmem {
 // Output staging reuses consumed row buffers: v_{j+1} -> slot of g_1, r_{j+2} -> slot of
 // g_2, interpolated rows in place of their v2 row.
 template <int NT, int P, int NU>
-__global__ void __launch_bounds__(NT) psi_level_kernel(const __grid_constant__ PsiSweepArgs a) {
+__global__ void __launch_bounds__(NT, 1) psi_level_kernel(const __grid_constant__ PsiSweepArgs a) {
   static_assert(P % 2 == 1, "contiguous windows need odd P");
   using L = LevelSmem<NT, P>;
   constexpr int W = L::W, WB = L::WB;
