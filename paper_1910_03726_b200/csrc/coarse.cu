@@ -226,7 +226,7 @@ struct SeqSmem {
 };
 
 template <int NT, int P, int D>
-__global__ void __launch_bounds__(NT) psi_seq_periodic_kernel(const __grid_constant__ CoarseArgs a) {
+__global__ void __launch_bounds__(NT, 1) psi_seq_periodic_kernel(const __grid_constant__ CoarseArgs a) {
   using SS = SeqSmem<NT, P, D>;
   constexpr int W = NT * P;
   extern __shared__ __align__(128) double smem[];
@@ -389,7 +389,7 @@ __device__ __forceinline__ void psi_apply_pad2(const double *__restrict__ s, int
 // reads of B[(i-1)&1] before its sends of x_i: the inter-CTA chain per step is
 // halo wait -> window load -> NU4/2 FMAs -> st.async.
 template <int NT, int P, int CL, int D, int NU4>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT)
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, 1)
     psi_seq_cluster_kernel(const __grid_constant__ CoarseArgs a) {
   static_assert(P % 2 == 0, "P even (16-byte vector loads)");
   namespace cg = cooperative_groups;
@@ -1153,7 +1153,7 @@ cudaError_t launch_psi_seq_periodic(SweepCfg c, const CoarseArgs &a, cudaStream_
 
 // --------------------------------------------------------------------------
 template <int NT, int P>
-__global__ void __launch_bounds__(NT) psi_sweep_kernel(const __grid_constant__ PsiSweepArgs a) {
+__global__ void __launch_bounds__(NT, 1) psi_sweep_kernel(const __grid_constant__ PsiSweepArgs a) {
   constexpr int W = NT * P;
   extern __shared__ double smem[];
   constexpr int SP = Pad<P>::SP;
@@ -1531,7 +1531,7 @@ cudaError_t launch_psi_level_tma(SweepCfg c, const PsiSweepArgs &a, cudaStream_t
 
 // --------------------------------------------------------------------------
 template <class SC, int NT, int P>
-__global__ void __launch_bounds__(NT) rk_coarse_kernel(const __grid_constant__ RKCoarseArgs a) {
+__global__ void __launch_bounds__(NT, 1) rk_coarse_kernel(const __grid_constant__ RKCoarseArgs a) {
   extern __shared__ double smem[];
   double *edge = smem;
   double *wbuf = edge + 2 * NT * (SC::NL + SC::NR) + 2;  // SDIRK recurrences + lane tables

@@ -35,7 +35,7 @@ __device__ __forceinline__ void phi_step(double (&x)[P], const SweepArgs &a, dou
 // layout) into the other buffer pair while it computes the current one, so a whole-row
 // CTA (one per SM for the 512-thread SDIRK and ERK5 rows) never idles on a cold load.
 template <class SC, int NT, int P>
-__global__ void __launch_bounds__(NT) rk_sweep_kernel(const __grid_constant__ SweepArgs a) {
+__global__ void __launch_bounds__(NT, 1) rk_sweep_kernel(const __grid_constant__ SweepArgs a) {
   constexpr int SP = Pad<P>::SP;
   constexpr int W = NT * P;
   constexpr int NW = NT / 32;
