@@ -478,7 +478,8 @@ def test_fullsize_solve_properties(wname):
 
 
 # ------------------------------------------------------------------ final check sweep
-@pytest.mark.parametrize("label", ["tiles_vcycle", "whole_rows", "parareal", "cap"])
+@pytest.mark.parametrize("label", ["tiles_vcycle", "whole_rows", "parareal", "parareal_tiles",
+                                   "cap"])
 def test_final_sweep_modes_identical(label):
     """mgrit_set_final_sweep: the check+materialise sweep (predicted, forced every
     iteration = the misprediction path, or off) yields the same history, K and FULL
@@ -488,6 +489,8 @@ def test_final_sweep_modes_identical(label):
     w = {"tiles_vcycle": W.CFG5.scaled(4096, 1024, levels=4),
          "whole_rows": W.CFG2.scaled(1024, 1024),
          "parareal": W.CFG2.scaled(256, 1024, relax="F", max_iter=40),
+         "parareal_tiles": W.CFG5.scaled(4096, 512, levels=2, relax="F", psi_widths=(9,),
+                                         max_iter=40),
          "cap": W.CFG4_LITERAL.scaled(256, 1024, max_iter=6)}[label]
     g = torch.from_numpy(w.guess()).cuda()
     runs = {}
