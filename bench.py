@@ -117,6 +117,19 @@ def aggregate(ms_local: float, dof_local: int, dist=None):
 
 
 # ------------------------------------------------------------------ oracle sample
+def host_info():
+    """CPU model and logical core count of the host the CPU baselines ran on."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu": model, "nproc": os.cpu_count()}
+
+
 def oracle_sample(w, budget_s: float = 12.0):
     """The oracle, as it stands, on a bounded sample of the workload: full-width rows
     (nx as configured), nt reduced so one V-cycle iteration takes ~budget_s."""
@@ -138,7 +151,7 @@ def oracle_sample(w, budget_s: float = 12.0):
             break
     dt = time.perf_counter() - t0
     dof = 2 * nt_s * ws.nx * iters
-    return {"value": dof / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": dof / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_info(),
             "sample": f"{iters} oracle V-cycle iteration(s) (FCF, m={ws.m}, {levels} levels) on "
                       f"nx={ws.nx} x nt={nt_s} rows of the {w.name} recipe, numpy fp64, "
                       f"{dt:.1f} s"}
@@ -162,6 +175,7 @@ def sequential_sample(w, budget_s: float = 6.0):
     dt = time.perf_counter() - t0
     rate = steps * w.nx / dt
     return {"value": rate, "unit": UNIT, "cores": 1, "kind": "sequential time-stepping",
+            "host": host_info(),
             "sample": f"{steps} of {w.nt} steps of {w.tableau}+U{w.order} at nx={w.nx} "
                       f"(oracle Phi, numpy fp64), {dt:.1f} s",
             "full_run_s_extrapolated": round(w.nt * w.nx / rate, 1)}
