@@ -56,6 +56,33 @@ __device__ __forceinline__ void psi_apply(const double *__restrict__ s, int base
   }
 }
 
+// Same with the tap count NU known at compile time and the window starting at the
+// thread's own first point (base = threadIdx.x * P): the whole P + NU - 1 window is read
+// once with immediate offsets and the NU * P FMAs (two partial sums) run from registers.
+template <int P, int NU>
+__device__ __forceinline__ void psi_apply_own(const double *__restrict__ s, const PsiOp &op,
+                                              double (&out)[P]) {
+  constexpr int SP = Pad<P>::SP;
+  const double *s0 = s + threadIdx.x * SP;
+  double w[P + NU - 1];
+#pragma unroll
+  for (int r = 0; r < P + NU - 1; ++r) w[r] = s0[(r / P) * SP + r % P];
+  double a0[P], a1[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) { a0[p] = 0.0; a1[p] = 0.0; }
+#pragma unroll
+  for (int q = 0; q < NU; ++q) {
+    const double c = op.psi[q];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (q & 1) a1[p] = fma(c, w[p + q], a1[p]);
+      else a0[p] = fma(c, w[p + q], a0[p]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) out[p] = a0[p] + a1[p];
+}
+
 // Write the state into s (padded layout) plus the periodic tail: logical
 // s[W + e] = s[e mod W] for e < PSI_EXT.
 template <int NT, int P>
@@ -98,7 +125,7 @@ struct CoarseSmem {
   static constexpr int TOTAL = 2 * X + R * WB + 3 * WB + 2 * R + 8;
 };
 
-template <int NT, int P, int R>
+template <int NT, int P, int R, int NU>
 __global__ void __launch_bounds__(NT, 1) psi_coarse_kernel(const __grid_constant__ CoarseArgs a) {
   using CS = CoarseSmem<NT, P, R>;
   constexpr int W = NT * P, WB = CS::WB;
@@ -150,7 +177,8 @@ __global__ void __launch_bounds__(NT, 1) psi_coarse_kernel(const __grid_constant
     const double *sprev = SX((i - 1) & 1);
     double *scur = SX(i & 1);
     double y[P];
-    psi_apply<P>(sprev, threadIdx.x * P, a.op, y);
+    if constexpr (NU > 0) psi_apply_own<P, NU>(sprev, a.op, y);
+    else psi_apply<P>(sprev, threadIdx.x * P, a.op, y);
     psi_put<NT, P>(scur, y);
     if (tid == 0) {
       fetch(i + R - 1);  // slot (i-1) % R was consumed before the last barrier
@@ -1630,26 +1658,38 @@ __global__ void fill_guess_kernel(double *dst, long long row0, long long rows, i
 #define MG_PSI_CFGS(X) \
   X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8)
 
-template <int NT, int P, int R>
+template <int NT, int P, int R, int NU>
 static cudaError_t launch_coarse_ring(const CoarseArgs &a, cudaStream_t s) {
   const size_t smem = sizeof(double) * CoarseSmem<NT, P, R>::TOTAL;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(psi_coarse_kernel<NT, P, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(psi_coarse_kernel<NT, P, R, NU>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  psi_coarse_kernel<NT, P, R><<<a.ntiles, NT, smem, s>>>(a);
+  psi_coarse_kernel<NT, P, R, NU><<<a.ntiles, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-// ring depth: 8 slots where shared memory allows, else 4
+// ring depth: 8 slots where shared memory allows, else 4.  The V-cycle coarsest level of
+// the cfg5 hierarchy (256 x 8 tiles) gets compile-time tap counts (nu_l = 9 .. 25).
 template <int NT, int P>
 static cudaError_t launch_coarse_one(const CoarseArgs &a, cudaStream_t s) {
-  if constexpr (sizeof(double) * CoarseSmem<NT, P, 8>::TOTAL <= 220 * 1024)
-    return launch_coarse_ring<NT, P, 8>(a, s);
-  else
-    return launch_coarse_ring<NT, P, 4>(a, s);
+  if constexpr (sizeof(double) * CoarseSmem<NT, P, 8>::TOTAL <= 220 * 1024) {
+    if constexpr (NT == 256 && P == 8) {
+      switch (a.op.nu) {
+        case 9: return launch_coarse_ring<NT, P, 8, 9>(a, s);
+        case 13: return launch_coarse_ring<NT, P, 8, 13>(a, s);
+        case 17: return launch_coarse_ring<NT, P, 8, 17>(a, s);
+        case 21: return launch_coarse_ring<NT, P, 8, 21>(a, s);
+        case 25: return launch_coarse_ring<NT, P, 8, 25>(a, s);
+        default: break;
+      }
+    }
+    return launch_coarse_ring<NT, P, 8, 0>(a, s);
+  } else {
+    return launch_coarse_ring<NT, P, 4, 0>(a, s);
+  }
 }
 
 template <int NT, int P>

@@ -12,5 +12,6 @@ prof() {
   python tools/ncu_source_top.py $OUT/$name.ncu-rep 30 > $OUT/${name}_source_top.txt
   rm -f $OUT/$name.ncu-rep
 }
-prof interp2_r01c psi_level_kernel 7
-prof check_r01c rk_sweep_tma_kernel 6
+# prof interp2_r01c psi_level_kernel 7
+# prof check_r01c rk_sweep_tma_kernel 6
+prof coarsest_r01c psi_coarse_kernel 0
