@@ -377,10 +377,12 @@ def test_solve_fcycle(nx, nt, levels, m):
     assert res["converged"]
 
 
-def test_solve_cfg5_fullwidth_vcycle():
+@pytest.mark.parametrize("nt,levels", [(1024, 4), (4096, 6)])
+def test_solve_cfg5_fullwidth_vcycle(nt, levels):
     """cfg5 at its full width nx = 16384 (the bench launch configurations: halo tiles for
-    the fine sweep, tiled level sweeps and tiled coarsest solve), nt reduced to 1024."""
-    w = W.CFG5.scaled(16384, 1024, levels=4)
+    the fine sweep, tiled level sweeps and the tiled coarsest solve in its compile-time
+    tap-count instantiations, nu = 17 and, with cfg5's six levels, nu = 25), nt reduced."""
+    w = W.CFG5.scaled(16384, nt, levels=levels)
     res, rep = _solve_parity(w, check_states=True)
     assert res["converged"]
 

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-1 final refresh: bench lines of every configuration, the cfg5 launch list, ncu
 # summaries of the fine sweep (cfg5), the SDIRK sweep (cfg4), the warp-specialised cluster
-# coarse solve (cfg4) and the level-2 sweep (cfg5).  Summaries are computed on the box and
+# coarse solve (cfg4), the level-2 sweep and the coarsest solve (cfg5).  Summaries are computed on the box and
 # the .ncu-rep files dropped (gpurun copies back at most 64 MiB).
 set -u
 OUT=gpurun_out
@@ -33,3 +33,4 @@ prof fine_r01c rk_sweep_tma_kernel 1 $CMD
 prof level2_r01c psi_level_kernel 0 $CMD
 prof sdirk_r01c rk_sweep_kernel 2 $C4
 prof coarse_tb_r01c psi_seq_cluster_tb_kernel 1 $C4
+prof coarsest_r01c psi_coarse_kernel 0 $CMD
