@@ -108,3 +108,23 @@ def test_setup_rejections_host_only(B):
     # the host-only setters reject a NULL context
     assert lib.mgrit_set_cycle(None, 0) == -1
     assert lib.mgrit_set_final_sweep(None, 1) == -1
+
+
+def test_missing_library_fails_loudly(B, monkeypatch, tmp_path):
+    """No CPU fallback: with the shared library absent the binding raises instead of
+    computing anything (the product path never routes through the oracle)."""
+    monkeypatch.setattr(B, "_lib", None)
+    monkeypatch.setattr(B, "LIB_PATH", str(tmp_path / "libmgrit.so"))
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        B.lib()
+    with pytest.raises(ImportError):
+        B.scheme_coefficients(1, "erk1", 0.85)
+
+
+def test_product_does_not_import_the_oracle():
+    """The oracle is test infrastructure: no module of the product package imports it."""
+    pkg = os.path.join(ROOT, "paper_1910_03726_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert not re.search(r"^\s*(from|import)\s+oracle\b", src, re.M), fn
