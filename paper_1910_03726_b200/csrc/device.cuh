@@ -23,6 +23,7 @@ struct RKCoeffs {
   double A[MAXS][MAXS];    // Butcher A
   double b[MAXS];          // Butcher b
   double mdiag[MAXS];      // SDIRK: a_ii (stage matrix I - a_ii Z)
+  double bz[MAXZ];         // ERK: b_{S-1} z_d, the last stage folded into the update
 };
 
 // Compile-time structure of a scheme: stages, stencil reach, zero pattern.
@@ -129,6 +130,28 @@ __device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
   }
 }
 
+// k = base + Z y (the stencil accumulated onto `base`, d ascending).
+template <int NL, int NR, int P, int NT>
+__device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
+                                        const double *__restrict__ z, double *edge,
+                                        int &phase, const double (&base)[P]) {
+  Arr<NL> L;
+  Arr<NR> R;
+  exchange<NL, NR, P, NT>(y, L, R, edge, phase);
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    double acc = base[p];
+#pragma unroll
+    for (int d = -NL; d <= NR; ++d) {
+      const int q = p + d;
+      const double v = (q < 0) ? L.v[(NL + q) < 0 ? 0 : (NL + q)]
+                               : (q >= P ? R.v[(q - P) < NR ? (q - P) : 0] : y[q < P ? q : 0]);
+      acc = fma(z[d + NL], v, acc);
+    }
+    k[p] = acc;
+  }
+}
+
 // One explicit RK step in stage form (App. A):
 //   k_i = Z(x + sum_{l<i} a_il k_l),  x <- x + sum_i b_i k_i.
 // Partial stage sums are accumulated as soon as k_l is known (same summation
@@ -147,6 +170,16 @@ __device__ __forceinline__ void erk_step(double (&x)[P], const RKCoeffs &c, doub
   }
 #pragma unroll
   for (int i = 0; i < S; ++i) {
+    if (i == S - 1 && SC::b_nz(i)) {
+      // last stage: k_{S-1} feeds only the update, so x += b_{S-1} Z y is applied as
+      // x += (b_{S-1} Z) y — NL + NR + 1 FMAs instead of a DMUL, NL + NR FMAs and one more
+      // FMA per point (same result up to rounding)
+      double t[P];
+      apply_Z<SC::NL, SC::NR, P, NT>(acc[i], t, c.bz, edge, phase, out);
+#pragma unroll
+      for (int p = 0; p < P; ++p) out[p] = t[p];
+      continue;
+    }
     double k[P];
     apply_Z<SC::NL, SC::NR, P, NT>(acc[i], k, c.z, edge, phase);
 #pragma unroll

@@ -122,6 +122,11 @@ void make_z(int order, double cfl, double *z, int *zlo, int *zn) {
   *zn = u.dmax - u.dmin + 1;
 }
 
+// b_{S-1} z_d for the explicit step's folded last stage (device.cuh erk_step)
+static void fold_last_stage(RKCoeffs &co, int s) {
+  for (int d = 0; d < MAXZ; ++d) co.bz[d] = (s > 0) ? co.b[s - 1] * co.z[d] : 0.0;
+}
+
 int scheme_id(int tableau) {
   switch (tableau) {
     case MGRIT_TAB_ERK1: return 0;
@@ -999,6 +1004,7 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
     c->fine.mdiag[i] = c->tab.A[i][i];
     for (int j = 0; j < MAXS; ++j) c->fine.A[i][j] = c->tab.A[i][j];
   }
+  fold_last_stage(c->fine, c->tab.s);
   std::memset(&c->sd, 0, sizeof(c->sd));
   if (c->implicit) {
     FineCfg f;
@@ -1038,6 +1044,7 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
       } else if (p.kind == MGRIT_PSI_REDISC) {
         int zlo, zn;
         make_z(order, p.redisc_cfl, c->coarse_rk.z, &zlo, &zn);
+        fold_last_stage(c->coarse_rk, c->tab.s);
         c->coarse_q = 1;
         c->redisc_cfl = p.redisc_cfl;
       } else {
