@@ -24,6 +24,12 @@ struct RKCoeffs {
   double b[MAXS];          // Butcher b
   double mdiag[MAXS];      // SDIRK: a_ii (stage matrix I - a_ii Z)
   double bz[MAXZ];         // ERK: b_{S-1} z_d, the last stage folded into the update
+  // 3-stage ERK whose update needs no stage-1 value (SSP-RK3): Shu-Osher form
+  //   y1 = x + a10 Z x,  y2 = so[0] x + so[1] y1 + a21 Z y1,  x' = so[2] x + so[3] y2 + b2 Z y2
+  // with soz[0] = a10 z, soz[1] = a21 z, soz[2] = b2 z (so3 = 0: stage form)
+  int so3;
+  double so[4];
+  double soz[3][MAXZ];
 };
 
 // Compile-time structure of a scheme: stages, stencil reach, zero pattern.
@@ -160,6 +166,19 @@ template <class SC, int P, int NT>
 __device__ __forceinline__ void erk_step(double (&x)[P], const RKCoeffs &c, double *edge,
                                          int &phase) {
   constexpr int S = SC::S;
+  if constexpr (S == 3) {
+    if (c.so3) {  // Shu-Osher form: 3ν + 4 instead of 3ν + 5 FP64 instructions per point
+      double y[P], t[P], u[P];
+      apply_Z<SC::NL, SC::NR, P, NT>(x, y, c.soz[0], edge, phase, x);
+#pragma unroll
+      for (int p = 0; p < P; ++p) t[p] = fma(c.so[1], y[p], c.so[0] * x[p]);
+      apply_Z<SC::NL, SC::NR, P, NT>(y, u, c.soz[1], edge, phase, t);
+#pragma unroll
+      for (int p = 0; p < P; ++p) t[p] = fma(c.so[3], u[p], c.so[2] * x[p]);
+      apply_Z<SC::NL, SC::NR, P, NT>(u, x, c.soz[2], edge, phase, t);
+      return;
+    }
+  }
   double acc[S][P];
   double out[P];
 #pragma unroll
