@@ -352,6 +352,10 @@ def run_ours(args, w):
                      "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
                      "peak_note": "FP64 pipe: 64 DFMA/clk/SM x 148 x 1.965 GHz (derived); "
                                   f"measured DFMA probe {FP64_PEAK_MEASURED} TF/s",
+                     "flops_note": f"{FLOPS_PER_POINT_STEP[w.tableau]:g} algorithmic flops per "
+                                   "point-step (stage form, SURVEY 8d); the kernel issues fewer "
+                                   "FP64 instructions (folded last stage, Shu-Osher SSP-RK3: "
+                                   "DESIGN.md 6.1)",
                      # ncu DRAM bytes per launch of this kernel, captured on cfg5 only
                      "traffic": _profile_traffic() if w.name == "cfg5" else None,
                      "avg_launch_ms": round(avg_ms, 4), "launches": n_f,
