@@ -24,9 +24,10 @@ struct RKCoeffs {
   double b[MAXS];          // Butcher b
   double mdiag[MAXS];      // SDIRK: a_ii (stage matrix I - a_ii Z)
   double bz[MAXZ];         // ERK: b_{S-1} z_d, the last stage folded into the update
-  // 3-stage ERK whose update needs no stage-1 value (SSP-RK3): Shu-Osher form
-  //   y1 = x + a10 Z x,  y2 = so[0] x + so[1] y1 + a21 Z y1,  x' = so[2] x + so[3] y2 + b2 Z y2
-  // with soz[0] = a10 z, soz[1] = a21 z, soz[2] = b2 z (so3 = 0: stage form)
+  // 3-stage ERK with a20 = a21 and b0 = b1 (SSP-RK3): since k0 = Zx, k1 = Zy1,
+  //   y1 = x + a10 Z x,  y2 = x + a21 Z (x + y1),  x' = so[0] x + so[1] y2 + b2 Z y2
+  // (so[1] = b0 / a21, so[0] = 1 - so[1]); soz[0] = a10 z, soz[1] = a21 z, soz[2] = b2 z
+  // (so3 = 0: stage form)
   int so3;
   double so[4];
   double soz[3][MAXZ];
@@ -168,14 +169,14 @@ __device__ __forceinline__ void erk_step(double (&x)[P], const RKCoeffs &c, doub
                                          int &phase) {
   constexpr int S = SC::S;
   if constexpr (S == 3) {
-    if (c.so3) {  // Shu-Osher form: 3ν + 4 instead of 3ν + 5 FP64 instructions per point
+    if (c.so3) {  // 3ν + 3 instead of 3ν + 5 FP64 instructions per point (ν taps)
       double y[P], t[P], u[P];
       apply_Z<SC::NL, SC::NR, P, NT>(x, y, c.soz[0], edge, phase, x);
 #pragma unroll
-      for (int p = 0; p < P; ++p) t[p] = fma(c.so[1], y[p], c.so[0] * x[p]);
-      apply_Z<SC::NL, SC::NR, P, NT>(y, u, c.soz[1], edge, phase, t);
+      for (int p = 0; p < P; ++p) y[p] += x[p];
+      apply_Z<SC::NL, SC::NR, P, NT>(y, u, c.soz[1], edge, phase, x);
 #pragma unroll
-      for (int p = 0; p < P; ++p) t[p] = fma(c.so[3], u[p], c.so[2] * x[p]);
+      for (int p = 0; p < P; ++p) t[p] = fma(c.so[1], u[p], c.so[0] * x[p]);
       apply_Z<SC::NL, SC::NR, P, NT>(u, x, c.soz[2], edge, phase, t);
       return;
     }

@@ -122,25 +122,19 @@ void make_z(int order, double cfl, double *z, int *zlo, int *zn) {
   *zn = u.dmax - u.dmin + 1;
 }
 
-// b_{S-1} z_d for the explicit step's folded last stage, and the Shu-Osher form of a
-// 3-stage ERK whose update has no y1 term (device.cuh erk_step).  With
-// k0 = (y1 - x)/a10, k1 = (y2 - s0 x - s1 y1)/a21 (s0 = 1 - a20/a10, s1 = a20/a10):
-// x' = x + b0 k0 + b1 k1 + b2 Z y2 = cx x + c1 y1 + c2 y2 + b2 Z y2.  Used only when c1 is
-// exactly 0 (SSP-RK3: s = 3/4, 1/4; cx = 1/3, c2 = 2/3).
+// b_{S-1} z_d for the explicit step's folded last stage, and the Shu-Osher-type form of
+// a 3-stage ERK with a20 = a21 and b0 = b1 (SSP-RK3: 1/4, 1/4 and 1/6, 1/6; device.cuh
+// erk_step): y2 = x + a21 Z(x + y1) and x' = x + b0 Z(x + y1) + b2 Z y2
+// = (1 - b0/a21) x + (b0/a21) y2 + b2 Z y2.
 static void fold_last_stage(RKCoeffs &co, int s) {
   for (int d = 0; d < MAXZ; ++d) co.bz[d] = (s > 0) ? co.b[s - 1] * co.z[d] : 0.0;
   co.so3 = 0;
   if (s != 3 || co.mdiag[0] != 0.0) return;
   const double a10 = co.A[1][0], a20 = co.A[2][0], a21 = co.A[2][1];
   const double b0 = co.b[0], b1 = co.b[1], b2 = co.b[2];
-  if (a10 == 0.0 || a21 == 0.0) return;
-  const double s1 = a20 / a10, s0 = 1.0 - s1;
-  const double c1 = b0 / a10 - (b1 / a21) * s1;
-  if (c1 != 0.0) return;
-  co.so[0] = s0;
-  co.so[1] = s1;
-  co.so[2] = 1.0 - b0 / a10 - (b1 / a21) * s0;
-  co.so[3] = b1 / a21;
+  if (a21 == 0.0 || a20 != a21 || b0 != b1) return;
+  co.so[1] = b0 / a21;
+  co.so[0] = 1.0 - co.so[1];
   for (int d = 0; d < MAXZ; ++d) {
     co.soz[0][d] = a10 * co.z[d];
     co.soz[1][d] = a21 * co.z[d];
