@@ -162,7 +162,7 @@ __device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
 // One explicit RK step in stage form (App. A):
 //   k_i = Z(x + sum_{l<i} a_il k_l),  x <- x + sum_i b_i k_i.
 // Partial stage sums are accumulated as soon as k_l is known (l ascending, as in the
-// oracle); the last stage is folded into the update and SSP-RK3 runs in Shu-Osher form
+// oracle); the last stage is folded into the update and SSP-RK3 uses Z(x + y1) (3 stencils)
 // (RKCoeffs::bz / so3), so results match the oracle to rounding.
 template <class SC, int P, int NT>
 __device__ __forceinline__ void erk_step(double (&x)[P], const RKCoeffs &c, double *edge,
