@@ -153,13 +153,16 @@ class SolveReport:
 
 def solve(U: np.ndarray, phis: Sequence[Callable], m: int, dx: float, dt: float,
           relax: str = "FCF", tol: float = 1e-10, max_iter: int = 64,
-          keep_states: bool = False, cycle: str = "V") -> SolveReport:
+          keep_states: bool = False, cycle: str = "V",
+          on_iter: Optional[Callable[[int, np.ndarray], None]] = None) -> SolveReport:
     """MGRIT / Parareal iteration on the fine space-time iterate U (in place).
 
     U[0] holds u0 and is never modified.  The residual is
     measured on the iterate after k complete iterations; K = first k with
     ||r^(k)|| < tol (R2).  No early stop on growth (R15), except
-    for non-finite values.  cycle: "V" or "F" (R19)."""
+    for non-finite values.  cycle: "V" or "F" (R19).  on_iter(k, U), if
+    given, is called after iteration k with the iterate (read-only observation, e.g. to
+    sample rows for a golden file; it does not take part in the arithmetic)."""
     phi = phis[0]
     hist = [residual_norm(U, phi, dx, dt)]
     states = []
@@ -173,6 +176,8 @@ def solve(U: np.ndarray, phis: Sequence[Callable], m: int, dx: float, dt: float,
         hist.append(r)
         if keep_states:
             states.append(U[::m].copy())
+        if on_iter is not None:
+            on_iter(k, U)
         if not np.isfinite(r):
             nonfinite = True
             break

@@ -102,20 +102,81 @@ SCHEMES = [(1, "erk1", 0.85), (2, "erk2", 0.425), (3, "erk3_ssp", 0.85), (3, "er
            (3, "sdirk3", 4.0), (4, "sdirk4", 4.0)]
 
 
+# sigma_p(theta) = dx * (symbol of U_p) written out from the displayed stencils:
+# U_p u'(x_i) = (1/(den dx)) sum_d w_d u_{i+d}  ->  sum_d w_d e^{i theta d} / den.
+def _E(th, d):
+    return np.exp(1j * th * d)
+
+
+SIGMA = {   # E(t, d) = e^{i t d}; numpy by default, mpmath in the high-precision pins
+    1: lambda t, E=_E: (E(t, 0) - E(t, -1)),                                           # (U1)
+    2: lambda t, E=_E: (3 * E(t, 0) - 4 * E(t, -1) + E(t, -2)) / 2,                    # (U2)
+    3: lambda t, E=_E: (2 * E(t, 1) + 3 * E(t, 0) - 6 * E(t, -1) + E(t, -2)) / 6,      # (U3)
+    4: lambda t, E=_E: (3 * E(t, 1) + 10 * E(t, 0) - 18 * E(t, -1) + 6 * E(t, -2)
+                        - E(t, -3)) / 12,                                              # (U4)
+    5: lambda t, E=_E: (-3 * E(t, 2) + 30 * E(t, 1) + 20 * E(t, 0) - 60 * E(t, -1)
+                        + 15 * E(t, -2) - 2 * E(t, -3)) / 60,                          # (U5)
+}
+
+
+def _R_linear_algebra(name, z):
+    """R(z) = 1 + z b^T (I - z A)^{-1} 1 by a dense linear solve per z (Butcher Lemma
+    351A, the route P:142-152 cites) -- not the oracle's stage recursion."""
+    tab = D.tableau(name)
+    A, b = np.array(tab.A), np.array(tab.b)
+    s = len(b)
+    return np.array([1 + zz * b @ np.linalg.solve(np.eye(s) - zz * A, np.ones(s)) for zz in z])
+
+
 @pytest.mark.parametrize("order,tab,c", SCHEMES)
 def test_phi_on_fourier_modes(order, tab, c):
-    """Phi = R(dt L) on every grid mode (Lemma 1, Corollary 1 P:154):
-    the stage-form step applied to cos/sin(theta_k i) equals Re/Im of
-    R(lambda_k) e^{i theta_k i}, with lambda_k the Fourier symbol of Z."""
+    """Phi = R(dt L) on every grid mode (Lemma 1, Corollary 1 P:154): the
+    oracle's stage-form step applied to cos/sin(theta_k i) equals Re/Im of
+    R(-c sigma_p(theta_k)) e^{i theta_k i}, where sigma_p is the symbol of the paper's U_p
+    display (written out above; the dt L = -c sigma_p sign of P:82) and R
+    is computed by the linear-algebra formula.  Nothing here comes from the oracle's z_d,
+    so a wrong sign or scale of z_coefficients fails it for every p."""
     nx = 64
     phi = D.make_phi(order, tab, c, nx)
     i = np.arange(nx)
     for k in [0, 1, 5, nx // 2 - 1, nx // 2]:
         th = 2 * np.pi * k / nx
-        lam = D.stability_function(D.tableau(tab), np.array([D.stencil_symbol(phi.z, th)]))[0]
+        lam = _R_linear_algebra(tab, np.array([-c * SIGMA[order](th)]))[0]
         ref = lam * np.exp(1j * th * i)
         np.testing.assert_allclose(phi(np.cos(th * i)), ref.real, atol=2e-14)
         np.testing.assert_allclose(phi(np.sin(th * i)), ref.imag, atol=2e-14)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("c", [0.85, 4.0])
+def test_z_coefficients_moments(p, c):
+    """Z = dt L with L ~ -alpha d/dx at CFL c = alpha dt/dx: on polynomials
+    of degree q <= p, sum_d z_d d^q = -c [q == 1] (Z maps u = i to -c dx/dx = -c: transport
+    by -c cells per step), and Z is not exact at q = p + 1."""
+    z = D.z_coefficients(p, c)
+    for q in range(p + 1):
+        mom = sum(zd * float(d) ** q for d, zd in z.items())
+        assert abs(mom - (-c if q == 1 else 0.0)) <= 1e-13 * c * 4 ** q, (p, q, mom)
+    assert abs(sum(zd * float(d) ** (p + 1) for d, zd in z.items())) > 1e-3 * c
+
+
+def test_phi_modified_equation_order():
+    """Phi approximates the exact transport e^{-i c theta} (u_t + u_x = 0 over one step)
+    with local error O(theta^{p+1}) for ERKp+Up: halving theta divides the
+    error by about 2^{p+1}."""
+    for order, tab in [(1, "erk1"), (2, "erk2"), (3, "erk3_ssp"), (4, "erk4"), (5, "erk5"),
+                       (3, "sdirk3")]:
+        nx = 4096
+        phi = D.make_phi(order, tab, 0.5, nx)
+        i = np.arange(nx)
+        errs = []
+        for k in (32, 16):
+            th = 2 * np.pi * k / nx
+            ex = np.exp(1j * th * (i - 0.5))
+            got = phi(np.cos(th * i)) + 1j * phi(np.sin(th * i))
+            errs.append(np.max(np.abs(got - ex)))
+        ratio = errs[0] / errs[1]
+        assert 2 ** (order + 1) * 0.8 <= ratio <= 2 ** (order + 1) * 1.25, (tab, ratio)
 
 
 def test_erk1_u1_cfl1_exact_shift():
@@ -377,6 +438,67 @@ def test_lsq_solution_real(tab, p, m, nu):
     assert fit.imag_residue < 1e-8 and fit.accepted
     mu = D.stencil_symbol(fit.stencil, 2 * np.pi * np.arange(nx) / nx)
     assert np.max(np.abs(mu)) < 1 + 1e-6
+
+
+@pytest.mark.parametrize("tab,p,m,offs", [("erk3_ssp", 3, 4, [-4, -3, -2]),
+                                          ("erk1", 1, 2, [-2, -1]),
+                                          ("sdirk3", 3, 4, [-6, -5, -4, -3])])
+def test_weighted_lsq_normal_equations(tab, p, m, offs):
+    """The weighted LSQ of eq. (LSQ_1D_problem) with w(z) = 1/(1 - z + eps)^2,
+    eps = 1e-6, evaluated at |lambda_k| of the operator being coarsened, on a
+    tiny grid (nx = 8) solved a second way: the real normal equations (Lemma 3's proof,
+    P:380-390) G psi = h with G_de = sum_k w_k cos(theta_k (e - d)) and
+    h_d = sum_k w_k Re(e^{-i theta_k d} lambda_k^m), where lambda_k = R(-c sigma_p(theta_k))
+    from the paper's stencil display and the linear-algebra R (no oracle function).  The
+    oracle's fit (oracle.psi.weights + lsq_psi) must agree, and must differ from the W = I
+    truncation (Remark 1), so a wrong weight function or a weight on the wrong spectrum
+    fails here."""
+    mp = pytest.importorskip("mpmath").mp
+    mp.dps = 50        # w_0 ~ 1e12: the normal equations need far more than fp64
+    nx = 8
+    c = mp.mpf(4) if tab.startswith("sdirk") else mp.mpf("0.85")
+    tb = D.tableau(tab)
+    A = mp.matrix([[mp.mpf(x) for x in row] for row in tb.A])
+    b = [mp.mpf(x) for x in tb.b]
+    s_ = len(b)
+    E = lambda t, d: mp.expj(t * d)       # noqa: E731
+    th = [2 * mp.pi * k / nx for k in range(nx)]
+    lam = []
+    for t in th:
+        z = -c * SIGMA[p](t, E)
+        x = mp.lu_solve(mp.eye(s_) - z * A, mp.matrix([1] * s_))
+        lam.append(1 + z * sum(b[i] * x[i] for i in range(s_)))
+    w = [1 / (1 - abs(lk) + mp.mpf("1e-6")) ** 2 for lk in lam]
+    G = mp.matrix([[sum(w[k] * mp.cos(th[k] * (e - d)) for k in range(nx)) for e in offs]
+                   for d in offs])
+    h = mp.matrix([sum(w[k] * mp.re(mp.expj(-th[k] * d) * lam[k] ** m) for k in range(nx))
+                   for d in offs])
+    psi_ne = np.array([float(v) for v in mp.lu_solve(G, h)])
+    phi = D.make_phi(p, tab, float(c), nx)
+    col = P.ideal_first_column(phi, nx, m)
+    lam_orc = P.eigenvalues(phi(np.eye(nx)[0]))
+    fit = P.lsq_psi(col, lam_orc, offs)
+    np.testing.assert_allclose(fit.coeffs, psi_ne, rtol=1e-9, atol=1e-12)
+    unit = P.lsq_psi(col, lam_orc, offs, w=np.ones(nx)).coeffs
+    assert np.max(np.abs(unit - psi_ne)) > 1e-4
+
+
+def test_operator_complexity_paper_values():
+    """eq. (OC) P:399-403 and the values P:403 states: nnz(Psi) = nnz(Phi) gives 1 + 1/m
+    for two levels and tends to (is bounded by) m/(m-1) with L; ideal operators
+    (nnz growing by m per level) give exactly L."""
+    for m in (2, 4, 8):
+        assert M.operator_complexity([7, 7], m) == pytest.approx(1 + 1 / m, rel=1e-15)
+        oc = [M.operator_complexity([9] * L, m) for L in range(2, 60)]
+        assert all(a <= b for a, b in zip(oc, oc[1:])) and oc[0] < oc[5]
+        assert all(v <= m / (m - 1) * (1 + 4e-16) for v in oc) and oc[10] < m / (m - 1)
+        assert oc[-1] == pytest.approx(m / (m - 1), rel=1e-12)
+        for L in (2, 3, 5):
+            assert M.operator_complexity([4 * m ** l for l in range(L)], m) == pytest.approx(L)
+    # cfg5 hierarchy (nu = 9, 13, 17, 21, 25 over nnz(Phi) = 10 for ERK3+U3 collapsed,
+    # SURVEY Q8): between 1 + 1/m and the paper's reported 1.38-1.39 for ERK3+U3
+    oc5 = M.operator_complexity([10, 9, 13, 17, 21, 25], 4)
+    assert 1.25 < oc5 < 1.39
 
 
 def test_threshold_pattern_sdirk3_cfg4():
