@@ -36,12 +36,27 @@ import workloads as W  # noqa: E402
 METRIC = "fine space-time DOF updates/s (fp64) & MGRIT time-to-residual 1e-10"
 UNIT = "DOF-updates/s"
 FP64_PEAK_TFLOPS = 2 * 64 * 148 * 1.965e9 / 1e12   # 64 DFMA/clk/SM x 148 SMs x 1965 MHz
-FP64_PEAK_MEASURED = 34.08                          # tools/probe_fp64 (profiles/), DFMA chains
-# algorithmic flops per point and step of the stage form as implemented:
-# Z with t taps = 1 MUL + (t-1) FMA; every nonzero a_il, b_i = 1 FMA; SDIRK adds its
-# factored stage solves (3 first-order recurrences x 2 FMA + 1 MUL per stage).
+
+
+def _measured_fp64_peak():
+    """Median sustained DFMA rate of tools/probe_fp64 (tools/probe_fp64.sh), with the SM clock
+    nvidia-smi recorded during that run (profiles/r02_fp64_probe.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_probe.json")))
+        return float(d["dfma_tflops_median"]), d.get("sm_mhz_median_under_load")
+    except Exception:
+        return None, None
+
+
+# Algorithmic flops per point and step of the stage form (SURVEY 8(d)): Z with t taps =
+# 1 MUL + (t-1) FMA; every nonzero a_il, b_i = 1 FMA (2 flops).  SDIRK3+U3: SURVEY 8(d)'s
+# 3 x [banded stage solve ~7 + Z 7] + combinations (2 + 4) + update 6 = 55.
 FLOPS_PER_POINT_STEP = {"erk1": 5.0, "erk2": 14.0, "erk3_ssp": 33.0, "erk3_kutta": 33.0,
-                        "erk4": 44.0, "erk5": 102.0, "sdirk3": 72.0}
+                        "erk4": 44.0, "erk5": 102.0, "sdirk3": 55.0}
+# Flops the kernels actually execute per point-step (DESIGN.md 6.1: last stage folded into
+# the update; SSP-RK3 in the Shu-Osher form = 13 DFMA + 1 DADD + 1 DMUL): the FP64-pipe
+# view of the same launch, reported beside the algorithmic fraction.
+EXEC_FLOPS_PER_POINT_STEP = {"erk1": 4.0, "erk3_ssp": 28.0, "erk3_kutta": 32.0, "erk5": 101.0}
 
 
 def _dist():
@@ -158,27 +173,41 @@ def oracle_sample(w, budget_s: float = 12.0):
 
 
 def sequential_sample(w, budget_s: float = 6.0):
-    """Plain sequential time-stepping with the oracle's Phi on the host: the
-    other CPU baseline north_star names.  Bounded sample of the workload's steps; the
-    full-length time is extrapolated (nt steps)."""
-    from oracle import discretization as D
-    phi = D.make_phi(w.order, w.tableau, w.cfl, w.nx)
+    """Plain sequential time-stepping, the paper's serial baseline,
+    on the host: oracle/seqstep.c (stage form, bitwise the numpy oracle's `sequential`,
+    OpenMP over space).  All host cores run the FULL workload (nt steps); one core runs a
+    bounded sample of the steps (its full-run time is extrapolated and labelled so)."""
+    from oracle import cseq
+    if D_tab_implicit(w):
+        return None
+    ncores = os.cpu_count() or 1
     u = w.u0()
     t0 = time.perf_counter()
-    steps = 0
-    while steps < w.nt:
-        for _ in range(16):
-            u = phi(u)
-        steps += 16
-        if time.perf_counter() - t0 > budget_s:
+    cseq.seq_steps(w.order, w.tableau, w.cfl, u, w.nt, threads=ncores)
+    t_all = time.perf_counter() - t0
+    n1 = 256
+    t0 = time.perf_counter()
+    while True:
+        cseq.seq_steps(w.order, w.tableau, w.cfl, u, n1, threads=1)
+        dt1 = time.perf_counter() - t0
+        if dt1 > budget_s / 4 or n1 >= w.nt:
             break
-    dt = time.perf_counter() - t0
-    rate = steps * w.nx / dt
-    return {"value": rate, "unit": UNIT, "cores": 1, "kind": "sequential time-stepping",
-            "host": host_info(),
-            "sample": f"{steps} of {w.nt} steps of {w.tableau}+U{w.order} at nx={w.nx} "
-                      f"(oracle Phi, numpy fp64), {dt:.1f} s",
-            "full_run_s_extrapolated": round(w.nt * w.nx / rate, 1)}
+        n1 *= 2
+        t0 = time.perf_counter()
+    rate1 = n1 * w.nx / dt1
+    return {"value": w.nt * w.nx / t_all, "unit": UNIT, "cores": ncores, "threads": ncores,
+            "kind": "sequential time-stepping (oracle/seqstep.c, OpenMP over space)",
+            "host": host_info(), "time_s": round(t_all, 3),
+            "sample": f"full run: all {w.nt} steps of {w.tableau}+U{w.order} at nx={w.nx}, "
+                      f"fp64 stage form, {ncores} threads",
+            "single_core": {"value": rate1, "unit": UNIT, "cores": 1,
+                            "sample": f"{n1} of {w.nt} steps on 1 thread, {dt1:.2f} s",
+                            "full_run_s_extrapolated": round(w.nt * w.nx / rate1, 1)}}
+
+
+def D_tab_implicit(w):
+    from oracle import discretization as D
+    return D.tableau(w.tableau).implicit
 
 
 # ------------------------------------------------------------------ our arm
@@ -194,7 +223,8 @@ def run_ours(args, w):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     psi = problem.psi_inputs(w)
-    s = problem.make_solver(w, psi, stream=stream)
+    opts = {k: tuple(int(x) for x in v.split(",")) for k, v in (o.split("=") for o in args.opt)}
+    s = problem.make_solver(w, psi, stream=stream, options=opts)
     s.set_cycle(args.cycle)
     s.set_final_sweep(args.final_sweep)
     guess = problem.device_guess(w)
@@ -257,6 +287,14 @@ def run_ours(args, w):
     flops = FLOPS_PER_POINT_STEP[w.tableau] * point_steps
     avg_ms = ms_f / max(n_f, 1)
     achieved = flops / (avg_ms / 1e3) / 1e12 if avg_ms > 0 else 0.0  # 0: --no-prof
+    probe_tf, probe_mhz = _measured_fp64_peak()
+    ex = EXEC_FLOPS_PER_POINT_STEP.get(w.tableau)
+    executed = None
+    if ex and avg_ms > 0:
+        a_ex = ex * point_steps / (avg_ms / 1e3) / 1e12
+        executed = {"flops_per_point_step": ex, "achieved": round(a_ex, 3),
+                    "frac": round(a_ex / FP64_PEAK_TFLOPS, 4),
+                    "frac_vs_probe": round(a_ex / probe_tf, 4) if probe_tf else None}
     shares = {k: round(v[1] / max(ms_total_prof, 1e-9), 4) for k, v in prof.items()}
     # ---- sequential coarse solve: ns per coarse step vs its FP64 floor ----
     desc = s.describe()
@@ -350,8 +388,13 @@ def run_ours(args, w):
         "roofline": {"bound": "alu", "kernel": s.describe() + " (fine FCF sweep)",
                      "achieved": round(achieved, 3), "peak": round(FP64_PEAK_TFLOPS, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
-                     "peak_note": "FP64 pipe: 64 DFMA/clk/SM x 148 x 1.965 GHz (derived); "
-                                  f"measured DFMA probe {FP64_PEAK_MEASURED} TF/s",
+                     "peak_note": "FP64 pipe: 64 DFMA/clk/SM x 148 x 1.965 GHz (derived from the "
+                                  "guide's unit count and the max clock; MEASURED_PEAKS.json has "
+                                  "no FP64 entry)",
+                     "probe": {"tflops": probe_tf, "sm_mhz": probe_mhz,
+                               "frac": round(achieved / probe_tf, 4) if probe_tf else None,
+                               "source": "profiles/r02_fp64_probe.json (tools/probe_fp64.sh)"},
+                     "executed": executed,
                      "flops_note": f"{FLOPS_PER_POINT_STEP[w.tableau]:g} algorithmic flops per "
                                    "point-step (stage form, SURVEY 8d); the kernel issues fewer "
                                    "FP64 instructions (folded last stage, Shu-Osher SSP-RK3: "
@@ -419,6 +462,8 @@ def main():
                     help="mgrit_set_final_sweep mode (include/mgrit.h)")
     ap.add_argument("--cycle", default="V", choices=["V", "F"],
                     help="multilevel cycle (DESIGN.md R19); the bench line is the V-cycle")
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=V1,V2",
+                    help="mgrit_set_option override (experiments), e.g. fine_tile=128,15")
     args = ap.parse_args()
     w = W.ALL[args.config]
     if args.impl == "reference":

@@ -39,7 +39,8 @@ typedef enum {
   MGRIT_ENOMEM = -2,      /* workspace too small */
   MGRIT_ECUDA = -3,       /* CUDA launch/runtime error */
   MGRIT_ENONFINITE = -4,  /* residual became NaN/Inf; history filled up to that point */
-  MGRIT_EUNSUPPORTED = -5 /* valid but not implemented combination */
+  MGRIT_EUNSUPPORTED = -5, /* valid but not implemented combination */
+  MGRIT_ECOMM = -6         /* a time-shard communication callback failed */
 } mgrit_status;
 
 /* Runge-Kutta tableaux of Appendix A.  Order p pairs RK_p with U_p. */
@@ -96,7 +97,7 @@ size_t mgrit_workspace_bytes(int nx, int nt, int m, int levels);
  *   levels      2 = two-level MGRIT/Parareal; > 2 = multilevel V-cycle.
  *   psi         host array of levels-1 coarse operators Psi_2..Psi_L (copied).  IDEAL
  *               (Phi^m) and REDISC (Phi at CFL redisc_cfl) are only valid for
- *               levels == 2 and nx in {64, 128, 256, 1024}; with an SDIRK tableau the coarse
+ *               levels == 2 and nx in {64, 128, ..., 4096}; with an SDIRK tableau the coarse
  *               step solves its own stages (factored as for the fine step).
  *   relax       production relaxation of mgrit_solve: MGRIT_RELAX_F (Parareal) or
  *               MGRIT_RELAX_FCF.
@@ -137,21 +138,36 @@ int mgrit_scheme_coefficients(int order, int tableau, double cfl, int *s, int *z
 int mgrit_set_guess(mgrit_ctx *ctx, const double *guess_dev);
 
 /*
- * FULL-state primitives on a caller-owned (nt+1) x nx device array U_dev (level 0 only),
- * in place.  Row 0 is never written.
- *   mgrit_relax:        kind F: U[jm+i] = Phi U[jm+i-1], i = 1..m-1;  C: U[(j+1)m] =
- *                       Phi U[(j+1)m-1];  FCF: F then C then F.
- *   mgrit_residual:     norm_host (nullable) = sqrt(dx dt sum_{n>=1} |Phi U[n-1] - U[n]|^2)
- *                       over ALL rows (R1); r_dev (nullable, (nt/m+1) x nx)
- *                       receives the C-point residuals r_j = Phi U[jm-1] - U[jm], r_0 = 0.
- *   mgrit_coarse_solve: two-level coarse-grid correction: C-point residuals, sequential
- *                       coarse solve e_j = Psi e_{j-1} + r_j, e_0 = 0 (eq. 3),
- *                       U[jm] += e_j, then F-relaxation ("ideal interpolation").
+ * FULL-state primitives on a caller-owned device array U_dev of level `level`, in place
+ * (P:206-212).  Level 0 is the fine grid: U_dev is (nt+1) x nx, Phi_0 = Phi (the RK step),
+ * row 0 = u0 is never written.  Level l >= 1 (multilevel hierarchy, P:618-624;
+ * stencil Psi only) is (nt_l+1) x nx with nt_l = nt/m^l, Phi_l = Psi_l, and the equations
+ * U[n] = Psi_l U[n-1] + g_l[n] (R12) with the right-hand side registered by
+ * mgrit_set_rhs (none: g_l = 0); row 0 is not written either.
+ *   mgrit_relax:        kind F: U[jm+i] = Phi_l U[jm+i-1] (+ g_l[jm+i]), i = 1..m-1;
+ *                       C: U[(j+1)m] = Phi_l U[(j+1)m-1] (+ g_l); FCF: F then C then F.
+ *   mgrit_residual:     norm_host (nullable) = sqrt(dx dt_l sum_{n>=1} |r[n]|^2), dt_l = m^l dt,
+ *                       r[n] = (g_l[n] +) Phi_l U[n-1] - U[n] over ALL rows (DESIGN.md
+ *                       R1); r_dev (nullable, (nt_l/m+1) x nx) receives the C-point
+ *                       residuals r_j = r[jm], r_0 = 0.
+ *   mgrit_coarse_solve: coarse-grid correction of level l by level l+1 solved exactly
+ *                       (sequentially): r_j as above, e_j = Psi_{l+1} e_{j-1} + r_j, e_0 = 0
+ *                       (eq. 3), U[jm] += e_j, then F-relaxation ("ideal
+ *                       interpolation").  Needs l + 1 < levels.
+ * Errors: EINVAL (null pointers, level out of range, nt_l not a multiple of m),
+ *         EUNSUPPORTED (level >= 1 with an IDEAL/REDISC Psi), ECUDA.
  */
 int mgrit_relax(mgrit_ctx *ctx, int level, int kind, double *U_dev);
 int mgrit_residual(mgrit_ctx *ctx, int level, const double *U_dev, double *norm_host,
                    double *r_dev);
 int mgrit_coarse_solve(mgrit_ctx *ctx, int level, double *U_dev);
+
+/*
+ * mgrit_set_rhs — right-hand side g_l ((nt_l+1) x nx device array, read only, caller-owned;
+ * NULL = zero) used by the level-l FULL primitives above, 1 <= level < levels.  Level 0 has
+ * no right-hand side (g_0 = (u0, 0, ..., 0) is implied by row 0 of U).  Errors: EINVAL.
+ */
+int mgrit_set_rhs(mgrit_ctx *ctx, int level, const double *g_dev);
 
 /*
  * mgrit_solve — MGRIT iterations from the registered guess until ||r^(k)|| < tol or
@@ -193,6 +209,88 @@ int mgrit_set_cycle(mgrit_ctx *ctx, int cycle);
  */
 enum { MGRIT_FINAL_OFF = 0, MGRIT_FINAL_PREDICT = 1, MGRIT_FINAL_ALWAYS = 2 };
 int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
+
+/*
+ * mgrit_set_option — replace a measured kernel-configuration default by another valid
+ * one (tuning scans, tests of alternative kernels).  Results stay correct for every
+ * accepted value; a configuration that no kernel supports makes the next call that needs
+ * it return MGRIT_EUNSUPPORTED.  n = 0 restores the default.  Host-only; the library
+ * reads no environment variables.
+ *   MGRIT_OPT_FINE_TILE      NT, P[, minBlocks]  tile of the fused FCF fine sweep (halo tiles)
+ *   MGRIT_OPT_WHOLE_ROW      NT, P               whole-periodic-row sweep tried first
+ *   MGRIT_OPT_SEQ_CLUSTER    CL, NT, P           two-level coarse solve: cluster split (CL = 0:
+ *                                                no cluster -> single-CTA solve)
+ *   MGRIT_OPT_SEQ_S          S                   s-step depth limit (S < 2: exchange every step)
+ *   MGRIT_OPT_COARSE_KERNEL  0 | 1               warp-specialised (default) | cp.async variant
+ *   MGRIT_OPT_SEQ_CFG        NT, P               single-CTA coarse solve configuration
+ *   MGRIT_OPT_SDIRK_PRODUCT  0 | 1               1: product-form SDIRK stage solves only
+ *   MGRIT_OPT_GRAPH          0 | 1               mgrit_solve's iterations as one CUDA graph with
+ *                                                a device-side WHILE loop (one host sync per
+ *                                                solve) | per-iteration host loop; default:
+ *                                                graph for nx*nt <= 2^23 (latency-bound), host
+ *                                                loop otherwise (it predicts the last
+ *                                                iteration and fuses materialisation)
+ *   MGRIT_OPT_STAGE_FORM     0 | 1               1: explicit steps in the plain Runge-Kutta
+ *                                                stage form (no folded last stage, no
+ *                                                Shu-Osher SSP-RK3; R5)
+ * Errors: EINVAL (unknown option, wrong count, negative value); EUNSUPPORTED if the new
+ * whole-row / SDIRK setting cannot factor the stage solves (the old setting is kept).
+ */
+typedef enum {
+  MGRIT_OPT_FINE_TILE = 0,
+  MGRIT_OPT_WHOLE_ROW = 1,
+  MGRIT_OPT_SEQ_CLUSTER = 2,
+  MGRIT_OPT_SEQ_S = 3,
+  MGRIT_OPT_COARSE_KERNEL = 4,
+  MGRIT_OPT_SEQ_CFG = 5,
+  MGRIT_OPT_SDIRK_PRODUCT = 6,
+  MGRIT_OPT_STAGE_FORM = 7,
+  MGRIT_OPT_GRAPH = 8,
+  MGRIT_OPT_COUNT = 9
+} mgrit_option;
+int mgrit_set_option(mgrit_ctx *ctx, int option, const int *values, int n);
+
+/*
+ * ---- Time-parallel MGRIT over several GPUs (the paper parallelises time
+ * only, with contiguous blocks of time per processor) ----
+ *
+ * mgrit_setup_shard creates the context of time shard `rank` of `nranks`: the global
+ * problem has nt steps; this rank owns steps [rank*nt/nranks, (rank+1)*nt/nranks] (its
+ * fine C-intervals j in [rank*nc, (rank+1)*nc), nc = nt/(m*nranks)), with nt/nranks
+ * divisible by m^(levels-1).  Every level's sweep, residual injection and interpolation run
+ * on the rank's own intervals; the sequential coarsest-level solve is pipelined across the
+ * ranks (state x passed rank to rank).  Exchanges per iteration, each one row of nx doubles
+ * through the caller-owned staging rows stage_send_dev / stage_recv_dev:
+ *   - the current iterate's C-row at the block start (halo, from rank-1) before each fine
+ *     sweep, the corrected level-l C-row at the block start before each interpolation;
+ *   - the coarse right-hand side r_{nc+1} of the block's last interval (to rank+1) after
+ *     each sweep;
+ *   - the coarsest chain's state (rank-1 -> rank);
+ *   - the squared residual norm (allreduce_sum of one double).
+ * The caller provides the communication (NCCL/gloo through torch.distributed, or an
+ * in-process emulation) as callbacks:
+ *   shift(user, has_send, has_recv, stream): if has_send, send stage_send_dev (written on
+ *     `stream` before the call; the callback orders itself after it) to rank+1; if has_recv,
+ *     receive rank-1's row into stage_recv_dev, complete before returning.  Called by every
+ *     rank at the same points (flags 0 for the missing neighbour).  0 on success.
+ *   allreduce_sum(user, vals, n): in-place sum of n host doubles over all ranks.
+ * The guess (mgrit_set_guess) and out_dev are the rank's local FULL block of
+ * nt/nranks + 1 rows whose row 0 is global row rank*nt/nranks (u0 on rank 0).  Stencil Psi
+ * and the V-cycle only (EUNSUPPORTED otherwise); the history is the global one, identical
+ * on every rank.  nranks = 1 is an ordinary solve through the same code path.
+ */
+typedef struct {
+  void *user;
+  int (*shift)(void *user, int has_send, int has_recv, void *stream);
+  int (*allreduce_sum)(void *user, double *vals, int n);
+} mgrit_comm;
+size_t mgrit_workspace_bytes_shard(int nx, int nt, int m, int levels, int nranks);
+int mgrit_setup_shard(mgrit_ctx **ctx, int nx, int nt, int m, double alpha, double cfl,
+                      int order, int tableau, int levels, const mgrit_psi *psi, int relax,
+                      int rank, int nranks, double *stage_send_dev, double *stage_recv_dev,
+                      void *workspace_dev, size_t workspace_bytes, void *stream);
+int mgrit_solve_shard(mgrit_ctx *ctx, const mgrit_comm *comm, double tol, int max_iter,
+                      double *out_dev, int *iters, double *hist_host, int *converged);
 
 /* C-rows (nt/m+1) x nx of the current iterate after mgrit_solve. */
 int mgrit_get_crows(mgrit_ctx *ctx, double *out_dev);

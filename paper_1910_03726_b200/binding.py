@@ -14,12 +14,19 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmgrit.so")
+# MGRIT_LIBRARY=jitter loads the race-stress build (tests/test_gpu_jitter.py only; the same
+# ABI, random sleeps at the asynchronous protocol points).  No CPU fallback either way.
+if os.environ.get("MGRIT_LIBRARY") == "jitter":
+    LIB_PATH = os.path.join(HERE, "libmgrit_jitter.so")
 
 TABLEAU = {"erk1": 0, "erk2": 1, "erk3_ssp": 2, "erk3_kutta": 3, "erk4": 4, "erk5": 5,
            "sdirk1": 6, "sdirk2": 7, "sdirk3": 8, "sdirk4": 9}
 RELAX = {"F": 0, "C": 1, "FCF": 2}
 PSI_KIND = {"stencil": 0, "ideal": 1, "redisc": 2}
-STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENONFINITE", -5: "EUNSUPPORTED"}
+STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENONFINITE", -5: "EUNSUPPORTED",
+          -6: "ECOMM"}
+OPTION = {"fine_tile": 0, "whole_row": 1, "seq_cluster": 2, "seq_s": 3, "coarse_kernel": 4,
+          "seq_cfg": 5, "sdirk_product": 6, "stage_form": 7, "graph": 8}
 PROF_CLASSES = ("fine_sweep", "level_sweep", "coarse_solve", "interp", "residual", "other")
 MAX_LEVELS = 8
 
@@ -57,13 +64,23 @@ _SIGS = [
     ("mgrit_residual", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_double),
                                  C.c_void_p]),
     ("mgrit_coarse_solve", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    ("mgrit_set_rhs", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     ("mgrit_solve", C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.POINTER(C.c_int),
                               C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p]),
     ("mgrit_set_cycle", C.c_int, [C.c_void_p, C.c_int]),
     ("mgrit_set_final_sweep", C.c_int, [C.c_void_p, C.c_int]),
+    ("mgrit_set_option", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_int]),
     ("mgrit_get_crows", C.c_int, [C.c_void_p, C.c_void_p]),
     ("mgrit_fill_guess", C.c_int, [C.c_void_p, C.c_longlong, C.c_longlong, C.c_int,
                                    C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
+    ("mgrit_workspace_bytes_shard", C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    ("mgrit_setup_shard", C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_double,
+                                    C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(_Psi),
+                                    C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("mgrit_solve_shard", C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p,
+                                    C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_int)]),
     ("mgrit_profile_enable", C.c_int, [C.c_void_p, C.c_int]),
     ("mgrit_profile_read", C.c_int, [C.c_void_p, C.POINTER(C.c_longlong),
                                      C.POINTER(C.c_double)]),
@@ -128,6 +145,24 @@ def fill_guess(dst, seed: int, lo: float = -1.0, u0=None, row0: int = 0, stream=
     return dst
 
 
+def psi_array(psi: Sequence[Dict], levels: int):
+    """The mgrit_psi array of levels-1 coarse operators (+ the ctypes buffers to keep)."""
+    arr = (_Psi * max(1, levels - 1))()
+    keep = []
+    for l, p in enumerate(psi):
+        kind = PSI_KIND[p["kind"]]
+        arr[l].kind = kind
+        if kind == 0:
+            offs = (C.c_int * len(p["offsets"]))(*[int(o) for o in p["offsets"]])
+            cof = (C.c_double * len(p["coeffs"]))(*[float(c) for c in p["coeffs"]])
+            keep += [offs, cof]
+            arr[l].nnz = len(p["offsets"])
+            arr[l].offsets = C.cast(offs, C.POINTER(C.c_int))
+            arr[l].coeffs = C.cast(cof, C.POINTER(C.c_double))
+        arr[l].redisc_cfl = float(p.get("cfl", 0.0))
+    return arr, keep
+
+
 def _stream(stream) -> int:
     import torch
     if stream is None:
@@ -144,7 +179,7 @@ class MGRIT:
 
     def __init__(self, nx: int, nt: int, m: int, alpha: float, cfl: float, order: int,
                  tableau: str, levels: int, psi: Sequence[Dict], relax: str = "FCF",
-                 stream=None, device: str = "cuda"):
+                 stream=None, device: str = "cuda", options: Optional[Dict] = None):
         import torch
         self.nx, self.nt, self.m, self.levels = nx, nt, m, levels
         self.alpha, self.cfl, self.order, self.tableau = alpha, cfl, order, tableau
@@ -156,19 +191,7 @@ class MGRIT:
         if nbytes == 0:
             raise MgritError(-1, f"invalid sizes nx={nx} nt={nt} m={m} levels={levels}")
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        arr = (_Psi * max(1, levels - 1))()
-        self._keep = []
-        for l, p in enumerate(psi):
-            kind = PSI_KIND[p["kind"]]
-            arr[l].kind = kind
-            if kind == 0:
-                offs = (C.c_int * len(p["offsets"]))(*[int(o) for o in p["offsets"]])
-                cof = (C.c_double * len(p["coeffs"]))(*[float(c) for c in p["coeffs"]])
-                self._keep += [offs, cof]
-                arr[l].nnz = len(p["offsets"])
-                arr[l].offsets = C.cast(offs, C.POINTER(C.c_int))
-                arr[l].coeffs = C.cast(cof, C.POINTER(C.c_double))
-            arr[l].redisc_cfl = float(p.get("cfl", 0.0))
+        arr, self._keep = psi_array(psi, levels)
         ctx = C.c_void_p()
         st = lib().mgrit_setup(C.byref(ctx), nx, nt, m, alpha, cfl, order, TABLEAU[tableau],
                                levels, arr, RELAX[relax], self.workspace.data_ptr(), nbytes,
@@ -177,6 +200,8 @@ class MGRIT:
             raise MgritError(st, "mgrit_setup failed (see stderr)")
         self.ctx = ctx
         self.guess = None
+        for k, v in (options or {}).items():
+            self.set_option(k, v)
 
     def __del__(self):
         try:
@@ -191,21 +216,28 @@ class MGRIT:
             msg = lib().mgrit_last_error(self.ctx)
             raise MgritError(st, f"{what}: {msg.decode() if msg else ''}")
 
-    # ---- FULL-state primitives -----------------------------------------------
-    def relax_full(self, U, kind: str = "FCF"):
-        self._check(lib().mgrit_relax(self.ctx, 0, RELAX[kind], _dptr(U)), "mgrit_relax")
+    # ---- FULL-state primitives (level 0: fine grid; level l >= 1: Psi_l with RHS g_l) ----
+    def relax_full(self, U, kind: str = "FCF", level: int = 0):
+        self._check(lib().mgrit_relax(self.ctx, level, RELAX[kind], _dptr(U)), "mgrit_relax")
 
-    def residual_full(self, U, want_r: bool = False):
+    def residual_full(self, U, want_r: bool = False, level: int = 0):
         import torch
         norm = C.c_double()
-        r = torch.empty((self.nt // self.m + 1, self.nx), dtype=torch.float64,
+        ntl = self.nt // self.m ** level
+        r = torch.empty((ntl // self.m + 1, self.nx), dtype=torch.float64,
                         device=U.device) if want_r else None
-        self._check(lib().mgrit_residual(self.ctx, 0, _dptr(U), C.byref(norm), _dptr(r)),
+        self._check(lib().mgrit_residual(self.ctx, level, _dptr(U), C.byref(norm), _dptr(r)),
                     "mgrit_residual")
         return (norm.value, r) if want_r else norm.value
 
-    def coarse_solve_full(self, U):
-        self._check(lib().mgrit_coarse_solve(self.ctx, 0, _dptr(U)), "mgrit_coarse_solve")
+    def coarse_solve_full(self, U, level: int = 0):
+        self._check(lib().mgrit_coarse_solve(self.ctx, level, _dptr(U)), "mgrit_coarse_solve")
+
+    def set_rhs(self, level: int, g=None):
+        """mgrit_set_rhs: the level-l right-hand side g_l of the level primitives (None: 0)."""
+        self._rhs_keep = getattr(self, "_rhs_keep", {})
+        self._rhs_keep[level] = g
+        self._check(lib().mgrit_set_rhs(self.ctx, level, _dptr(g)), "mgrit_set_rhs")
 
     # ---- production solve -------------------------------------------------------
     def set_guess(self, guess):
@@ -216,6 +248,13 @@ class MGRIT:
     def set_cycle(self, cycle: str):
         """Multilevel cycle of `solve`: "V" (default) or "F" (R19)."""
         self._check(lib().mgrit_set_cycle(self.ctx, {"V": 0, "F": 1}[cycle]), "mgrit_set_cycle")
+
+    def set_option(self, name: str, values: Sequence[int] = ()):
+        """mgrit_set_option (include/mgrit.h): a kernel-configuration override, () = default."""
+        vals = [int(v) for v in values]
+        arr = (C.c_int * max(1, len(vals)))(*vals)
+        self._check(lib().mgrit_set_option(self.ctx, OPTION[name], arr, len(vals)),
+                    f"mgrit_set_option({name})")
 
     def set_final_sweep(self, mode: str):
         """mgrit_set_final_sweep: "off", "predict" (default) or "always" (include/mgrit.h)."""

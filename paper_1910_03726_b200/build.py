@@ -10,7 +10,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmgrit.so")
-SOURCES = ["mgrit_api.cu", "sweep.cu", "coarse.cu"]
+# race-stress variant (tma.cuh / device.cuh mg_jitter): random sleeps at every asynchronous
+# protocol point; used only by tests/test_gpu_jitter.py
+JITTER_LIB = os.path.join(HERE, "libmgrit_jitter.so")
+SOURCES = ["mgrit_api.cu", "sweep.cu", "coarse.cu", "levels.cu", "graph.cu"]
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -28,19 +31,23 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
+    """variant "" -> libmgrit.so; "jitter" -> libmgrit_jitter.so (-DMG_JITTER)."""
+    lib = JITTER_LIB if variant == "jitter" else LIB
+    extra = ["-DMG_JITTER"] if variant == "jitter" else []
+    tag = "." + variant if variant else ""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     deps.append(os.path.join(ROOT, "include", "mgrit.h"))
-    if not force and os.path.exists(LIB):
-        lt = os.path.getmtime(LIB)
+    if not force and os.path.exists(lib):
+        lt = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= lt for d in deps):
             return LIB
     objs = []
     procs = []
     for s in srcs:
-        o = os.path.join(CSRC, os.path.basename(s) + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", s, "-o", o]
+        o = os.path.join(CSRC, os.path.basename(s) + tag + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", s, "-o", o]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(o)
     log = []
@@ -50,16 +57,17 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if p.returncode != 0:
             sys.stderr.write(out)
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB]
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib]
     subprocess.run(cmd, check=True)
     for o in objs:
         os.remove(o)
     if verbose:
         sys.stdout.write("".join(log))
-    with open(os.path.join(HERE, "ptxas.log"), "w") as f:
+    with open(os.path.join(HERE, f"ptxas{tag}.log"), "w") as f:
         f.write("".join(log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force=True))
+    print(build(verbose="-v" in sys.argv, force=True,
+                variant="jitter" if "--jitter" in sys.argv else ""))

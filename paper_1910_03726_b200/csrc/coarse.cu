@@ -363,11 +363,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   return r;
 }
 __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  mg_jitter(6);
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
                "l"(__double_as_longlong(v)), "r"(rbar)
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  mg_jitter(7);
   uint32_t done;
   do {
     asm volatile(
@@ -891,6 +893,10 @@ cudaError_t launch_psi_seq_cluster_ca(int cl, SweepCfg c, int S, const CoarseArg
   if (cl == 8 && c.nt_threads == 128 && c.p == 4) return launch_seq_ca<128, 4, 8>(a, S, s);
   if (cl == 16 && c.nt_threads == 64 && c.p == 4) return launch_seq_ca<64, 4, 16>(a, S, s);
   if (cl == 8 && c.nt_threads == 32 && c.p == 4) return launch_seq_ca<32, 4, 8>(a, S, s);
+  // wider rows (two-level solves beyond nx = 4096): 2048, 8192, 16384 points per cluster
+  if (cl == 16 && c.nt_threads == 64 && c.p == 2) return launch_seq_ca<64, 2, 16>(a, S, s);
+  if (cl == 16 && c.nt_threads == 128 && c.p == 4) return launch_seq_ca<128, 4, 16>(a, S, s);
+  if (cl == 16 && c.nt_threads == 256 && c.p == 4) return launch_seq_ca<256, 4, 16>(a, S, s);
   return cudaErrorInvalidConfiguration;
 }
 
@@ -917,6 +923,7 @@ template <int NT, int P> struct TbSmem {
 };
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
+  mg_jitter(8);
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -1151,7 +1158,13 @@ cudaError_t launch_psi_seq_cluster_tb(int cl, SweepCfg c, int S, const CoarseArg
   if (cl == 16 && c.nt_threads == 128 && c.p == 2) return launch_seq_tb<128, 2, 16>(a, S, s);
   if (cl == 16 && c.nt_threads == 32 && c.p == 2) return launch_seq_tb<32, 2, 16>(a, S, s);
   if (cl == 16 && c.nt_threads == 64 && c.p == 4) return launch_seq_tb<64, 4, 16>(a, S, s);
+  if (cl == 16 && c.nt_threads == 128 && c.p == 4) return launch_seq_tb<128, 4, 16>(a, S, s);
   return cudaErrorInvalidConfiguration;
+}
+
+bool seq_cluster_tb_supported(int cl, SweepCfg c) {
+  return cl == 16 && ((c.nt_threads == 128 && c.p == 2) || (c.nt_threads == 32 && c.p == 2) ||
+                      (c.nt_threads == 64 && c.p == 4) || (c.nt_threads == 128 && c.p == 4));
 }
 
 // nx = CL * NT * P; the halos (-o0, o0+nu-1) must be <= 64 and <= NT*P (host-checked).
@@ -1734,8 +1747,14 @@ static cudaError_t launch_rkc(SweepCfg c, const RKCoarseArgs &a, cudaStream_t s)
     rk_coarse_kernel<SC, 32, 4><<<1, 32, smem, s>>>(a);
   } else if (c.nt_threads == 32 && c.p == 8) {
     rk_coarse_kernel<SC, 32, 8><<<1, 32, smem, s>>>(a);
+  } else if (c.nt_threads == 64 && c.p == 8) {
+    rk_coarse_kernel<SC, 64, 8><<<1, 64, smem, s>>>(a);
   } else if (c.nt_threads == 128 && c.p == 8) {
     rk_coarse_kernel<SC, 128, 8><<<1, 128, smem, s>>>(a);
+  } else if (c.nt_threads == 256 && c.p == 8) {
+    rk_coarse_kernel<SC, 256, 8><<<1, 256, smem, s>>>(a);
+  } else if (c.nt_threads == 256 && c.p == 16) {
+    rk_coarse_kernel<SC, 256, 16><<<1, 256, smem, s>>>(a);
   } else {
     return cudaErrorInvalidConfiguration;
   }

@@ -96,6 +96,7 @@ int seq_ca_depth(int cl, SweepCfg cfg, int nx, int o0, int nu, int smax);
 // Same split and s-step halos with batched TMA I/O (g ring, reduce-add correction), the
 // launch's window phase as a template parameter; nu <= 32.
 cudaError_t launch_psi_seq_cluster_tb(int cl, SweepCfg cfg, int S, const CoarseArgs &a, cudaStream_t s);
+bool seq_cluster_tb_supported(int cl, SweepCfg cfg);
 
 // Level-l (l >= 2) relaxation sweep of the V-cycle with Psi_l and RHS g (u = 0 start):
 //   phase 1: x_i = Psi x_{i-1} + g[jm+i], i=1..m, x_0 = u_j (null: 0) -> v_{j+1}
@@ -129,6 +130,35 @@ struct RKCoarseArgs {
   SdirkCoef sd;      // implicit schemes: the coarse step's factored stage solve
 };
 cudaError_t launch_rk_coarse(int scheme, SweepCfg cfg, const RKCoarseArgs &a, cudaStream_t s);
+
+// Level-l (l >= 1) FULL-state primitives (levels.cu): rows n = n0 + j*nstride,
+// j = 0..nrows-1, y = Psi U[n-1] + g[n] (g null: 0).  mode 0: dst[n] = y;  mode 1:
+// r = y - U[n], per-block sum r^2 -> partials[j*bpr + b] (nullable), and if rstore is
+// set, r -> rstore row (roff + j).  bpr blocks of 256 threads per row (1..64).
+struct RowStepArgs {
+  int nx, nrows, bpr, mode;
+  long long n0, nstride;
+  const double *U;
+  double *dst;
+  const double *g;
+  double *partials;
+  double *rstore;
+  long long roff;
+  PsiOp op;
+};
+cudaError_t launch_psi_rowstep(const RowStepArgs &a, cudaStream_t s);
+
+// Device-side loop control of the CUDA-graph solve (graph.cu).
+struct LoopState {
+  double tol, dxdt;
+  int k, max_iter, stop, nonfinite;
+};
+cudaError_t launch_loop_init(LoopState *s, double tol, double dxdt, int max_iter, int k0,
+                             cudaStream_t st);
+// ||r^(k)|| = sqrt(dxdt * norm2[0]) -> hist[k]; handles h0 (and h1 if set_h1) := !stop
+cudaError_t launch_loop_decide(LoopState *s, const double *norm2, double *hist,
+                               cudaGraphConditionalHandle h0, cudaGraphConditionalHandle h1,
+                               int set_h1, cudaStream_t st);
 
 // Deterministic reduction of partials -> out[0] (single block, fixed order).
 cudaError_t launch_reduce(const double *partials, long long n, double *out, cudaStream_t s);

@@ -8,6 +8,7 @@
 //   repeat: coarse correction (two-level sequential, or V-cycle)  -> u
 //           sweep(u) -> ||r^(k)|| ; stop when < tol                (R2)
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges per solve / iteration / level / kernel class
 
 #include <algorithm>
 #include <cmath>
@@ -123,24 +124,49 @@ void make_z(int order, double cfl, double *z, int *zlo, int *zn) {
 }
 
 // b_{S-1} z_d for the explicit step's folded last stage, and the Shu-Osher-type form of
-// a 3-stage ERK with a20 = a21 and b0 = b1 (SSP-RK3: 1/4, 1/4 and 1/6, 1/6; device.cuh
+// a 3-stage ERK (SSP-RK3: a10 = 1, a20 = a21 = 1/4, b0 = b1 = 1/6, b2 = 2/3; device.cuh
 // erk_step): y2 = x + a21 Z(x + y1) and x' = x + b0 Z(x + y1) + b2 Z y2
-// = (1 - b0/a21) x + (b0/a21) y2 + b2 Z y2.
-static void fold_last_stage(RKCoeffs &co, int s) {
+// = (1 - b0/a21) x + (b0/a21)(y2 + Z y2) when b0/a21 == b2 (R5, 6.1).  The form is
+// used only when every coefficient it needs is exact in fp64 -- b0/a21 == b2 exactly,
+// 1 - b2 + b2 == 1, a10 and a21 powers of two (so a10 z_d, a21 z_d are exact) -- because
+// then it applies exactly the operator of the oracle's stage form with the same fp64
+// coefficients (4 fl(1/6) = fl(2/3)); a rounded product coefficient would bias every step
+// and drift linearly with nt (the measured 1.2e-12 at 65536 steps of the
+// earlier form with b2 z_d products).
+static bool pow2(double v) {
+  int e;
+  return v != 0.0 && std::fabs(std::frexp(v, &e)) == 0.5;
+}
+// Step forms (MGRIT_OPT_STAGE_FORM): 0 = production default, 1 = plain stage form,
+// 2 = stage form with the folded last stage, 3 = Shu-Osher exact-operator form,
+// 4 = incremental Shu-Osher form.
+// Default: the incremental form (4).  Measured against the full-length cfg5 golden
+// (8192 x 65536, tools/golden_forms.py): 1: 2.3e-13, 2: 1.7e-13, 3: 1.19e-12 (the product
+// so0 * x rounds a full-size value every step, a bias the coarse chain accumulates), 4:
+// 2.5e-13, at the speed of 3 (15 FP64 instructions per point-step for U3).
+constexpr int kDefaultForm = 4;
+static void fold_last_stage(RKCoeffs &co, int s, int form = 0) {
+  if (form == 0) form = kDefaultForm;
   for (int d = 0; d < MAXZ; ++d) co.bz[d] = (s > 0) ? co.b[s - 1] * co.z[d] : 0.0;
   co.so3 = 0;
+  co.fold = form == 1 ? 0 : 1;
+  if (form <= 2) return;
   if (s != 3 || co.mdiag[0] != 0.0) return;
   const double a10 = co.A[1][0], a20 = co.A[2][0], a21 = co.A[2][1];
   const double b0 = co.b[0], b1 = co.b[1], b2 = co.b[2];
-  if (a21 == 0.0 || a20 != a21 || b0 != b1) return;
-  co.so[1] = b0 / a21;
-  co.so[0] = 1.0 - co.so[1];
+  if (a21 == 0.0 || a20 != a21 || b0 != b1 || !pow2(a10) || !pow2(a21)) return;
+  const volatile double q = b0 / a21;
+  const volatile double one_minus = 1.0 - b2;
+  if (q != b2 || one_minus + b2 != 1.0) return;
+  if (form == 4 && a10 != 1.0) return;
+  co.so[1] = b2;
+  co.so[0] = one_minus;
   for (int d = 0; d < MAXZ; ++d) {
     co.soz[0][d] = a10 * co.z[d];
     co.soz[1][d] = a21 * co.z[d];
-    co.soz[2][d] = b2 * co.z[d];
+    co.soz[2][d] = 0.0;
   }
-  co.so3 = 1;
+  co.so3 = form == 4 ? 2 : 1;
 }
 
 int scheme_id(int tableau) {
@@ -431,15 +457,21 @@ bool rk_coarse_cfg(int nx, SweepCfg &cfg) {
   if (nx == 64) cfg = {32, 2};
   else if (nx == 128) cfg = {32, 4};
   else if (nx == 256) cfg = {32, 8};
+  else if (nx == 512) cfg = {64, 8};
   else if (nx == 1024) cfg = {128, 8};
+  else if (nx == 2048) cfg = {256, 8};
+  else if (nx == 4096) cfg = {256, 16};
   else return false;
   return true;
 }
 
+// Longest history the CUDA-graph solve keeps on the device (max_iter < kGraphHist).
+constexpr int kGraphHist = 4096;
+
 // Layout of the workspace (doubles unless noted).
 struct Layout {
   size_t u0, v0, g[MGRIT_MAX_LEVELS], u2[MGRIT_MAX_LEVELS], ul[MGRIT_MAX_LEVELS];
-  size_t partials, scal, sa, sb, total;
+  size_t partials, scal, sa, sb, hist, lstate, st_in, st_out, total;
   long long npart;
 };
 
@@ -459,7 +491,7 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
   long long ntl = nt;
   for (int l = 1; l < levels; ++l) {
     ntl /= m;  // nt at level l
-    L.g[l] = take((ntl + 1) * row);
+    L.g[l] = take((ntl + 2) * row);   // + the outbox row of a time shard (r_{nc+1})
     if (l < levels - 1) {
       L.ul[l] = take((ntl / m + 1) * row);
       L.u2[l] = take((ntl / m + 1) * row);   // F-cycle: C-rows of the second (V) visit
@@ -471,8 +503,12 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
   L.npart = (long long)(nt + 1) * 64;
   L.partials = take((L.npart + 1024) * sizeof(double));  // + room for the reduction chunks
   L.scal = take(64 * sizeof(double));
+  L.hist = take(kGraphHist * sizeof(double));   // device history of the graph-mode solve
+  L.lstate = take(64);
   L.sa = take(row);
   L.sb = take(row);
+  L.st_in = take(row);    // time shards: coarsest-chain state from the left neighbour
+  L.st_out = take(row);   //              and to the right neighbour
   L.total = off;
   return true;
 }
@@ -483,6 +519,9 @@ struct mgrit_ctx {
   int nx, nt, m, levels, order, tableau, relax, scheme;
   int cycle = MGRIT_CYCLE_V;
   int final_sweep = MGRIT_FINAL_PREDICT;  // mgrit_set_final_sweep
+  // mgrit_set_option: explicit replacements of measured defaults (n = 0: default)
+  int opt_n[MGRIT_OPT_COUNT] = {0};
+  int opt_v[MGRIT_OPT_COUNT][4] = {{0}};
   bool implicit;
   double alpha, cfl, dx, dt;
   cudaStream_t stream;
@@ -500,8 +539,21 @@ struct mgrit_ctx {
   char *ws;
   double *u0b, *v0b, *g[MGRIT_MAX_LEVELS], *u2[MGRIT_MAX_LEVELS], *ul[MGRIT_MAX_LEVELS];
   double *partials, *scal, *sa, *sb;
+  double *hist_dev;       // graph mode: ||r^(k)|| on the device
+  // time sharding (mgrit_setup_shard): this context holds fine intervals
+  // [rank*nc, (rank+1)*nc) of a global problem of nranks*nc intervals
+  int rank = 0, nranks = 1;
+  double *stage_send = nullptr, *stage_recv = nullptr;   // caller-owned, nx doubles each
+  const mgrit_comm *comm = nullptr;                       // during mgrit_solve_shard
+  double *st_in = nullptr, *st_out = nullptr;
+  LoopState *lstate;      // graph mode: k, stop flags, tol
+  cudaGraphExec_t gexec = nullptr;   // cached loop graph (invalidated by setters)
+  long long glaunch[2] = {0, 0};     // kernels per captured iteration body (A, B)
+  cudaStream_t gstream = nullptr;    // private capture/launch stream (the caller's may be
+  cudaEvent_t gevent = nullptr;      //   the legacy default stream, which cannot capture)
   double *ucur, *unext;   // fine C-rows: current iterate / next (FCF ping-pong of u0b, v0b)
   const double *guess;
+  const double *rhs[MGRIT_MAX_LEVELS] = {nullptr};  // mgrit_set_rhs: g_l of level-l primitives
   bool have_iterate;   // u0b holds the iterate (after >= 1 iteration)
   std::string err;
   // profiling
@@ -515,6 +567,11 @@ struct mgrit_ctx {
 
 namespace {
 
+bool opt(const mgrit_ctx *c, int key, int need = 1) { return c->opt_n[key] >= need; }
+int stage_form(const mgrit_ctx *c) {
+  return opt(c, MGRIT_OPT_STAGE_FORM) ? c->opt_v[MGRIT_OPT_STAGE_FORM][0] : 0;
+}
+
 int fail(mgrit_ctx *c, int code, const char *fmt, ...) {
   char buf[512];
   va_list ap;
@@ -525,31 +582,49 @@ int fail(mgrit_ctx *c, int code, const char *fmt, ...) {
   return code;
 }
 
+// Status of an asynchronous runtime call (memcpy/memset on the context's stream): a
+// failure is reported where it happens, not at the next synchronisation.
+#define MG_CK(c, expr)                                                                     \
+  do {                                                                                     \
+    const cudaError_t e_ = (expr);                                                         \
+    if (e_ != cudaSuccess) return fail((c), MGRIT_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
 cudaEvent_t get_event(mgrit_ctx *c) {
   if (!c->evpool.empty()) {
     cudaEvent_t e = c->evpool.back();
     c->evpool.pop_back();
     return e;
   }
-  cudaEvent_t e;
-  cudaEventCreate(&e);
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
   return e;
 }
+
+// NVTX range (RAII): visible in Nsight Systems / ncu --nvtx; a no-op without a tool.
+struct Range {
+  explicit Range(const char *name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
+const char *const kClassName[MGRIT_PROF_CLASSES] = {"fine_sweep", "level_sweep", "coarse_solve",
+                                                    "interp", "residual", "other"};
 
 // Run a launch, counting it and (if profiling) bracketing it with events.
 template <class F>
 int run(mgrit_ctx *c, int cls, F &&f) {
+  Range nv(kClassName[cls]);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->prof) {
     e0 = get_event(c);
     e1 = get_event(c);
-    cudaEventRecord(e0, c->stream);
+    if (!e0 || !e1) return fail(c, MGRIT_ECUDA, "cudaEventCreate failed");
+    MG_CK(c, cudaEventRecord(e0, c->stream));
   }
   cudaError_t st = f();
   if (st != cudaSuccess) return fail(c, MGRIT_ECUDA, "kernel launch failed: %s", cudaGetErrorString(st));
   c->launches++;
   if (c->prof) {
-    cudaEventRecord(e1, c->stream);
+    MG_CK(c, cudaEventRecord(e1, c->stream));
     c->pending.push_back({cls, {e0, e1}});
   }
   return MGRIT_OK;
@@ -581,8 +656,10 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
   // SDIRK rows of 4096 points: 256 threads x 16 points (twice the work per scan and
   // barrier of 512 x 8; measured 1.02 vs 1.10 ms per cfg4 sweep)
   int cand[][2] = {{256, 16}, {512, 8}, {256, 8}, {128, 8}, {64, 8}, {32, 8}, {32, 4}, {32, 2}};
-  if (const char *env = getenv("MGRIT_WHOLE_ROW"))  // experiments: "NT,P" tried first
-    sscanf(env, "%d,%d", &cand[0][0], &cand[0][1]);
+  if (opt(c, MGRIT_OPT_WHOLE_ROW, 2)) {  // mgrit_set_option: (NT, P) tried first
+    cand[0][0] = c->opt_v[MGRIT_OPT_WHOLE_ROW][0];
+    cand[0][1] = c->opt_v[MGRIT_OPT_WHOLE_ROW][1];
+  }
   for (auto &cc : cand) {
     if (cc[0] * cc[1] == nx && rk_sweep_supported(c->scheme, {cc[0], cc[1]})) {
       f.cfg = {cc[0], cc[1]};
@@ -600,12 +677,10 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
   HL += HL & 1;
   const int HR = steps * S * rk_scheme_reach_right(c->scheme);
   int tcand[][3] = {{128, 15, 0}, {256, 11, 0}};
-  const char *env = steps == 2 * c->m ? getenv("MGRIT_FINE_TILE") : nullptr;
-  if (env) {  // experiments on the FCF sweep: "NT,P[,minBlocks]"
-    int nt_ = 0, p_ = 0, mb_ = 0;
-    if (sscanf(env, "%d,%d,%d", &nt_, &p_, &mb_) >= 2) {
-      tcand[0][0] = nt_; tcand[0][1] = p_; tcand[0][2] = mb_;
-    }
+  if (steps == 2 * c->m && opt(c, MGRIT_OPT_FINE_TILE, 2)) {  // FCF sweep: (NT, P[, minBlocks])
+    tcand[0][0] = c->opt_v[MGRIT_OPT_FINE_TILE][0];
+    tcand[0][1] = c->opt_v[MGRIT_OPT_FINE_TILE][1];
+    tcand[0][2] = c->opt_n[MGRIT_OPT_FINE_TILE] >= 3 ? c->opt_v[MGRIT_OPT_FINE_TILE][2] : 0;
   }
   for (auto &cc : tcand) {
     const int W = cc[0] * cc[1];
@@ -736,54 +811,63 @@ int reduce_norm(mgrit_ctx *c, long long n, double *norm2_host) {
 // Long chains (two-level): the row split over a thread-block cluster (DSMEM halos), else
 // one periodic CTA.
 struct CoarsePlan {
-  enum Kind { NONE, TILES, CLUSTER, CLUSTER_CA, SEQ } kind = NONE;
+  enum Kind { NONE, TILES, CLUSTER, CLUSTER_CA, SEQ, TILES_SEG } kind = NONE;
   SweepCfg cfg = {0, 0};
   int ntiles = 1, cl = 0, S = 0;
+  int seg = 0;       // TILES_SEG: steps per launch (trapezoid tiles, state row carried over)
+  bool tb = false;   // CLUSTER_CA: warp-specialised variant (psi_seq_cluster_tb_kernel)
 };
-// The warp-specialised variant of the CA cluster solve (psi_seq_cluster_tb_kernel)
-// applies when the window fits its register form (nu <= 32); the correction always
-// accumulates into the C-rows that hold v.  MGRIT_COARSE_KERNEL=ca selects the
-// per-thread cp.async variant (experiments).
-static bool coarse_tb(const mgrit_ctx *c, int l) {
-  const char *e = getenv("MGRIT_COARSE_KERNEL");
-  if (e && std::string(e) == "ca") return false;
-  return c->op[l].nu <= 32;
-}
 
 static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
   CoarsePlan pl;
   const PsiOp &op = c->op[l];
   const long long cone = c->ntl[l] * (long long)(op.nu - 1);
   PsiCfg pc;
-  if (cone <= 2048 && c->nx >= 2048 && choose_psi(c->nx, (int)cone, false, pc)) {
+  // trapezoid tiles of the coarse kernel: 256 x 8 windows (the 512 x 8 ring exceeds the
+  // shared memory of one SM), so the cone must leave >= 128 outputs of 2048
+  if (cone <= 2048 - 128 && c->nx >= 2048 && choose_psi(c->nx, (int)cone, false, pc)) {
     pl.kind = CoarsePlan::TILES;
     pl.cfg = pc.cfg;
     pl.ntiles = pc.ntiles;
     return pl;
   }
-  if (!(choose_psi(c->nx, 0, true, pc) && pc.ntiles == 1 && pc.cfg.nt_threads * pc.cfg.p == c->nx))
-    return pl;
+  const bool whole = choose_psi(c->nx, 0, true, pc) && pc.ntiles == 1 &&
+                     pc.cfg.nt_threads * pc.cfg.p == c->nx;
   // 16-CTA clusters (measured with tools/probe_cfgs.sh): the warp-
   // specialised kernel (nu <= 32) prefers 4 points per thread at nx = 4096 (half the
   // shared-memory window loads per output) and deeper s-steps; the cp.async variant
-  // (wider stencils) keeps 2 points per thread and depth 4 for wide stencils.
-  const bool tb = coarse_tb(c, l);
+  // (wider stencils) keeps 2 points per thread and depth 4 for wide stencils.  Rows wider
+  // than one CTA can hold (nx = 8192, 16384) are split 16 ways as well (512 / 1024 points
+  // per SM; the warp-specialised ring does not fit 1024-point slices in shared memory).
+  const bool want_tb = op.nu <= 32 && !(opt(c, MGRIT_OPT_COARSE_KERNEL) &&
+                                        c->opt_v[MGRIT_OPT_COARSE_KERNEL][0] == 1);
   int cl = 0, smax = 8;
   SweepCfg cc = {0, 0};
   if (c->nx == 4096) {
     cl = 16;
-    cc = (op.nu <= 16 || tb) ? SweepCfg{64, 4} : SweepCfg{128, 2};
-    smax = op.nu <= 16 ? 8 : (tb ? 6 : 4);
+    cc = (op.nu <= 16 || want_tb) ? SweepCfg{64, 4} : SweepCfg{128, 2};
+    smax = op.nu <= 16 ? 8 : (want_tb ? 6 : 4);
   } else if (c->nx == 1024) {
     cl = 16;
     cc = {32, 2};
-    smax = tb ? 12 : 8;
+    smax = want_tb ? 12 : 8;
+  } else if (c->nx == 2048) {
+    cl = 16;
+    cc = {64, 2};
+  } else if (c->nx == 8192) {
+    cl = 16;
+    cc = {128, 4};
+    smax = 6;
+  } else if (c->nx == 16384) {
+    cl = 16;
+    cc = {256, 4};
+    smax = 6;
   }
-  if (const char *env = getenv("MGRIT_SEQ_CLUSTER")) {
-    cl = 0;
-    sscanf(env, "%d,%d,%d", &cl, &cc.nt_threads, &cc.p);
+  if (opt(c, MGRIT_OPT_SEQ_CLUSTER, 3)) {
+    cl = c->opt_v[MGRIT_OPT_SEQ_CLUSTER][0];
+    cc = {c->opt_v[MGRIT_OPT_SEQ_CLUSTER][1], c->opt_v[MGRIT_OPT_SEQ_CLUSTER][2]};
   }
-  if (const char *env = getenv("MGRIT_SEQ_S")) smax = atoi(env);
+  if (opt(c, MGRIT_OPT_SEQ_S)) smax = c->opt_v[MGRIT_OPT_SEQ_S][0];
   if (smax >= 2) {
     const int S = seq_ca_depth(cl, cc, c->nx, op.o0, op.nu, smax);
     if (S >= 2) {
@@ -791,6 +875,7 @@ static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
       pl.cfg = cc;
       pl.cl = cl;
       pl.S = S;
+      pl.tb = want_tb && seq_cluster_tb_supported(cl, cc);
       return pl;
     }
   }
@@ -800,16 +885,33 @@ static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
     pl.cl = cl;
     return pl;
   }
+  if (!whole) {
+    // any other width: the chain in segments of `seg` steps whose trapezoid cone fits a
+    // 4096- (or 2048-) point window; the state row x_n is carried between launches
+    for (const int W : {2048}) {
+      if (W > c->nx) continue;
+      const int seg = (W - 128) / std::max(1, op.nu - 1);
+      if (seg < 1) continue;
+      if (!choose_psi(c->nx, seg * (op.nu - 1), false, pc)) continue;
+      pl.kind = CoarsePlan::TILES_SEG;
+      pl.cfg = pc.cfg;
+      pl.ntiles = pc.ntiles;
+      pl.seg = (int)std::min<long long>(seg, c->ntl[l]);
+      return pl;
+    }
+    return pl;
+  }
   SweepCfg sc = pc.cfg;  // more threads per row for the latency-bound chain
   if (c->nx == 4096) sc = {1024, 4};
   else if (c->nx == 1024) sc = {256, 4};
-  if (const char *env = getenv("MGRIT_SEQ_CFG")) sscanf(env, "%d,%d", &sc.nt_threads, &sc.p);
+  if (opt(c, MGRIT_OPT_SEQ_CFG, 2)) sc = {c->opt_v[MGRIT_OPT_SEQ_CFG][0], c->opt_v[MGRIT_OPT_SEQ_CFG][1]};
   pl.kind = CoarsePlan::SEQ;
   pl.cfg = sc;
   return pl;
 }
 
-int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
+int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
+                       const double *state_in = nullptr, double *state_out = nullptr) {
   const long long N = c->ntl[l];
   if (c->psi_kind != MGRIT_PSI_STENCIL) {
     RKCoarseArgs a;
@@ -824,7 +926,7 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
     a.sd = c->coarse_sd;
     SweepCfg cfg;
     if (!rk_coarse_cfg(c->nx, cfg))
-      return fail(c, MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,256,1024}");
+      return fail(c, MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,...,4096}");
     return run(c, 2, [&] { return launch_rk_coarse(c->scheme, cfg, a, c->stream); });
   }
   const CoarsePlan pl = plan_coarse(c, l);
@@ -838,18 +940,32 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
   a.n0 = 0;
   a.g = rm(c->g[l], 0, 1);
   a.out = out;
-  a.state_in = nullptr;
-  a.state_out = nullptr;
+  a.state_in = state_in;
+  a.state_out = state_out;
   a.op = c->op[l];
   switch (pl.kind) {
     case CoarsePlan::CLUSTER:
       return run(c, 2, [&] { return launch_psi_seq_cluster(pl.cl, pl.cfg, a, c->stream); });
     case CoarsePlan::CLUSTER_CA:
-      if (coarse_tb(c, l))
+      if (pl.tb)
         return run(c, 2, [&] { return launch_psi_seq_cluster_tb(pl.cl, pl.cfg, pl.S, a, c->stream); });
       return run(c, 2, [&] { return launch_psi_seq_cluster_ca(pl.cl, pl.cfg, pl.S, a, c->stream); });
     case CoarsePlan::SEQ:
       return run(c, 2, [&] { return launch_psi_seq_periodic(pl.cfg, a, c->stream); });
+    case CoarsePlan::TILES_SEG: {
+      // segments n0 = 0, seg, 2 seg, ...: x_{n0} in / x_{n0+seg} out through sa / sb
+      double *st[2] = {c->sa, c->sb};
+      int k = 0;
+      for (long long n0 = 0; n0 < N; n0 += pl.seg, ++k) {
+        a.n0 = n0;
+        a.nsteps = (int)std::min<long long>(pl.seg, N - n0);
+        a.state_in = n0 == 0 ? state_in : st[(k + 1) & 1];
+        a.state_out = n0 + a.nsteps < N ? st[k & 1] : state_out;
+        const int s = run(c, 2, [&] { return launch_psi_coarse(pl.cfg, a, c->stream); });
+        if (s) return s;
+      }
+      return MGRIT_OK;
+    }
     default:
       return run(c, 2, [&] { return launch_psi_coarse(pl.cfg, a, c->stream); });
   }
@@ -859,6 +975,13 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out) {
 // v_l rows 1..nc, g_{l+1} rows 2..nc.
 // uin: C-rows of a nonzero level-l iterate (F-cycle's second visit), null: zero guess;
 // the FCF C-rows v go to vout rows 1..nc, r_{j+2} = Psi^m delta to g_{l+1} rows 2..nc.
+// Phase 2 (the coarse right-hand side r_{j+2}) of the last interval: the global problem has
+// no C-point nc+1, but a time shard that is not the last one computes its right
+// neighbour's first coarse RHS row into the outbox row nc+1 of g_{l+1}.
+int p2_count(const mgrit_ctx *c, long long nc) {
+  return (int)(c->rank < c->nranks - 1 ? nc : nc - 1);
+}
+
 int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout) {
   const PsiOp &op = c->op[l];
   const int m = c->m;
@@ -879,7 +1002,7 @@ int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout) {
   a.g = rm(c->g[l], 0, m);
   a.v = rm(vout, 1, 1);   // v_{j+1} is the uncorrected C-row; the coarse levels add E
   a.r2 = rm(c->g[l + 1], 2, 1);
-  a.p2_items = (int)nc - 1;
+  a.p2_items = p2_count(c, nc);
   a.v2 = a.out2 = kNone;
   a.op = op;
   if (tma) return run(c, 1, [&] { return launch_psi_level_tma(pc.cfg, a, c->stream); });
@@ -931,6 +1054,9 @@ int level_interp(mgrit_ctx *c, int l, const double *usrc_rows, RowMap out_prev) 
 //      cycle_V(l+1) -> u2[l]; interp(l) from u2[l] -> dst               (R19)
 // The coarsest level is the sequential solve (its F- and V-visits coincide).
 int level_cycle(mgrit_ctx *c, int l, bool fcyc, RowMap dst) {
+  static const char *const kLevel[MGRIT_MAX_LEVELS] = {"level 0", "level 1", "level 2", "level 3",
+                                                       "level 4", "level 5", "level 6", "level 7"};
+  Range nv(kLevel[l]);
   const int L = c->levels;
   if (l == L - 1) return coarse_solve_level(c, l, dst, dst);
   int st = level_sweep(c, l, nullptr, c->ul[l]);
@@ -953,7 +1079,220 @@ int coarse_correction(mgrit_ctx *c, RowMap out0) {
   return level_cycle(c, 1, c->cycle == MGRIT_CYCLE_F, out0);
 }
 
+// ---- level >= 1 FULL-state primitives (levels.cu) ----------------------------------
+int level_check(mgrit_ctx *c, int level, bool need_coarser) {
+  if (level < 1 || level >= c->levels || (need_coarser && level + 1 >= c->levels))
+    return fail(c, MGRIT_EINVAL, "level %d out of range for %d levels", level, c->levels);
+  if (c->psi_kind != MGRIT_PSI_STENCIL)
+    return fail(c, MGRIT_EUNSUPPORTED, "level >= 1 primitives need stencil Psi operators");
+  if (c->ntl[level] % c->m)
+    return fail(c, MGRIT_EINVAL, "level %d has nt = %lld, not a multiple of m", level, c->ntl[level]);
+  return MGRIT_OK;
+}
+
+RowStepArgs rowstep(const mgrit_ctx *c, int level, const double *U) {
+  RowStepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nx = c->nx;
+  a.bpr = std::max(1, std::min(64, (c->nx + 1023) / 1024));
+  a.U = U;
+  a.dst = const_cast<double *>(U);
+  a.g = c->rhs[level];
+  a.op = c->op[level];
+  return a;
+}
+
+// F- (positions i = 1..m-1) or C-relaxation (position m) of a level-l FULL array.
+int level_relax_rows(mgrit_ctx *c, int level, double *U, int i_first, int i_last) {
+  const int m = c->m;
+  const long long nc = c->ntl[level] / m;
+  for (int i = i_first; i <= i_last; ++i) {
+    RowStepArgs a = rowstep(c, level, U);
+    a.mode = 0;
+    a.n0 = i;
+    a.nstride = m;
+    a.nrows = (int)nc;
+    int st = run(c, 1, [&] { return launch_psi_rowstep(a, c->stream); });
+    if (st) return st;
+  }
+  return MGRIT_OK;
+}
+
+
+// ---- CUDA-graph loop (graph.cu) --------------------------------------------------------
+void drop_graph(mgrit_ctx *c) {
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->gexec = nullptr;
+}
+
+// Leaf nodes (no dependents) of a graph: the dependencies of a node appended after it.
+std::vector<cudaGraphNode_t> graph_leaves(cudaGraph_t g) {
+  size_t n = 0;
+  cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n), leaves;
+  if (n) cudaGraphGetNodes(g, nodes.data(), &n);
+  for (auto nd : nodes) {
+    size_t d = 0;
+    cudaGraphNodeGetDependentNodes(nd, nullptr, &d);
+    if (d == 0) leaves.push_back(nd);
+  }
+  return leaves;
+}
+
+// Capture `body` followed by the decide kernel into graph `g` (appended to its nodes).
+template <class F>
+int capture_into(mgrit_ctx *c, cudaGraph_t g, F &&body, cudaGraphConditionalHandle h0,
+                 cudaGraphConditionalHandle h1, int set_h1, long long &nlaunch) {
+  MG_CK(c, cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+  const long long l0 = c->launches;
+  int st = body();
+  if (!st) {
+    const cudaError_t e = launch_loop_decide(c->lstate, c->scal, c->hist_dev, h0, h1, set_h1,
+                                             c->stream);
+    if (e != cudaSuccess) st = fail(c, MGRIT_ECUDA, "decide: %s", cudaGetErrorString(e));
+  }
+  nlaunch = c->launches - l0 + 1;
+  c->launches = l0;                       // counted per executed iteration instead
+  cudaGraph_t out = g;
+  const cudaError_t e = cudaStreamEndCapture(c->stream, &out);
+  if (st) return st;
+  if (e != cudaSuccess) return fail(c, MGRIT_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  return MGRIT_OK;
+}
+
+// WHILE(h_w) { A; decide -> h_w, h_i; IF(h_i) { B; decide -> h_w } } for FCF (A and B are
+// the two buffer parities of the C-row ping-pong), WHILE(h_w) { A; decide } for F.
+template <class F>
+int build_loop_graph(mgrit_ctx *c, bool fcf, F &&iteration) {
+  cudaGraph_t g = nullptr;
+  MG_CK(c, cudaGraphCreate(&g, 0));
+  auto cleanup = [&](int st) {
+    cudaGraphDestroy(g);
+    return st;
+  };
+  cudaGraphConditionalHandle hw, hi = 0;
+  if (cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+    return cleanup(fail(c, MGRIT_ECUDA, "conditional handle"));
+  alignas(cudaGraphNodeParams) unsigned char wbuf[sizeof(cudaGraphNodeParams)];
+  std::memset(wbuf, 0, sizeof(wbuf));
+  cudaGraphNodeParams &wp = *reinterpret_cast<cudaGraphNodeParams *>(wbuf);
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  if (cudaGraphAddNode(&wn, g, nullptr, 0, &wp) != cudaSuccess)
+    return cleanup(fail(c, MGRIT_ECUDA, "while node"));
+  cudaGraph_t bw = wp.conditional.phGraph_out[0];
+  if (fcf && cudaGraphConditionalHandleCreate(&hi, bw, 0, cudaGraphCondAssignDefault) != cudaSuccess)
+    return cleanup(fail(c, MGRIT_ECUDA, "conditional handle"));
+  int st = capture_into(c, bw, iteration, hw, hi, fcf ? 1 : 0, c->glaunch[0]);
+  if (st) return cleanup(st);
+  c->glaunch[1] = 0;
+  if (fcf) {
+    std::vector<cudaGraphNode_t> deps = graph_leaves(bw);
+    alignas(cudaGraphNodeParams) unsigned char ibuf[sizeof(cudaGraphNodeParams)];
+    std::memset(ibuf, 0, sizeof(ibuf));
+    cudaGraphNodeParams &ip = *reinterpret_cast<cudaGraphNodeParams *>(ibuf);
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hi;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t in;
+    if (cudaGraphAddNode(&in, bw, deps.data(), deps.size(), &ip) != cudaSuccess)
+      return cleanup(fail(c, MGRIT_ECUDA, "if node"));
+    st = capture_into(c, ip.conditional.phGraph_out[0], iteration, hw, hw, 0, c->glaunch[1]);
+    if (st) return cleanup(st);
+  }
+  const cudaError_t e = cudaGraphInstantiate(&c->gexec, g, 0);
+  if (e != cudaSuccess) {
+    c->gexec = nullptr;
+    return cleanup(fail(c, MGRIT_ECUDA, "graph instantiate: %s", cudaGetErrorString(e)));
+  }
+  return cleanup(MGRIT_OK);
+}
+
+
+// ---- time shards (mgrit_setup_shard / mgrit_solve_shard) ------------------------------
+double *row_ptr(const mgrit_ctx *c, double *base, long long r) { return base + r * (long long)c->nx; }
+
+// Neighbour exchange through the staging rows: send_row -> rank+1, rank-1 -> recv_row.
+int comm_shift(mgrit_ctx *c, const double *send_row, double *recv_row) {
+  if (c->nranks == 1) return MGRIT_OK;
+  const bool hs = send_row && c->rank < c->nranks - 1;
+  const bool hr = recv_row && c->rank > 0;
+  const size_t row = (size_t)c->nx * sizeof(double);
+  if (hs) MG_CK(c, cudaMemcpyAsync(c->stage_send, send_row, row, cudaMemcpyDeviceToDevice, c->stream));
+  if (c->comm->shift(c->comm->user, hs ? 1 : 0, hr ? 1 : 0, c->stream))
+    return fail(c, MGRIT_ECOMM, "mgrit_comm.shift failed (rank %d)", c->rank);
+  if (hr) MG_CK(c, cudaMemcpyAsync(recv_row, c->stage_recv, row, cudaMemcpyDeviceToDevice, c->stream));
+  return MGRIT_OK;
+}
+
+int comm_sum(mgrit_ctx *c, double *v, int n) {
+  if (c->nranks == 1) return MGRIT_OK;
+  if (c->comm->allreduce_sum(c->comm->user, v, n))
+    return fail(c, MGRIT_ECOMM, "mgrit_comm.allreduce_sum failed (rank %d)", c->rank);
+  return MGRIT_OK;
+}
+
+// V-cycle on level l of a time shard (zero initial guess, RHS g_l; result added to dst,
+// the level-(l-1) C-rows).  As level_cycle, plus: the right neighbour's first coarse RHS
+// row after the sweep, the corrected C-row at the block start before the interpolation,
+// and the coarsest chain's state rank -> rank+1.
+int level_cycle_shard(mgrit_ctx *c, int l, RowMap dst) {
+  const int L = c->levels;
+  const bool first = c->rank == 0, last = c->rank == c->nranks - 1;
+  if (l == L - 1) {
+    int st = first ? MGRIT_OK : comm_shift(c, nullptr, c->st_in);
+    if (st) return st;
+    st = coarse_solve_level(c, l, dst, dst, first ? nullptr : c->st_in, last ? nullptr : c->st_out);
+    if (st) return st;
+    return last ? MGRIT_OK : comm_shift(c, c->st_out, nullptr);
+  }
+  const long long nc = c->ntl[l] / c->m;
+  int st = level_sweep(c, l, nullptr, c->ul[l]);
+  if (st) return st;
+  st = comm_shift(c, row_ptr(c, c->g[l + 1], nc + 1), row_ptr(c, c->g[l + 1], 1));
+  if (st) return st;
+  st = level_cycle_shard(c, l + 1, rm(c->ul[l], 0, 1));
+  if (st) return st;
+  st = comm_shift(c, row_ptr(c, c->ul[l], nc), row_ptr(c, c->ul[l], 0));
+  if (st) return st;
+  return level_interp(c, l, c->ul[l], dst);
+}
+
+
 }  // namespace
+
+// Factored SDIRK stage solves (sdirk.cuh) of the fine step and, for an RK-form Psi, of the
+// coarse step (Phi at CFL m*c or Phi^m).  Depends on the whole-row configuration
+// (points per thread) and on MGRIT_OPT_SDIRK_PRODUCT, so mgrit_set_option re-runs it.
+int setup_sdirk(mgrit_ctx *c, std::string &why) {
+  std::memset(&c->sd, 0, sizeof(c->sd));
+  std::memset(&c->coarse_sd, 0, sizeof(c->coarse_sd));
+  if (!c->implicit) return MGRIT_OK;
+  const bool fused = !(opt(c, MGRIT_OPT_SDIRK_PRODUCT) && c->opt_v[MGRIT_OPT_SDIRK_PRODUCT][0] == 1);
+  FineCfg f;
+  if (!choose_fine(c, 1, f)) {
+    why = "SDIRK needs nx in {64,128,256,...,4096} (whole-row CTAs)";
+    return MGRIT_EUNSUPPORTED;
+  }
+  if (!make_sdirk(c->fine.z, c->zlo, c->zn, c->tab.A[0][0], f.cfg.p, c->nx, c->sd, why, fused))
+    return MGRIT_EUNSUPPORTED;
+  if (c->psi_kind != MGRIT_PSI_STENCIL) {
+    SweepCfg rc;
+    if (!rk_coarse_cfg(c->nx, rc)) {
+      why = "RK-form Psi supports nx in {64,128,...,4096}";
+      return MGRIT_EUNSUPPORTED;
+    }
+    if (!make_sdirk(c->coarse_rk.z, c->zlo, c->zn, c->tab.A[0][0], rc.p, c->nx, c->coarse_sd, why,
+                    fused))
+      return MGRIT_EUNSUPPORTED;
+  }
+  return MGRIT_OK;
+}
 
 __global__ void mg_add_rows_kernel(double *dst, const double *a, const double *b, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -1020,18 +1359,7 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
     c->fine.mdiag[i] = c->tab.A[i][i];
     for (int j = 0; j < MAXS; ++j) c->fine.A[i][j] = c->tab.A[i][j];
   }
-  fold_last_stage(c->fine, c->tab.s);
-  std::memset(&c->sd, 0, sizeof(c->sd));
-  if (c->implicit) {
-    FineCfg f;
-    if (!choose_fine(c, 1, f)) return bad(MGRIT_EUNSUPPORTED, "SDIRK needs nx in {64,128,256,...,4096} (whole-row CTAs)");
-    std::string why;
-    const char *prod = getenv("MGRIT_SDIRK_PRODUCT");  // experiments/tests: product form only
-    if (!make_sdirk(c->fine.z, c->zlo, c->zn, c->tab.A[0][0], f.cfg.p, nx, c->sd, why,
-                    !(prod && atoi(prod))))
-      return bad(MGRIT_EUNSUPPORTED, why.c_str());
-
-  }
+  fold_last_stage(c->fine, c->tab.s, stage_form(c));
   // coarse operators
   c->psi_kind = psi[0].kind;
   for (int l = 1; l < levels; ++l) {
@@ -1060,22 +1388,18 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
       } else if (p.kind == MGRIT_PSI_REDISC) {
         int zlo, zn;
         make_z(order, p.redisc_cfl, c->coarse_rk.z, &zlo, &zn);
-        fold_last_stage(c->coarse_rk, c->tab.s);
+        fold_last_stage(c->coarse_rk, c->tab.s, stage_form(c));
         c->coarse_q = 1;
         c->redisc_cfl = p.redisc_cfl;
       } else {
         return bad(MGRIT_EINVAL, "unknown Psi kind");
       }
-      if (c->implicit) {  // the coarse SDIRK step's stage solve (Phi at CFL m*c or Phi^m)
-        SweepCfg rc;
-        if (!rk_coarse_cfg(nx, rc)) return bad(MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,256,1024}");
-        std::string why;
-        const char *prod = getenv("MGRIT_SDIRK_PRODUCT");
-        if (!make_sdirk(c->coarse_rk.z, c->zlo, c->zn, c->tab.A[0][0], rc.p, nx, c->coarse_sd, why,
-                        !(prod && atoi(prod))))
-          return bad(MGRIT_EUNSUPPORTED, why.c_str());
-      }
     }
+  }
+  {
+    std::string why;
+    const int st = setup_sdirk(c, why);
+    if (st) return bad(st, why.c_str());
   }
   // carve the workspace
   c->ws = (char *)workspace_dev;
@@ -1092,19 +1416,20 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
   c->scal = (double *)(c->ws + c->lay.scal);
   c->sa = (double *)(c->ws + c->lay.sa);
   c->sb = (double *)(c->ws + c->lay.sb);
+  c->hist_dev = (double *)(c->ws + c->lay.hist);
+  c->st_in = (double *)(c->ws + c->lay.st_in);
+  c->st_out = (double *)(c->ws + c->lay.st_out);
+  c->lstate = (LoopState *)(c->ws + c->lay.lstate);
   c->guess = nullptr;
   c->have_iterate = false;
   // constant rows: g_l rows 0 and 1 (r_1 = 0), coarse v_l/u_l row 0
   const size_t row = (size_t)nx * sizeof(double);
   for (int l = 1; l < levels; ++l) {
-    cudaMemsetAsync(c->g[l], 0, 2 * row, c->stream);
-    if (l < levels - 1) {
-      cudaMemsetAsync(c->ul[l], 0, row, c->stream);
-      cudaMemsetAsync(c->u2[l], 0, row, c->stream);
-    }
+    cudaError_t e = cudaMemsetAsync(c->g[l], 0, 2 * row, c->stream);
+    if (e == cudaSuccess && l < levels - 1) e = cudaMemsetAsync(c->ul[l], 0, row, c->stream);
+    if (e == cudaSuccess && l < levels - 1) e = cudaMemsetAsync(c->u2[l], 0, row, c->stream);
+    if (e != cudaSuccess) return bad(MGRIT_ECUDA, cudaGetErrorString(e));
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return bad(MGRIT_ECUDA, cudaGetErrorString(e));
   *out = c;
   return MGRIT_OK;
 }
@@ -1116,6 +1441,9 @@ void mgrit_destroy(mgrit_ctx *c) {
     cudaEventDestroy(p.second.second);
   }
   for (auto e : c->evpool) cudaEventDestroy(e);
+  drop_graph(c);
+  if (c->gevent) cudaEventDestroy(c->gevent);
+  if (c->gstream) cudaStreamDestroy(c->gstream);
   delete c;
 }
 
@@ -1155,9 +1483,26 @@ int mgrit_set_guess(mgrit_ctx *c, const double *guess_dev) {
   return MGRIT_OK;
 }
 
+int mgrit_set_rhs(mgrit_ctx *c, int level, const double *g_dev) {
+  if (!c) return MGRIT_EINVAL;
+  if (level < 1 || level >= c->levels) return fail(c, MGRIT_EINVAL, "rhs level %d out of range", level);
+  c->rhs[level] = g_dev;
+  return MGRIT_OK;
+}
+
 int mgrit_relax(mgrit_ctx *c, int level, int kind, double *U) {
   if (!c || !U) return MGRIT_EINVAL;
-  if (level != 0) return fail(c, MGRIT_EUNSUPPORTED, "FULL primitives are level 0 only");
+  if (kind != MGRIT_RELAX_F && kind != MGRIT_RELAX_C && kind != MGRIT_RELAX_FCF)
+    return fail(c, MGRIT_EINVAL, "relax kind");
+  if (level != 0) {  // Phi_l = Psi_l with RHS g_l (P:206 on level l; R12)
+    int st = level_check(c, level, false);
+    if (st) return st;
+    const int m = c->m;
+    if (kind != MGRIT_RELAX_C) st = level_relax_rows(c, level, U, 1, m - 1);
+    if (!st && kind != MGRIT_RELAX_F) st = level_relax_rows(c, level, U, m, m);
+    if (!st && kind == MGRIT_RELAX_FCF) st = level_relax_rows(c, level, U, 1, m - 1);
+    return st;
+  }
   const int m = c->m;
   const long long nc = c->nt / m;
   auto frelax = [&]() {
@@ -1193,9 +1538,9 @@ int mgrit_relax(mgrit_ctx *c, int level, int kind, double *U) {
 // Rows per work item of the streaming all-row residual kernel.
 constexpr int kResidualChunk = 64;
 
-int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, double *r_dev) {
-  if (!c || !U) return MGRIT_EINVAL;
-  if (level != 0) return fail(c, MGRIT_EUNSUPPORTED, "FULL primitives are level 0 only");
+// Level-0 all-row residual: sum of squares over rows 1..nt (n2_host, nullable: no
+// readback) and, if r_dev, the C-point residuals.
+static int residual0(mgrit_ctx *c, const double *U, double *n2_host, double *r_dev) {
   FineCfg f;
   if (!r_dev && choose_fine(c, 1, f) && f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1)) {
     // norm only: streaming kernel, every row loaded once
@@ -1212,11 +1557,7 @@ int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, 
       return launch_rk_residual_tma(c->scheme, f.cfg, a, kResidualChunk, c->stream);
     });
     if (st) return st;
-    double n2 = 0;
-    st = reduce_norm(c, np, norm_host ? &n2 : nullptr);
-    if (st) return st;
-    if (norm_host) *norm_host = std::sqrt(c->dx * c->dt * n2);
-    return MGRIT_OK;
+    return reduce_norm(c, np, n2_host);
   }
   SweepArgs a = base_sweep(c);
   a.nitems = c->nt;
@@ -1225,15 +1566,56 @@ int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, 
   a.cmp = rm(U, 1, 1);
   a.partials = c->partials;
   if (r_dev) {
-    cudaMemsetAsync(r_dev, 0, (size_t)c->nx * sizeof(double), c->stream);
+    MG_CK(c, cudaMemsetAsync(r_dev, 0, (size_t)c->nx * sizeof(double), c->stream));
     a.dstore = rm(r_dev, 0, 1);
     a.d_every = c->m;
     a.d_phase = 1;
   }
   int st = sweep(c, 4, a, 1);
   if (st) return st;
+  return reduce_norm(c, partial_count(c, c->nt, 1), n2_host);
+}
+
+
+int mgrit_residual(mgrit_ctx *c, int level, const double *U, double *norm_host, double *r_dev) {
+  if (!c || !U) return MGRIT_EINVAL;
+  if (level != 0) {  // r[n] = g[n] + Psi U[n-1] - U[n], n = 1..nt_l; dt_l = m^l dt
+    int st = level_check(c, level, false);
+    if (st) return st;
+    const long long ntl = c->ntl[level];
+    RowStepArgs a = rowstep(c, level, U);
+    a.mode = 1;
+    a.n0 = 1;
+    a.nstride = 1;
+    a.nrows = (int)ntl;
+    a.partials = c->partials;
+    const long long np = ntl * a.bpr;
+    if (np > c->lay.npart) return fail(c, MGRIT_ENOMEM, "partials buffer too small");
+    st = run(c, 4, [&] { return launch_psi_rowstep(a, c->stream); });
+    if (st) return st;
+    double n2 = 0;
+    st = reduce_norm(c, np, norm_host ? &n2 : nullptr);
+    if (st) return st;
+    if (norm_host) {
+      double dtl = c->dt;
+      for (int l = 0; l < level; ++l) dtl *= c->m;
+      *norm_host = std::sqrt(c->dx * dtl * n2);
+    }
+    if (r_dev) {  // C-point residuals r_j = g[jm] + Psi U[jm-1] - U[jm], r_0 = 0
+      MG_CK(c, cudaMemsetAsync(r_dev, 0, (size_t)c->nx * sizeof(double), c->stream));
+      RowStepArgs b = rowstep(c, level, U);
+      b.mode = 1;
+      b.n0 = c->m;
+      b.nstride = c->m;
+      b.nrows = (int)(ntl / c->m);
+      b.rstore = r_dev;
+      b.roff = 1;
+      st = run(c, 4, [&] { return launch_psi_rowstep(b, c->stream); });
+    }
+    return st;
+  }
   double n2 = 0;
-  st = reduce_norm(c, partial_count(c, c->nt, 1), norm_host ? &n2 : nullptr);
+  const int st = residual0(c, U, norm_host ? &n2 : nullptr, r_dev);
   if (st) return st;
   if (norm_host) *norm_host = std::sqrt(c->dx * c->dt * n2);
   return MGRIT_OK;
@@ -1247,17 +1629,80 @@ int mgrit_set_final_sweep(mgrit_ctx *c, int mode) {
   return MGRIT_OK;
 }
 
+int mgrit_set_option(mgrit_ctx *c, int option, const int *values, int n) {
+  if (!c) return MGRIT_EINVAL;
+  static const int kMin[MGRIT_OPT_COUNT] = {2, 2, 3, 1, 1, 2, 1, 1, 1};
+  static const int kMax[MGRIT_OPT_COUNT] = {3, 2, 3, 1, 1, 2, 1, 1, 1};
+  if (option < 0 || option >= MGRIT_OPT_COUNT) return fail(c, MGRIT_EINVAL, "unknown option %d", option);
+  if (n != 0 && (n < kMin[option] || n > kMax[option] || !values))
+    return fail(c, MGRIT_EINVAL, "option %d takes %d..%d values", option, kMin[option], kMax[option]);
+  for (int i = 0; i < n; ++i)
+    if (values[i] < 0) return fail(c, MGRIT_EINVAL, "option %d: negative value", option);
+  if ((option == MGRIT_OPT_COARSE_KERNEL || option == MGRIT_OPT_SDIRK_PRODUCT ||
+       option == MGRIT_OPT_GRAPH) && n && values[0] > 1)
+    return fail(c, MGRIT_EINVAL, "option %d takes 0 or 1", option);
+  if (option == MGRIT_OPT_STAGE_FORM && n && values[0] > 4)
+    return fail(c, MGRIT_EINVAL, "option %d takes 0 or 1", option);
+  const int old_n = c->opt_n[option];
+  int old_v[4];
+  std::memcpy(old_v, c->opt_v[option], sizeof(old_v));
+  drop_graph(c);
+  c->opt_n[option] = n;
+  for (int i = 0; i < 4; ++i) c->opt_v[option][i] = i < n ? values[i] : 0;
+  if (option == MGRIT_OPT_STAGE_FORM) {  // re-derive the step coefficients in the new form
+    fold_last_stage(c->fine, c->tab.s, stage_form(c));
+    if (c->psi_kind != MGRIT_PSI_STENCIL) {
+      if (c->coarse_q == 1) {  // REDISC: own z at the coarse CFL
+        int zlo, zn;
+        make_z(c->order, c->redisc_cfl, c->coarse_rk.z, &zlo, &zn);
+      } else {
+        std::memcpy(c->coarse_rk.z, c->fine.z, sizeof(c->fine.z));
+      }
+      fold_last_stage(c->coarse_rk, c->tab.s, stage_form(c));
+    }
+  }
+  if (option == MGRIT_OPT_WHOLE_ROW || option == MGRIT_OPT_SDIRK_PRODUCT) {
+    std::string why;
+    const int st = setup_sdirk(c, why);
+    if (st) {  // restore the previous (valid) state
+      c->opt_n[option] = old_n;
+      std::memcpy(c->opt_v[option], old_v, sizeof(old_v));
+      std::string why2;
+      setup_sdirk(c, why2);
+      return fail(c, st, "%s", why.c_str());
+    }
+  }
+  return MGRIT_OK;
+}
+
 int mgrit_set_cycle(mgrit_ctx *c, int cycle) {
   if (!c) return MGRIT_EINVAL;
   if (cycle != MGRIT_CYCLE_V && cycle != MGRIT_CYCLE_F) return fail(c, MGRIT_EINVAL, "cycle must be V or F");
+  drop_graph(c);
   c->cycle = cycle;
   return MGRIT_OK;
 }
 
 int mgrit_coarse_solve(mgrit_ctx *c, int level, double *U) {
   if (!c || !U) return MGRIT_EINVAL;
-  if (level != 0 || c->levels != 2)
-    return fail(c, MGRIT_EUNSUPPORTED, "FULL coarse_solve is two-level, level 0 only");
+  if (level != 0) {  // level l: r_j -> g_{l+1}; e = sequential Psi_{l+1} solve; U[jm] += e_j; F
+    int st = level_check(c, level, true);
+    if (st) return st;
+    RowStepArgs a = rowstep(c, level, U);
+    a.mode = 1;
+    a.n0 = c->m;
+    a.nstride = c->m;
+    a.nrows = (int)(c->ntl[level] / c->m);
+    a.rstore = c->g[level + 1];
+    a.roff = 1;
+    st = run(c, 4, [&] { return launch_psi_rowstep(a, c->stream); });
+    if (st) return st;
+    st = coarse_solve_level(c, level + 1, rm(U, 0, c->m), rm(U, 0, c->m));
+    if (st) return st;
+    return mgrit_relax(c, level, MGRIT_RELAX_F, U);
+  }
+  if (c->psi_kind != MGRIT_PSI_STENCIL && c->levels != 2)
+    return fail(c, MGRIT_EUNSUPPORTED, "RK-form Psi: two levels only");
   const int m = c->m;
   const long long nc = c->nt / m;
   // r_j = Phi U[jm-1] - U[jm], j = 1..nc  -> g_1 rows 1..nc
@@ -1281,6 +1726,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   if (!c) return MGRIT_EINVAL;
   if (!c->guess) return fail(c, MGRIT_EINVAL, "mgrit_set_guess first");
   if (max_iter < 0) return fail(c, MGRIT_EINVAL, "max_iter < 0");
+  Range nv_solve("mgrit_solve");
   const int m = c->m, nx = c->nx;
   const long long nc = c->nt / m;
   const size_t row = (size_t)nx * sizeof(double);
@@ -1289,16 +1735,16 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   // row 0 of the C-row buffers = u0
   c->ucur = c->u0b;
   c->unext = c->v0b;
-  cudaMemcpyAsync(c->u0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream);
-  cudaMemcpyAsync(c->v0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream);
+  MG_CK(c, cudaMemcpyAsync(c->u0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream));
+  MG_CK(c, cudaMemcpyAsync(c->v0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream));
   // hist[0]: all-row residual of the guess
   double r0;
   st = mgrit_residual(c, 0, c->guess, &r0, nullptr);
   if (st) return st;
   if (hist) hist[0] = r0;
   if (!fcf)  // Parareal: the coarse correction updates the C-rows in place (v = u)
-    cudaMemcpy2DAsync(c->ucur, row, c->guess, row * m, row, nc + 1, cudaMemcpyDeviceToDevice,
-                      c->stream);
+    MG_CK(c, cudaMemcpy2DAsync(c->ucur, row, c->guess, row * m, row, nc + 1,
+                               cudaMemcpyDeviceToDevice, c->stream));
   int k = 0;
   bool conv = r0 < tol;
   bool nonfinite = !std::isfinite(r0);
@@ -1351,10 +1797,69 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   };
   bool materialised = false;
   std::vector<double> h(1, r0);
-  if (!conv && !nonfinite && max_iter > 0) {
+  // graph mode (option MGRIT_OPT_GRAPH; default: latency-bound problems): the iterations run
+  // as one CUDA graph with a device-side WHILE loop (graph.cu), one host sync per solve
+  const bool graph = !c->prof && !crows_hist && max_iter < kGraphHist &&
+                     (opt(c, MGRIT_OPT_GRAPH) ? c->opt_v[MGRIT_OPT_GRAPH][0] == 1
+                                              : (long long)nx * c->nt <= (1ll << 23));
+  // one iteration after the first sweep: coarse correction, (FCF: swap), fused sweep, norm
+  auto iteration = [&]() -> int {
+    int s2 = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
+    if (s2) return s2;
+    if (fcf) std::swap(c->ucur, c->unext);
+    s2 = do_sweep(false, true);
+    if (s2) return s2;
+    return reduce_norm(c, partial_count(c, nc, fcf ? 2 * m : m), nullptr);
+  };
+  if (!conv && !nonfinite && max_iter > 0 && graph) {
+    st = do_sweep(true, false);
+    if (st) return st;
+    c->ucur = c->u0b;
+    c->unext = c->v0b;
+    // capture and launch on the context's private stream, ordered after the caller's
+    if (!c->gstream) {
+      MG_CK(c, cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+      MG_CK(c, cudaEventCreateWithFlags(&c->gevent, cudaEventDisableTiming));
+    }
+    const cudaStream_t user = c->stream;
+    MG_CK(c, cudaEventRecord(c->gevent, user));
+    MG_CK(c, cudaStreamWaitEvent(c->gstream, c->gevent, 0));
+    c->stream = c->gstream;
+    auto graph_run = [&](LoopState &ls, std::vector<double> &hd) -> int {
+      if (!c->gexec) {
+        const int s2 = build_loop_graph(c, fcf, iteration);
+        c->ucur = c->u0b;
+        c->unext = c->v0b;
+        if (s2) return s2;
+      }
+      MG_CK(c, launch_loop_init(c->lstate, tol, c->dx * c->dt, max_iter, 0, c->stream));
+      MG_CK(c, cudaGraphLaunch(c->gexec, c->stream));
+      MG_CK(c, cudaMemcpyAsync(&ls, c->lstate, sizeof(ls), cudaMemcpyDeviceToHost, c->stream));
+      MG_CK(c, cudaMemcpyAsync(hd.data(), c->hist_dev, (max_iter + 1) * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+      MG_CK(c, cudaStreamSynchronize(c->stream));
+      return MGRIT_OK;
+    };
+    LoopState ls;
+    std::vector<double> hd(max_iter + 1);
+    st = graph_run(ls, hd);
+    c->stream = user;
+    if (st) return st;
+    k = ls.k;
+    for (int i = 1; i <= k; ++i) {
+      if (hist) hist[i] = hd[i];
+      h.push_back(hd[i]);
+    }
+    nonfinite = ls.nonfinite != 0;
+    conv = !nonfinite && hd[k] < tol;
+    c->launches += (long long)((k + 1) / 2) * c->glaunch[0] + (long long)(k / 2) * c->glaunch[1] + 1;
+    if (fcf && (k & 1)) std::swap(c->ucur, c->unext);   // odd k: the iterate is in v0b
+    c->have_iterate = true;
+  } else if (!conv && !nonfinite && max_iter > 0) {
     st = do_sweep(true, false);
     if (st) return st;
     while (true) {
+      Range nv_it("iteration");
       // coarse-grid correction: (FCF) unext += E, then unext becomes the iterate;
       // (F) ucur += e in place
       st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
@@ -1363,8 +1868,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       c->have_iterate = true;
       ++k;
       if (crows_hist)
-        cudaMemcpyAsync(crows_hist + (size_t)(k - 1) * (nc + 1) * nx, c->ucur, (nc + 1) * row,
-                        cudaMemcpyDeviceToDevice, c->stream);
+        MG_CK(c, cudaMemcpyAsync(crows_hist + (size_t)(k - 1) * (nc + 1) * nx, c->ucur,
+                                 (nc + 1) * row, cudaMemcpyDeviceToDevice, c->stream));
       // residual of iterate k (computed by the next sweep).  Predicted last: the
       // previous two residuals extrapolated geometrically fall below tol.
       bool last = false;
@@ -1395,10 +1900,11 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   if (converged) *converged = conv ? 1 : 0;
   if (out_dev) {
     if (!c->have_iterate) {
-      cudaMemcpyAsync(out_dev, c->guess, (size_t)(c->nt + 1) * row, cudaMemcpyDeviceToDevice, c->stream);
+      MG_CK(c, cudaMemcpyAsync(out_dev, c->guess, (size_t)(c->nt + 1) * row,
+                               cudaMemcpyDeviceToDevice, c->stream));
     } else if (materialised) {
-      cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->ucur + (size_t)nc * nx, row,
-                      cudaMemcpyDeviceToDevice, c->stream);
+      MG_CK(c, cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->ucur + (size_t)nc * nx, row,
+                               cudaMemcpyDeviceToDevice, c->stream));
     } else {
       SweepArgs a = base_sweep(c);
       a.nitems = (int)nc;
@@ -1410,8 +1916,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       a.each_last = m - 1;
       st = sweep(c, 3, a, m - 1);
       if (st) return st;
-      cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->ucur + (size_t)nc * nx, row,
-                      cudaMemcpyDeviceToDevice, c->stream);
+      MG_CK(c, cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->ucur + (size_t)nc * nx, row,
+                               cudaMemcpyDeviceToDevice, c->stream));
     }
   }
   cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -1426,9 +1932,10 @@ int mgrit_get_crows(mgrit_ctx *c, double *out_dev) {
   const long long nc = c->nt / c->m;
   const size_t row = (size_t)c->nx * sizeof(double);
   if (c->have_iterate)
-    cudaMemcpyAsync(out_dev, c->ucur, (nc + 1) * row, cudaMemcpyDeviceToDevice, c->stream);
+    MG_CK(c, cudaMemcpyAsync(out_dev, c->ucur, (nc + 1) * row, cudaMemcpyDeviceToDevice, c->stream));
   else
-    cudaMemcpy2DAsync(out_dev, row, c->guess, row * c->m, row, nc + 1, cudaMemcpyDeviceToDevice, c->stream);
+    MG_CK(c, cudaMemcpy2DAsync(out_dev, row, c->guess, row * c->m, row, nc + 1,
+                               cudaMemcpyDeviceToDevice, c->stream));
   return MGRIT_OK;
 }
 
@@ -1475,7 +1982,7 @@ int mgrit_describe(const mgrit_ctx *c, char *buf, size_t len) {
     const CoarsePlan pl = plan_coarse(c, c->levels - 1);
     if (pl.kind == CoarsePlan::CLUSTER_CA)
       snprintf(coarse, sizeof(coarse), "%s<NT=%d,P=%d,CL=%d,S=%d>",
-               coarse_tb(c, c->levels - 1) ? "psi_seq_cluster_tb_kernel" : "psi_seq_cluster_ca_kernel",
+               pl.tb ? "psi_seq_cluster_tb_kernel" : "psi_seq_cluster_ca_kernel",
                pl.cfg.nt_threads, pl.cfg.p, pl.cl, pl.S);
     else if (pl.kind == CoarsePlan::CLUSTER)
       snprintf(coarse, sizeof(coarse), "psi_seq_cluster_kernel<NT=%d,P=%d,CL=%d>", pl.cfg.nt_threads,
@@ -1485,12 +1992,163 @@ int mgrit_describe(const mgrit_ctx *c, char *buf, size_t len) {
     else if (pl.kind == CoarsePlan::TILES)
       snprintf(coarse, sizeof(coarse), "psi_coarse_kernel<NT=%d,P=%d> tiles=%d", pl.cfg.nt_threads,
                pl.cfg.p, pl.ntiles);
+    else if (pl.kind == CoarsePlan::TILES_SEG)
+      snprintf(coarse, sizeof(coarse), "psi_coarse_kernel<NT=%d,P=%d> tiles=%d seg=%d",
+               pl.cfg.nt_threads, pl.cfg.p, pl.ntiles, pl.seg);
     else
       snprintf(coarse, sizeof(coarse), "none");
   }
   snprintf(buf, len, "fine=%s<scheme%d,NT=%d,P=%d> tiles=%d halo=%d levels=%d coarse=%s", kern,
            c->scheme, ok ? f.cfg.nt_threads : 0, ok ? f.cfg.p : 0, ok ? f.ntiles : 0, ok ? f.HL : 0,
            c->levels, coarse);
+  return MGRIT_OK;
+}
+
+// ---- time shards ---------------------------------------------------------------------
+size_t mgrit_workspace_bytes_shard(int nx, int nt, int m, int levels, int nranks) {
+  if (nranks < 1 || nt % nranks) return 0;
+  return mgrit_workspace_bytes(nx, nt / nranks, m, levels);
+}
+
+int mgrit_setup_shard(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl, int order,
+                      int tableau, int levels, const mgrit_psi *psi, int relax, int rank,
+                      int nranks, double *stage_send, double *stage_recv, void *workspace_dev,
+                      size_t workspace_bytes, void *stream) {
+  if (!out) return MGRIT_EINVAL;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || nt % nranks) {
+    fprintf(stderr, "mgrit_setup_shard: bad rank/nranks or nt %% nranks != 0\n");
+    return MGRIT_EINVAL;
+  }
+  if (nranks > 1 && (!stage_send || !stage_recv)) {
+    fprintf(stderr, "mgrit_setup_shard: staging rows required\n");
+    return MGRIT_EINVAL;
+  }
+  const int st = mgrit_setup(out, nx, nt / nranks, m, alpha, cfl, order, tableau, levels, psi,
+                             relax, workspace_dev, workspace_bytes, stream);
+  if (st) return st;
+  (*out)->rank = rank;
+  (*out)->nranks = nranks;
+  (*out)->stage_send = stage_send;
+  (*out)->stage_recv = stage_recv;
+  return MGRIT_OK;
+}
+
+int mgrit_solve_shard(mgrit_ctx *c, const mgrit_comm *comm, double tol, int max_iter,
+                      double *out_dev, int *iters, double *hist, int *converged) {
+  if (!c) return MGRIT_EINVAL;
+  if (!c->guess) return fail(c, MGRIT_EINVAL, "mgrit_set_guess first");
+  if (max_iter < 0) return fail(c, MGRIT_EINVAL, "max_iter < 0");
+  if (c->nranks > 1 && (!comm || !comm->shift || !comm->allreduce_sum))
+    return fail(c, MGRIT_EINVAL, "time shards need a mgrit_comm");
+  if (c->psi_kind != MGRIT_PSI_STENCIL || c->cycle != MGRIT_CYCLE_V)
+    return fail(c, MGRIT_EUNSUPPORTED, "time shards: stencil Psi and V-cycles only");
+  Range nv_solve("mgrit_solve_shard");
+  c->comm = comm;
+  struct Reset {
+    mgrit_ctx *c;
+    ~Reset() { c->comm = nullptr; }
+  } reset{c};
+  const int m = c->m, nx = c->nx;
+  const long long nc = c->nt / m;
+  const size_t row = (size_t)nx * sizeof(double);
+  const bool fcf = c->relax == MGRIT_RELAX_FCF;
+  const double dxdt = c->dx * c->dt;
+  c->ucur = c->u0b;
+  c->unext = c->v0b;
+  MG_CK(c, cudaMemcpyAsync(c->u0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream));
+  MG_CK(c, cudaMemcpyAsync(c->v0b, c->guess, row, cudaMemcpyDeviceToDevice, c->stream));
+  // hist[0]: the guess's residual over the block's rows, summed over the ranks
+  double n2 = 0.0;
+  int st = residual0(c, c->guess, &n2, nullptr);
+  if (st) return st;
+  st = comm_sum(c, &n2, 1);
+  if (st) return st;
+  const double r0 = std::sqrt(dxdt * n2);
+  if (hist) hist[0] = r0;
+  if (!fcf)
+    MG_CK(c, cudaMemcpy2DAsync(c->ucur, row, c->guess, row * m, row, nc + 1,
+                               cudaMemcpyDeviceToDevice, c->stream));
+  auto do_sweep = [&](bool first, bool want_norm) -> int {
+    SweepArgs a = base_sweep(c);
+    a.nitems = (int)nc;
+    a.nsteps1 = m;
+    if (first && fcf) {
+      a.in = rm(c->guess, 0, m);
+      a.cmp = rm(c->guess, m, m);
+    } else {
+      a.in = rm(c->ucur, 0, 1);
+      a.cmp = rm(c->ucur, 1, 1);
+    }
+    a.partials = want_norm ? c->partials : nullptr;
+    if (fcf) {
+      a.endw = rm(c->unext, 1, 1);
+      a.nsteps2 = m;
+      a.p2_items = p2_count(c, nc);
+      a.r2 = rm(c->g[1], 2, 1);
+    } else {
+      a.dstore = rm(c->g[1], 1, 1);
+      a.d_every = 1;
+      a.d_phase = 0;
+    }
+    int s2 = sweep(c, 0, a, fcf ? 2 * m : m);
+    if (s2) return s2;
+    // the right neighbour's first coarse RHS row r_{nc+1} (FCF; Parareal's r_j are local)
+    return fcf ? comm_shift(c, row_ptr(c, c->g[1], nc + 1), row_ptr(c, c->g[1], 1)) : MGRIT_OK;
+  };
+  int k = 0;
+  bool conv = r0 < tol, nonfinite = !std::isfinite(r0);
+  c->have_iterate = false;
+  if (!conv && !nonfinite && max_iter > 0) {
+    st = do_sweep(true, false);
+    if (st) return st;
+    while (true) {
+      Range nv_it("iteration");
+      st = level_cycle_shard(c, 1, rm(fcf ? c->unext : c->ucur, 0, 1));
+      if (st) return st;
+      if (fcf) std::swap(c->ucur, c->unext);
+      c->have_iterate = true;
+      ++k;
+      // the corrected C-row at the block start belongs to rank-1
+      st = comm_shift(c, row_ptr(c, c->ucur, nc), row_ptr(c, c->ucur, 0));
+      if (st) return st;
+      st = do_sweep(false, true);
+      if (st) return st;
+      st = reduce_norm(c, partial_count(c, nc, fcf ? 2 * m : m), &n2);
+      if (st) return st;
+      st = comm_sum(c, &n2, 1);
+      if (st) return st;
+      const double rk = std::sqrt(dxdt * n2);
+      if (hist) hist[k] = rk;
+      if (!std::isfinite(rk)) { nonfinite = true; break; }
+      if (rk < tol) { conv = true; break; }
+      if (k >= max_iter) break;
+    }
+  }
+  if (iters) *iters = k;
+  if (converged) *converged = conv ? 1 : 0;
+  if (out_dev) {
+    if (!c->have_iterate) {
+      MG_CK(c, cudaMemcpyAsync(out_dev, c->guess, (size_t)(c->nt + 1) * row,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+      SweepArgs a = base_sweep(c);
+      a.nitems = (int)nc;
+      a.nsteps1 = m - 1;
+      a.in = rm(c->ucur, 0, 1);
+      a.each = rm(out_dev, 0, m);
+      a.each_step = 1;
+      a.each_first = 0;
+      a.each_last = m - 1;
+      st = sweep(c, 3, a, m - 1);
+      if (st) return st;
+      MG_CK(c, cudaMemcpyAsync(out_dev + (size_t)c->nt * nx, c->ucur + (size_t)nc * nx, row,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return fail(c, MGRIT_ECUDA, "solve_shard: %s", cudaGetErrorString(e));
+  if (nonfinite) return fail(c, MGRIT_ENONFINITE, "residual became non-finite at iteration %d", k);
   return MGRIT_OK;
 }
 

@@ -392,7 +392,7 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-#define MG_TMA_CFGS(X) X(128, 15) X(256, 11) X(64, 15)
+#define MG_TMA_CFGS(X) X(128, 15) X(256, 11) X(64, 15) X(32, 31)
 
 template <class SC>
 static cudaError_t dispatch_tma(SweepCfg c, const SweepArgs &a, cudaStream_t s) {

@@ -18,9 +18,11 @@ def psi_inputs(w) -> List[Dict]:
                             w.psi_widths, w.psi_eta)
 
 
-def make_solver(w, psi: Optional[List[Dict]] = None, stream=None) -> binding.MGRIT:
+def make_solver(w, psi: Optional[List[Dict]] = None, stream=None,
+                options: Optional[Dict] = None) -> binding.MGRIT:
     return binding.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels,
-                         psi if psi is not None else psi_inputs(w), w.relax, stream=stream)
+                         psi if psi is not None else psi_inputs(w), w.relax, stream=stream,
+                         options=options)
 
 
 def device_guess(w, device="cuda"):

@@ -61,8 +61,20 @@ def threshold(lam_m: np.ndarray, eta: float) -> List[int]:
     return list(range(ds[0], ds[-1] + 1))
 
 
-def lsq(lam: np.ndarray, m: int, offsets: Sequence[int], eps: float = 1e-6) -> np.ndarray:
-    """Real weighted LSQ  min || W^{1/2} (lambda^m - mu(psi)) ||  over psi in R^nu."""
+IMAG_TOL = 1e-8   # "if an imaginary component larger than 1e-8 is detected, we flag"
+
+
+class PsiRejected(ValueError):
+    """The LSQ solution was flagged and is not accepted as a coarse operator."""
+
+
+def lsq(lam: np.ndarray, m: int, offsets: Sequence[int], eps: float = 1e-6,
+        return_imag: bool = False):
+    """Weighted LSQ  min || W^{1/2} (lambda^m - mu(psi)) ||  (eq. LSQ_1D_problem).
+
+    Solved in the real form (Lemma 3, guarantees a real minimiser); the complex
+    least-squares problem the paper solves is solved as well and its largest imaginary
+    component is the P:394 flag (return_imag=True returns it)."""
     nx = lam.shape[0]
     theta = 2.0 * np.pi * np.arange(nx) / nx
     sw = 1.0 / (1.0 - np.abs(lam) + eps)
@@ -71,12 +83,18 @@ def lsq(lam: np.ndarray, m: int, offsets: Sequence[int], eps: float = 1e-6) -> n
     Ar = np.concatenate([M.real, M.imag], axis=0)
     br = np.concatenate([rhs.real, rhs.imag])
     psi, *_ = np.linalg.lstsq(Ar, br, rcond=None)
-    return psi
+    if not return_imag:
+        return psi
+    pc, *_ = np.linalg.lstsq(M, rhs, rcond=None)
+    return psi, float(np.max(np.abs(pc.imag)))
 
 
 def hierarchy(order: int, tableau: str, cfl: float, nx: int, m: int, levels: int,
-              widths: Sequence[int] = (), eta: float = None) -> List[Dict]:
-    """Psi_2..Psi_L as library inputs [{"kind": "stencil", "offsets", "coeffs"}, ...]."""
+              widths: Sequence[int] = (), eta: float = None,
+              allow_flagged: bool = False) -> List[Dict]:
+    """Psi_2..Psi_L as library inputs [{"kind": "stencil", "offsets", "coeffs"}, ...].
+    Each entry also carries the P:394 flag ("imag": largest imaginary component of the
+    complex LSQ solution); a flagged fit (> 1e-8) raises PsiRejected unless allow_flagged."""
     lam = phi_eigenvalues(order, tableau, cfl, nx)
     out = []
     for lvl in range(levels - 1):
@@ -84,7 +102,11 @@ def hierarchy(order: int, tableau: str, cfl: float, nx: int, m: int, levels: int
             offs = threshold(lam ** m, eta)
         else:
             offs = window(m ** (lvl + 1) * cfl, widths[lvl])
-        psi = lsq(lam, m, offs)
-        out.append({"kind": "stencil", "offsets": offs, "coeffs": [float(c) for c in psi]})
+        psi, imag = lsq(lam, m, offs, return_imag=True)
+        if imag > IMAG_TOL and not allow_flagged:
+            raise PsiRejected(f"level {lvl + 2}: LSQ imaginary component {imag:.2e} > 1e-8 "
+                              f"(P:394) for offsets {offs[0]}..{offs[-1]}")
+        out.append({"kind": "stencil", "offsets": offs, "coeffs": [float(c) for c in psi],
+                    "imag": imag})
         lam = symbol(dict(zip(offs, psi)), nx)
     return out

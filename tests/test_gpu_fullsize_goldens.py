@@ -54,10 +54,9 @@ def test_goldens_present():
         assert n in names, n
 
 
-@pytest.mark.parametrize("path", GOLD, ids=lambda p: os.path.basename(p)[9:-4])
-def test_fullsize_solve_vs_oracle_golden(path):
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
+def compare_with_golden(path, options=None):
+    """Run the library on a golden's workload; return (K, hist errors, per-iteration C-row
+    errors, final-row error, meta) without asserting."""
     from paper_1910_03726_b200 import binding, problem
     binding.lib()
     meta, psi, z = _load(path)
@@ -66,7 +65,7 @@ def test_fullsize_solve_vs_oracle_golden(path):
     ho = np.array(z["history"])
     assert bool(z["converged"]) and len(ho) == K + 1
     s = binding.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels, psi,
-                      w.relax)
+                      w.relax, options=options)
     s.set_cycle(meta["cycle"])
     g = problem.device_guess(w)
     s.set_guess(g)
@@ -74,24 +73,34 @@ def test_fullsize_solve_vs_oracle_golden(path):
     # max_iter = K: K is identical iff the solve converges at K and not at K-1
     res = s.solve(w.tol, K, out=out, keep_crows=True)
     hg = np.array(res["history"])
-    assert res["iterations"] == K and res["converged"], (res["iterations"], hg)
-    assert hg[K - 1] >= w.tol
     umax = float(z["umax"])
     floor = 1e-15 * math.sqrt(2 * w.nt * w.dt) * umax
-    herr = np.abs(hg - ho) / np.abs(ho)
-    for k in range(K + 1):
-        assert abs(hg[k] - ho[k]) <= REL * abs(ho[k]) + floor, (k, hg[k], ho[k])
     ci = torch.as_tensor(z["crow_idx"], device="cuda")
-    worst = []
-    for k in range(K):
+    crow_err = []
+    for k in range(min(K, res["iterations"])):
         got = res["crows"][k].index_select(0, ci).cpu().numpy()
         ref = z["crows"][k]
-        e = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
-        worst.append(e)
-        assert e <= REL, (k, e)
+        crow_err.append(float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))
     fi = torch.as_tensor(z["final_idx"], device="cuda")
     got = out.index_select(0, fi).cpu().numpy()
-    ef = float(np.max(np.abs(got - z["final_rows"])) / umax)
-    assert ef <= REL, ef
-    print(f"\n[golden {meta['name']}] K={K} hist rel.err max {herr.max():.2e}; C-row rel.err "
-          f"per iteration {['%.1e' % e for e in worst]}; final rows {ef:.2e}")
+    final_err = float(np.max(np.abs(got - z["final_rows"])) / umax)
+    hist_ok = [abs(a - b) <= REL * abs(b) + floor for a, b in zip(hg, ho)]
+    return dict(K=K, res=res, hg=hg, ho=ho, hist_ok=hist_ok, crow_err=crow_err,
+                final_err=final_err, meta=meta, w=w)
+
+
+@pytest.mark.parametrize("path", GOLD, ids=lambda p: os.path.basename(p)[9:-4])
+def test_fullsize_solve_vs_oracle_golden(path):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = compare_with_golden(path)
+    K, res, hg, ho = r["K"], r["res"], r["hg"], r["ho"]
+    herr = np.abs(hg - ho[: len(hg)]) / np.abs(ho[: len(hg)])
+    print(f"\n[golden {r['meta']['name']}] K={K} hist rel.err max {herr.max():.2e}; C-row rel.err "
+          f"per iteration {['%.1e' % e for e in r['crow_err']]}; final rows {r['final_err']:.2e}")
+    # max_iter = K: K is identical iff the solve converges at K and not at K-1
+    assert res["iterations"] == K and res["converged"], (res["iterations"], hg)
+    assert hg[K - 1] >= r["w"].tol
+    assert all(r["hist_ok"]), list(zip(hg, ho))
+    assert max(r["crow_err"]) <= REL, r["crow_err"]
+    assert r["final_err"] <= REL, r["final_err"]

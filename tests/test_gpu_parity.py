@@ -118,9 +118,9 @@ SDIRK_FORMS = [  # (order, tableau, cfl, nx): real, complex-pair and mixed root 
 
 
 @pytest.mark.parametrize("order,tab,cfl,nx", SDIRK_FORMS)
-def test_sdirk_fused_vs_product_form(order, tab, cfl, nx, monkeypatch):
+def test_sdirk_fused_vs_product_form(order, tab, cfl, nx):
     """The partial-fraction (fused, one barrier) stage solve and the product of
-    first-order periodic solves (MGRIT_SDIRK_PRODUCT=1) are the same operator (sdirk.cuh):
+    first-order periodic solves (option sdirk_product) are the same operator (sdirk.cuh):
     F-relaxation of the FULL state agrees with the oracle for both and between them."""
     B = _cuda()
     nt, m = 16, 4
@@ -130,9 +130,9 @@ def test_sdirk_fused_vs_product_form(order, tab, cfl, nx, monkeypatch):
     M.f_relax(Uo, phi, m)
     psi = [{"kind": "stencil", "offsets": [-1, 0], "coeffs": [0.5, 0.5]}]
     outs = []
-    for prod in ("0", "1"):
-        monkeypatch.setenv("MGRIT_SDIRK_PRODUCT", prod)
-        s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2, psi, "FCF")
+    for prod in (0, 1):
+        s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2, psi, "FCF",
+                    options={"sdirk_product": (prod,)})
         Ug = torch.from_numpy(U0).cuda()
         s.relax_full(Ug, "F")
         outs.append(Ug.cpu().numpy())
@@ -200,36 +200,33 @@ def test_coarse_correction_primitive(order, tab, cfl, nx, nt, m, nu):
     assert _rel(Ug.cpu().numpy(), Uo) <= REL
 
 
-@pytest.mark.parametrize("nx,o0,nu,env", [
+@pytest.mark.parametrize("nx,o0,nu,opts", [
     (4096, -7, 15, {}),                                   # default s-step cluster solve
-    (4096, -4, 9, {"MGRIT_SEQ_CLUSTER": "16,128,2"}),     # 16-CTA (non-portable) cluster
+    (4096, -4, 9, {"seq_cluster": (16, 128, 2)}),     # 16-CTA (non-portable) cluster
     (4096, -24, 37, {}),                                  # wide stencil (chunked window)
-    (4096, 0, 11, {"MGRIT_SEQ_S": "5"}),                  # one-sided (right), odd depth
-    (4096, -12, 12, {"MGRIT_SEQ_S": "16"}),               # one-sided (left), deep
+    (4096, 0, 11, {"seq_s": (5,)}),                  # one-sided (right), odd depth
+    (4096, -12, 12, {"seq_s": (16,)}),               # one-sided (left), deep
     (4096, -14, 15, {}),                                  # cfg3's shape
-    (4096, -14, 15, {"MGRIT_SEQ_S": "0"}),                # step-by-step exchange kernel
-    (4096, -30, 32, {"MGRIT_SEQ_S": "0", "MGRIT_SEQ_CLUSTER": "8,128,4"}),
+    (4096, -14, 15, {"seq_s": (0,)}),                # step-by-step exchange kernel
+    (4096, -30, 32, {"seq_s": (0,), "seq_cluster": (8, 128, 4)}),
     (1024, -4, 9, {}),                                    # cfg2-like: 8 x 64 x 2
-    (1024, -5, 11, {"MGRIT_SEQ_CLUSTER": "16,32,2", "MGRIT_SEQ_S": "3"}),
-    (1024, -5, 11, {"MGRIT_SEQ_S": "2"}),
+    (1024, -5, 11, {"seq_cluster": (16, 32, 2), "seq_s": (3,)}),
+    (1024, -5, 11, {"seq_s": (2,)}),
     (4096, -30, 32, {}),                                  # cfg4's shape (warp-specialised)
     (4096, -30, 32, {"_nt": "2044"}),                     # ragged: N = 511 = 4*127 + 3
     (1024, -4, 9, {"_nt": "1000"}),                       # ragged: N = 250 = 4*62 + 2
     (1024, -7, 9, {"_nt": "20"}),                         # N = 5: shorter than the g ring
-    (4096, -14, 15, {"MGRIT_COARSE_KERNEL": "ca"}),       # per-thread cp.async variant
-    (1024, -4, 9, {"MGRIT_COARSE_KERNEL": "ca", "_nt": "1000"}),
+    (4096, -14, 15, {"coarse_kernel": (1,)}),       # per-thread cp.async variant
+    (1024, -4, 9, {"coarse_kernel": (1,), "_nt": "1000"}),
 ])
-def test_coarse_correction_cluster(nx, o0, nu, env, monkeypatch):
+def test_coarse_correction_cluster(nx, o0, nu, opts):
     """Two-level coarse correction through the thread-block-cluster sequential solve
     (row split over 8/16 SMs, DSMEM halos): e_j = Psi e_{j-1} + r_j, U[jm] += e_j, then
     F-relaxation vs the oracle, for halo shapes on both / one side."""
     B = _cuda()
-    for k, v in env.items():
-        if not k.startswith("_"):
-            monkeypatch.setenv(k, v)
     order, tab, cfl, m = 3, "erk3_kutta", 0.85, 4
     nt = 2048 if nx == 4096 else 1024   # coarse chain long enough for the cluster path
-    nt = int(env.get("_nt", nt))
+    nt = int(opts.get("_nt", nt))
     phi = D.make_phi(order, tab, cfl, nx)
     rng = np.random.default_rng(nu)
     coeffs = rng.uniform(-1.0, 1.0, nu)
@@ -246,7 +243,8 @@ def test_coarse_correction_cluster(nx, o0, nu, env, monkeypatch):
     Uo[cpts] += E[1:]
     M.f_relax(Uo, phi, m)
     s = B.MGRIT(nx, nt, m, 1.0, cfl, order, tab, 2,
-                [{"kind": "stencil", "offsets": offsets, "coeffs": list(coeffs)}], "FCF")
+                [{"kind": "stencil", "offsets": offsets, "coeffs": list(coeffs)}], "FCF",
+                options={k: v for k, v in opts.items() if not k.startswith("_")})
     assert "coarse=psi_seq_cluster" in s.describe(), s.describe()
     Ug = torch.from_numpy(U).cuda()
     s.coarse_solve_full(Ug)
