@@ -423,6 +423,65 @@ def run_ours(args, w):
         dist.destroy_process_group()
 
 
+def run_shard(args, w):
+    """--mode shard: one problem split into N contiguous time blocks, one per GPU
+    (mgrit_solve_shard); value = the problem's fine DOF updates / the
+    max-over-ranks device time (strong scaling)."""
+    import torch
+    from paper_1910_03726_b200 import build as B
+    from paper_1910_03726_b200 import problem, timeshard
+
+    dist, rank, world = _dist()
+    B.build()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    psi = problem.psi_inputs(w)
+    sh = timeshard.ShardSolver(w, psi, rank, world, stream=stream)
+    comm = timeshard.TorchDistComm(sh.send_stage, sh.recv_stage, stream) if world > 1 else None
+    guess = sh.local_guess()
+    out = torch.empty_like(guess)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        res = sh.solve(comm, guess, w.tol, w.max_iter, out=out)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = sh.solve(comm, guess, w.tol, w.max_iter, out=out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    K = res["iterations"]
+    dof = problem.dof_updates(w, K)
+    ms = ms_local
+    if dist:
+        t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        line = {"metric": METRIC, "value": dof / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "mode": "shard",
+                "config": {"workload": w.name, "nx": w.nx, "nt": w.nt, "m": w.m,
+                           "levels": w.levels, "relax": w.relax, "iterations": K,
+                           "history": [float(f"{h:.4e}") for h in res["history"]],
+                           "parallelism": f"time{world}",
+                           "l2": "inputs larger than L2"},
+                "e2e": None}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_reference(args, w):
     dist, rank, world = _dist()
     if rank != 0:
@@ -462,12 +521,17 @@ def main():
                     help="mgrit_set_final_sweep mode (include/mgrit.h)")
     ap.add_argument("--cycle", default="V", choices=["V", "F"],
                     help="multilevel cycle (DESIGN.md R19); the bench line is the V-cycle")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
+                    help="N > 1: independent replicas (default, weak scaling) or one problem "
+                         "in N time blocks (mgrit_solve_shard, strong scaling; DESIGN.md §7)")
     ap.add_argument("--opt", action="append", default=[], metavar="NAME=V1,V2",
                     help="mgrit_set_option override (experiments), e.g. fine_tile=128,15")
     args = ap.parse_args()
     w = W.ALL[args.config]
     if args.impl == "reference":
         run_reference(args, w)
+    elif args.mode == "shard":
+        run_shard(args, w)
     else:
         run_ours(args, w)
 

@@ -292,6 +292,30 @@ int mgrit_setup_shard(mgrit_ctx **ctx, int nx, int nt, int m, double alpha, doub
 int mgrit_solve_shard(mgrit_ctx *ctx, const mgrit_comm *comm, double tol, int max_iter,
                       double *out_dev, int *iters, double *hist_host, int *converged);
 
+/*
+ * ---- Coarse-operator synthesis on the GPU (§4) ----
+ * mgrit_psi_fit computes Psi_2..Psi_levels by the weighted linear least-squares fit of
+ * eq. (LSQ_1D_problem) (w(z) = 1/(1 - z + 1e-6)^2 at |eigenvalues| of the
+ * operator being coarsened), recursively Psi_{l+1} ~ Psi_l^m, for the
+ * scheme (order, tableau, cfl) on nx points:
+ *   widths      levels-1 window widths nu_l: contiguous offsets centred on
+ *               round_half_away(-m^l cfl) (R8); NULL with eta > 0:
+ *   eta         > 0: two-level threshold pattern, the contiguous hull of the entries of
+ *               the first column of Phi^m with magnitude >= eta * max.
+ * Outputs (host): nnz_out[levels-1], offsets_out / coeffs_out [(levels-1) x
+ * MGRIT_MAX_PSI_TAPS] (row l: nnz_out[l] increasing offsets), imag_out (nullable,
+ * levels-1): the P:394 flag, the largest imaginary component of the complex problem's
+ * solution (fits with imag > 1e-8 are not accepted by the paper).  The normal equations
+ * are formed and solved in double-double arithmetic on the device (csrc/psifit.cu).
+ * workspace_dev: caller-owned device memory of mgrit_psi_fit_workspace_bytes(nx).
+ * Synchronous on `stream`.  Errors: EINVAL (sizes, ids, pattern), ENOMEM, ECUDA.
+ */
+size_t mgrit_psi_fit_workspace_bytes(int nx);
+int mgrit_psi_fit(int nx, int order, int tableau, double cfl, int m, int levels,
+                  const int *widths, double eta, int *offsets_out, int *nnz_out,
+                  double *coeffs_out, double *imag_out, void *workspace_dev,
+                  size_t workspace_bytes, void *stream);
+
 /* C-rows (nt/m+1) x nx of the current iterate after mgrit_solve. */
 int mgrit_get_crows(mgrit_ctx *ctx, double *out_dev);
 

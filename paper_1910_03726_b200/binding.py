@@ -81,6 +81,11 @@ _SIGS = [
     ("mgrit_solve_shard", C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p,
                                     C.POINTER(C.c_int), C.POINTER(C.c_double),
                                     C.POINTER(C.c_int)]),
+    ("mgrit_psi_fit_workspace_bytes", C.c_size_t, [C.c_int]),
+    ("mgrit_psi_fit", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                C.POINTER(C.c_int), C.c_double, C.POINTER(C.c_int),
+                                C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                C.POINTER(C.c_double), C.c_void_p, C.c_size_t, C.c_void_p]),
     ("mgrit_profile_enable", C.c_int, [C.c_void_p, C.c_int]),
     ("mgrit_profile_read", C.c_int, [C.c_void_p, C.POINTER(C.c_longlong),
                                      C.POINTER(C.c_double)]),
@@ -132,6 +137,34 @@ def scheme_coefficients(order: int, tableau: str, cfl: float):
     zd = {zlo.value + k: z[k] for k in range(zn.value)}
     Am = np.array(A[:]).reshape(6, 6)[:S, :S].copy()
     return zd, Am, np.array(b[:S])
+
+
+def psi_fit_device(order: int, tableau: str, cfl: float, nx: int, m: int, levels: int,
+                   widths: Sequence[int] = (), eta: Optional[float] = None, stream=None):
+    """mgrit_psi_fit: the Psi hierarchy fitted on the GPU (include/mgrit.h).  Returns
+    library inputs [{"kind": "stencil", "offsets", "coeffs", "imag"}, ...]."""
+    import torch
+    L = lib()
+    nb = L.mgrit_psi_fit_workspace_bytes(nx)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    nl = levels - 1
+    T = 64
+    offs = (C.c_int * (nl * T))()
+    nnz = (C.c_int * nl)()
+    cof = (C.c_double * (nl * T))()
+    imag = (C.c_double * nl)()
+    wid = (C.c_int * max(1, nl))(*[int(v) for v in list(widths)[:nl]]) if widths else None
+    st = L.mgrit_psi_fit(nx, order, TABLEAU[tableau], cfl, m, levels, wid,
+                         float(eta) if eta else 0.0, offs, nnz, cof, imag, ws.data_ptr(), nb,
+                         C.c_void_p(_stream(stream)))
+    if st:
+        raise MgritError(st, "mgrit_psi_fit")
+    out = []
+    for l in range(nl):
+        n = nnz[l]
+        out.append({"kind": "stencil", "offsets": [offs[l * T + a] for a in range(n)],
+                    "coeffs": [cof[l * T + a] for a in range(n)], "imag": imag[l]})
+    return out
 
 
 def fill_guess(dst, seed: int, lo: float = -1.0, u0=None, row0: int = 0, stream=None):

@@ -13,7 +13,7 @@ LIB = os.path.join(HERE, "libmgrit.so")
 # race-stress variant (tma.cuh / device.cuh mg_jitter): random sleeps at every asynchronous
 # protocol point; used only by tests/test_gpu_jitter.py
 JITTER_LIB = os.path.join(HERE, "libmgrit_jitter.so")
-SOURCES = ["mgrit_api.cu", "sweep.cu", "coarse.cu", "levels.cu", "graph.cu"]
+SOURCES = ["mgrit_api.cu", "sweep.cu", "coarse.cu", "levels.cu", "graph.cu", "psifit.cu"]
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -307,13 +307,23 @@ __device__ __forceinline__ void fused_lane_tables(const SdirkCoef &sd, double *w
   }
 }
 
-template <int NL, int NR, int P, int NT>
+// Compile-time specialisation of the fused solve for a launch whose factor structure is
+// known on the host (mgrit_api.cu make_sdirk): DMAX > 0 fixes the warp-scan depth, WL / PAIR
+// >= 0 fix warp_local / the complex pair, FUSED = 1 drops the product-form branch.  The
+// defaults read those fields at run time (every shape; FusedRT).
+template <int DMAX = 0, int WL = -1, int PAIR = -1, int FUSED = 0>
+struct FusedSpec {
+  static constexpr int dmax = DMAX, wl = WL, pair = PAIR, fused = FUSED;
+};
+using FusedRT = FusedSpec<>;
+
+template <int NL, int NR, int P, int NT, class FS = FusedRT>
 __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoef &sd,
                                                   double *wbuf, int &wphase) {
   constexpr int NW = NT / 32;
   constexpr int NSLOT = NL + 2 * (NL / 2) + NR;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool pair = (NL >= 2) && sd.ncrec > 0;   // warp-uniform
+  const bool pair = (NL >= 2) && (FS::pair >= 0 ? FS::pair == 1 : sd.ncrec > 0);  // warp-uniform
   double *wb = wbuf + wphase * NSLOT * NW;
   const double *lt = wbuf + 2 * 8 * NW;            // lane tables (fused_lane_tables)
   double y[P];
@@ -362,7 +372,7 @@ __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoe
   // ---- warp scans of the chunk totals (interleaved) --------------------------------
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    if (d >= sd.dmax) break;  // warp-uniform
+    if (d >= (FS::dmax > 0 ? FS::dmax : sd.dmax)) break;  // warp-uniform
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
       const double v = __shfl_up_sync(FULL, A[k], d);
@@ -394,7 +404,7 @@ __device__ __forceinline__ void fused_stage_solve(double (&f)[P], const SdirkCoe
   }
   __syncthreads();
   const int ld = lane < NW ? lane : 0;
-  const bool wl = sd.warp_local != 0;
+  const bool wl = FS::wl >= 0 ? FS::wl == 1 : sd.warp_local != 0;
   const int wprev = (warp + NW - 1) % NW, wnext = (warp + 1) % NW;
   // ---- carries entering the warp, then entering the lane; fix-up into y ------------
 #pragma unroll
@@ -467,7 +477,7 @@ __device__ __forceinline__ void stage_solve(double (&y)[P], const SdirkCoef &sd,
 
 // One SDIRK step in stage form (b-form update, R14):
 //   (I - a_ii Z) y_i = x + sum_{l<i} a_il k_l,   k_i = Z y_i,   x <- x + sum_i b_i k_i.
-template <class SC, int P, int NT>
+template <class SC, int P, int NT, class FS = FusedRT>
 __device__ __forceinline__ void dirk_step(double (&x)[P], const RKCoeffs &c, const SdirkCoef &sd,
                                           double *edge, int &phase, double *wbuf, int &wphase) {
   constexpr int S = SC::S;
@@ -481,8 +491,8 @@ __device__ __forceinline__ void dirk_step(double (&x)[P], const RKCoeffs &c, con
   }
 #pragma unroll
   for (int i = 0; i < S; ++i) {
-    if (sd.fused)
-      fused_stage_solve<SC::NL, SC::NR, P, NT>(acc[i], sd, wbuf, wphase);
+    if (FS::fused == 1 || sd.fused)
+      fused_stage_solve<SC::NL, SC::NR, P, NT, FS>(acc[i], sd, wbuf, wphase);
     else
       stage_solve<P, NT>(acc[i], sd, wbuf, wphase);
     double k[P];

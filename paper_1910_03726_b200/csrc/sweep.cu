@@ -21,11 +21,11 @@
 namespace mg {
 
 // One step of Phi: explicit stage form, or SDIRK with periodic banded stage solves.
-template <class SC, int P, int NT>
+template <class SC, int P, int NT, class FS = FusedRT>
 __device__ __forceinline__ void phi_step(double (&x)[P], const SweepArgs &a, double *edge,
                                          int &phase, double *wbuf, int &wphase) {
   if constexpr (SC::implicit)
-    dirk_step<SC, P, NT>(x, a.co, a.sd, edge, phase, wbuf, wphase);
+    dirk_step<SC, P, NT, FS>(x, a.co, a.sd, edge, phase, wbuf, wphase);
   else
     erk_step<SC, P, NT>(x, a.co, edge, phase);
 }
@@ -34,7 +34,7 @@ __device__ __forceinline__ void phi_step(double (&x)[P], const SweepArgs &a, dou
 // the next item's input / comparison windows with per-thread cp.async copies (padded
 // layout) into the other buffer pair while it computes the current one, so a whole-row
 // CTA (one per SM for the 512-thread SDIRK and ERK5 rows) never idles on a cold load.
-template <class SC, int NT, int P>
+template <class SC, int NT, int P, class FS = FusedRT>
 __global__ void __launch_bounds__(NT, 1) rk_sweep_kernel(const __grid_constant__ SweepArgs a) {
   constexpr int SP = Pad<P>::SP;
   constexpr int W = NT * P;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(NT, 1) rk_sweep_kernel(const __grid_constant__
                       (a.each.off + item * a.each.stride) * (long long)nx, x);
 #pragma unroll 1
     for (int i = 1; i <= a.nsteps1; ++i) {
-      phi_step<SC, P, NT>(x, a, edge, phase, wbuf, wphase);
+      phi_step<SC, P, NT, FS>(x, a, edge, phase, wbuf, wphase);
       if (i >= a.each_first && i <= a.each_last)
         store_slice(const_cast<double *>(a.each.base) +
                         (a.each.off + item * a.each.stride + i * a.each_step) * (long long)nx,
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(NT, 1) rk_sweep_kernel(const __grid_constant__
 #pragma unroll
         for (int p = 0; p < P; ++p) x[p] = d[p];
 #pragma unroll 1
-        for (int i = 1; i <= a.nsteps2; ++i) phi_step<SC, P, NT>(x, a, edge, phase, wbuf, wphase);
+        for (int i = 1; i <= a.nsteps2; ++i) phi_step<SC, P, NT, FS>(x, a, edge, phase, wbuf, wphase);
         store_slice(const_cast<double *>(rowp(a.r2, item)), x);
       }
     }
@@ -556,16 +556,16 @@ int rk_scheme_stages(int scheme) {
 }
 bool rk_scheme_implicit(int scheme) { return scheme >= 5 && scheme < 9; }
 
-template <class SC, int NT, int P>
+template <class SC, int NT, int P, class FS = FusedRT>
 static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
   constexpr int SP = Pad<P>::SP;
   const size_t smem = sizeof(double) * (4 * NT * SP + 2 * NT * (SC::NL + SC::NR) + 2 +
                                         NT / 32 + 2 + 16 * (NT / 32) + 8 * 32 + 2);
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
-    cudaFuncSetAttribute(rk_sweep_kernel<SC, NT, P>,
+    cudaFuncSetAttribute(rk_sweep_kernel<SC, NT, P, FS>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rk_sweep_kernel<SC, NT, P>, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rk_sweep_kernel<SC, NT, P, FS>, NT, smem);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   int dev = 0, sms = 148;
@@ -574,7 +574,7 @@ static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
   const long long total = (long long)a.nitems * a.ntiles;
   if (total <= 0) return cudaSuccess;
   const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
-  rk_sweep_kernel<SC, NT, P><<<(unsigned)grid, NT, smem, s>>>(a);
+  rk_sweep_kernel<SC, NT, P, FS><<<(unsigned)grid, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -593,6 +593,13 @@ static cudaError_t dispatch_cfg(SweepCfg c, const SweepArgs &a, cudaStream_t s) 
 #define MG_IMPL_CFGS(X) X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8) X(256, 16)
 template <class SC>
 static cudaError_t dispatch_implicit(SweepCfg c, const SweepArgs &a, cudaStream_t s) {
+  // cfg4's production shape (SDIRK3+U3, 4096-point rows, three real factors, scan depth 8,
+  // warp-local carries): the fused solve's structure fixed at compile time
+  if constexpr (std::is_same<SC, SDIRK3U3>::value) {
+    if (c.nt_threads == 256 && c.p == 16 && a.sd.fused && a.sd.ncrec == 0 && a.sd.dmax == 8 &&
+        a.sd.warp_local)
+      return launch_one<SC, 256, 16, FusedSpec<8, 1, 0, 1>>(a, s);
+  }
 #define MG_CASE(NT_, P_) \
   if (c.nt_threads == NT_ && c.p == P_) return launch_one<SC, NT_, P_>(a, s);
   MG_IMPL_CFGS(MG_CASE)

@@ -8,12 +8,20 @@ import numpy as np
 from . import binding, psi as psimod
 
 
-def psi_inputs(w) -> List[Dict]:
-    """Coarse operators of a workload as library inputs (host LSQ fit)."""
+def psi_inputs(w, device: bool = False) -> List[Dict]:
+    """Coarse operators of a workload as library inputs (LSQ fit): host numpy
+    (default) or on the GPU (mgrit_psi_fit, device=True)."""
     if w.psi_kind == "ideal":
         return [{"kind": "ideal"}]
     if w.psi_kind == "redisc":
         return [{"kind": "redisc", "cfl": w.redisc_cfl}]
+    if device:
+        out = binding.psi_fit_device(w.order, w.tableau, w.cfl, w.nx, w.m, w.levels,
+                                     w.psi_widths, w.psi_eta)
+        for lvl, p in enumerate(out):
+            if p["imag"] > psimod.IMAG_TOL:
+                raise psimod.PsiRejected(f"level {lvl + 2}: imaginary component {p['imag']:.2e}")
+        return out
     return psimod.hierarchy(w.order, w.tableau, w.cfl, w.nx, w.m, w.levels,
                             w.psi_widths, w.psi_eta)
 
