@@ -154,7 +154,8 @@ class SolveReport:
 def solve(U: np.ndarray, phis: Sequence[Callable], m: int, dx: float, dt: float,
           relax: str = "FCF", tol: float = 1e-10, max_iter: int = 64,
           keep_states: bool = False, cycle: str = "V",
-          on_iter: Optional[Callable[[int, np.ndarray], None]] = None) -> SolveReport:
+          on_iter: Optional[Callable[[int, np.ndarray], None]] = None,
+          g0: Optional[np.ndarray] = None) -> SolveReport:
     """MGRIT / Parareal iteration on the fine space-time iterate U (in place).
 
     U[0] holds u0 and is never modified.  The residual is
@@ -162,17 +163,20 @@ def solve(U: np.ndarray, phis: Sequence[Callable], m: int, dx: float, dt: float,
     ||r^(k)|| < tol (R2).  No early stop on growth (R15), except
     for non-finite values.  cycle: "V" or "F" (R19).  on_iter(k, U), if
     given, is called after iteration k with the iterate (read-only observation, e.g. to
-    sample rows for a golden file; it does not take part in the arithmetic)."""
+    sample rows for a golden file; it does not take part in the arithmetic).  g0: the fine
+    level's right-hand side (rows 1..nt; row 0 unused) for an affine fine propagator
+    U[n+1] = Phi U[n] + g0[n+1], e.g. the inflow forcing of oracle.inflow (R12, R20);
+    None = 0."""
     phi = phis[0]
-    hist = [residual_norm(U, phi, dx, dt)]
+    hist = [residual_norm(U, phi, dx, dt, g0)]
     states = []
     k = 0
     converged = hist[0] < tol
     nonfinite = False
     while not converged and k < max_iter:
-        (fcycle if cycle == "F" else vcycle)(0, U, None, phis, m, relax)
+        (fcycle if cycle == "F" else vcycle)(0, U, g0, phis, m, relax)
         k += 1
-        r = residual_norm(U, phi, dx, dt)
+        r = residual_norm(U, phi, dx, dt, g0)
         hist.append(r)
         if keep_states:
             states.append(U[::m].copy())

@@ -183,3 +183,27 @@ CFG5 = Workload("cfg5", 16384, 65536, 0.85, "ERK", 3, "erk3_ssp", 4, 6, "FCF", "
                 max_iter=64)
 
 ALL = {w.name: w for w in (CFG1_REDISC, CFG1_IDEAL, CFG2, CFG3, CFG4_LITERAL, CFG4, CFG5)}
+
+
+# ----------------------------------------------------------------------------
+# Inflow data of the inflow/outflow problem (§4.5): u(-1, t) = sin^4(pi t).
+# The derivative table g^(r)(t_n), r = 0..nq-1, is the boundary DATA both the oracle and the
+# library consume; the inverse Lax-Wendroff / stage-value arithmetic that turns it into
+# ghost values is the method's and lives on each side separately (R20).
+# sin^4(y) = 3/8 - cos(2y)/2 + cos(4y)/8.
+# ----------------------------------------------------------------------------
+def inflow_sin4_derivatives(t: np.ndarray, nq: int) -> np.ndarray:
+    """Rows n: g^(r)(t_n) for r = 0..nq-1, g(t) = sin^4(pi t)."""
+    t = np.asarray(t, dtype=np.float64).reshape(-1)
+    out = np.empty((t.shape[0], nq))
+    for r in range(nq):
+        ph = r * np.pi / 2.0
+        v = -0.5 * (2.0 * np.pi) ** r * np.cos(2.0 * np.pi * t + ph) + \
+            0.125 * (4.0 * np.pi) ** r * np.cos(4.0 * np.pi * t + ph)
+        out[:, r] = v + (0.375 if r == 0 else 0.0)
+    return out
+
+
+def inflow_grid(nx: int) -> np.ndarray:
+    """Unknowns of the inflow/outflow grid: x_i = -1 + i dx, i = 1..nx (x_0 = -1 is data)."""
+    return -1.0 + np.arange(1, nx + 1, dtype=np.float64) * (2.0 / nx)
