@@ -170,6 +170,32 @@ int mgrit_coarse_solve(mgrit_ctx *ctx, int level, double *U_dev);
 int mgrit_set_rhs(mgrit_ctx *ctx, int level, const double *g_dev);
 
 /*
+ * mgrit_set_inflow — inflow/outflow boundaries instead of the periodic one (PAPER.md 4.5,
+ * P:672-680; R20).  The row then holds the nx unknowns u_1..u_nx at x_i = -1 + i dx,
+ * x_0 = -1 is the inflow point (its value is data), x_nx = 1 the outflow point.
+ *   enable   0: back to periodic rows.  1: every fine step is Phi(u; t_n) = Phi_h u + b_n:
+ *            Phi_h uses zero inflow ghosts and degree-p polynomial extrapolation of every
+ *            stage vector at the outflow; b_n = Phi(0; t_n) carries the inflow data through
+ *            the Taylor / inverse-Lax-Wendroff ghost values of each Runge-Kutta stage
+ *            (Carpenter et al.); every stencil Psi_l is truncated at the boundaries (Toeplitz,
+ *            no wrap), IDEAL/REDISC Psi use the same closures.
+ *   dg_dev   device, nt x (order + s) row-major: the inflow derivatives g^(r)(t_n),
+ *            r = 0..order+s-1, at t_n = n dt, n = 0..nt-1 (s = stages); read during the call
+ *            only (the forcing rows b_n go to the workspace).  NULL: homogeneous inflow.
+ * All entry points then act on the affine system U[n+1] = Phi_h U[n] + b_n (mgrit_relax,
+ * mgrit_residual, mgrit_coarse_solve, mgrit_solve; coarse levels are error equations and
+ * stay homogeneous).  Asynchronous on the context's stream.
+ * Errors: EUNSUPPORTED (SDIRK tableau; time shards; a row that does not fit one CTA with
+ * more points per thread than the order: nx in {64, 128, ..., 4096}, nx >= 128 for order
+ * 3-4, nx >= 256 for order 5; RK-form Psi with nx = 4096), ECUDA.
+ * mgrit_get_forcing copies the nt x MGRIT_FORCING_LD forcing rows (b_n on the first
+ * s*|d_min| points of the row, zero-padded) to out_dev.
+ */
+#define MGRIT_FORCING_LD 24
+int mgrit_set_inflow(mgrit_ctx *ctx, int enable, const double *dg_dev);
+int mgrit_get_forcing(mgrit_ctx *ctx, double *out_dev);
+
+/*
  * mgrit_solve — MGRIT iterations from the registered guess until ||r^(k)|| < tol or
  * k == max_iter (R2, R15).  Production engine: C-point storage, fused
  * relax+residual+restriction sweeps, sequential (or V-cycle) coarse solve.

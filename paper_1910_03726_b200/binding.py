@@ -65,6 +65,8 @@ _SIGS = [
                                  C.c_void_p]),
     ("mgrit_coarse_solve", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     ("mgrit_set_rhs", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    ("mgrit_set_inflow", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    ("mgrit_get_forcing", C.c_int, [C.c_void_p, C.c_void_p]),
     ("mgrit_solve", C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.POINTER(C.c_int),
                               C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p]),
     ("mgrit_set_cycle", C.c_int, [C.c_void_p, C.c_int]),
@@ -271,6 +273,22 @@ class MGRIT:
         self._rhs_keep = getattr(self, "_rhs_keep", {})
         self._rhs_keep[level] = g
         self._check(lib().mgrit_set_rhs(self.ctx, level, _dptr(g)), "mgrit_set_rhs")
+
+    def set_inflow(self, dg=None, enable: bool = True):
+        """mgrit_set_inflow: inflow/outflow boundaries (PAPER.md 4.5); dg = nt x (order + s)
+        device array of inflow derivatives g^(r)(t_n) (None: homogeneous inflow)."""
+        if dg is not None:
+            assert dg.is_cuda and dg.dtype.is_floating_point and dg.is_contiguous()
+            assert dg.shape[0] == self.nt
+        self._check(lib().mgrit_set_inflow(self.ctx, 1 if enable else 0, _dptr(dg)),
+                    "mgrit_set_inflow")
+
+    def get_forcing(self):
+        """mgrit_get_forcing: the nt x 24 compact forcing rows b_n (device tensor)."""
+        import torch
+        out = torch.empty((self.nt, 24), dtype=torch.float64, device=self.workspace.device)
+        self._check(lib().mgrit_get_forcing(self.ctx, _dptr(out)), "mgrit_get_forcing")
+        return out
 
     # ---- production solve -------------------------------------------------------
     def set_guess(self, guess):

@@ -13,7 +13,8 @@ LIB = os.path.join(HERE, "libmgrit.so")
 # race-stress variant (tma.cuh / device.cuh mg_jitter): random sleeps at every asynchronous
 # protocol point; used only by tests/test_gpu_jitter.py
 JITTER_LIB = os.path.join(HERE, "libmgrit_jitter.so")
-SOURCES = ["mgrit_api.cu", "sweep.cu", "coarse.cu", "levels.cu", "graph.cu", "psifit.cu"]
+SOURCES = ["mgrit_api.cu", "sweep.cu", "coarse.cu", "levels.cu", "graph.cu", "psifit.cu",
+           "bounded.cu"]
 NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -43,24 +44,39 @@ def build(verbose: bool = False, force: bool = False, variant: str = "") -> str:
         lt = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= lt for d in deps):
             return LIB
+    # objects are kept (git-ignored): a translation unit is recompiled only when its source
+    # or any header is newer than its object
+    hdr_t = max(os.path.getmtime(d) for d in deps[len(srcs):])
     objs = []
     procs = []
     for s in srcs:
         o = os.path.join(CSRC, os.path.basename(s) + tag + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", s, "-o", o]
-        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(o)
+        if not force and os.path.exists(o) and os.path.getmtime(o) >= max(hdr_t, os.path.getmtime(s)):
+            continue
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", s, "-o", o]
+        procs.append((cmd, o, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     log = []
-    for cmd, p in procs:
+    failed = None
+    for cmd, o, p in procs:
         out, _ = p.communicate()
         log.append(out)
+        with open(o + ".log", "w") as f:
+            f.write(out)
         if p.returncode != 0:
             sys.stderr.write(out)
-            raise RuntimeError("nvcc failed: " + " ".join(cmd))
+            if os.path.exists(o):
+                os.remove(o)
+            failed = failed or cmd
+    if failed:
+        raise RuntimeError("nvcc failed: " + " ".join(failed))
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib]
     subprocess.run(cmd, check=True)
+    # ptxas report of every unit (the logs of units not recompiled this time are kept)
+    log = []
     for o in objs:
-        os.remove(o)
+        if os.path.exists(o + ".log"):
+            log.append(open(o + ".log").read())
     if verbose:
         sys.stdout.write("".join(log))
     with open(os.path.join(HERE, f"ptxas{tag}.log"), "w") as f:

@@ -14,6 +14,7 @@
 //  * rk_coarse_kernel: IDEAL (Phi^m) / REDISC Psi in Runge-Kutta form.
 #include "kernels.h"
 #include "tma.cuh"
+#include "rows.cuh"
 
 #include <cooperative_groups.h>
 
@@ -1571,62 +1572,6 @@ cudaError_t launch_psi_level_tma(SweepCfg c, const PsiSweepArgs &a, cudaStream_t
 }
 
 // --------------------------------------------------------------------------
-template <class SC, int NT, int P>
-__global__ void __launch_bounds__(NT, 1) rk_coarse_kernel(const __grid_constant__ RKCoarseArgs a) {
-  extern __shared__ double smem[];
-  double *edge = smem;
-  double *wbuf = edge + 2 * NT * (SC::NL + SC::NR) + 2;  // SDIRK recurrences + lane tables
-  int wphase = 0;
-  const int tid = threadIdx.x, nx = a.nx;
-  int phase = 0;
-  if constexpr (SC::implicit) {
-    if (a.sd.fused) fused_lane_tables<SC::NL, SC::NR, NT>(a.sd, wbuf);
-    __syncthreads();
-  }
-  // one coarse step = q steps of the (explicit or SDIRK) Runge-Kutta propagator
-  auto rk = [&](double(&x)[P]) {
-    if constexpr (SC::implicit) dirk_step<SC, P, NT>(x, a.co, a.sd, edge, phase, wbuf, wphase);
-    else erk_step<SC, P, NT>(x, a.co, edge, phase);
-  };
-  double x[P];
-#pragma unroll
-  for (int p = 0; p < P; ++p) x[p] = 0.0;
-  // g_n and v_n do not depend on the chain: a register ring loads them D steps ahead, so
-  // their latency (~1 us) overlaps D coarse steps (one-warp rows exchange by shuffles, no
-  // barrier).  The ring is indexed at compile time: steps run in blocks of D.
-  constexpr int D = SC::implicit ? 2 : ((16 / P) < 2 ? 2 : (16 / P));
-  auto load = [&](int n, double(&gv)[P], double(&vv)[P]) {
-    if (n > a.nsteps) return;
-    const double *g = a.g.base + (a.g.off + (long long)n * a.g.stride) * nx;
-    const double *v = a.v.base ? a.v.base + (a.v.off + (long long)n * a.v.stride) * nx : nullptr;
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      gv[p] = g[tid * P + p];
-      vv[p] = v ? v[tid * P + p] : 0.0;
-    }
-  };
-  double gr[D][P], vr[D][P];
-#pragma unroll
-  for (int d = 0; d < D; ++d) load(1 + d, gr[d], vr[d]);
-#pragma unroll 1
-  for (int n0 = 1; n0 <= a.nsteps; n0 += D) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int n = n0 + d;
-      if (n > a.nsteps) break;
-#pragma unroll 1
-      for (int r = 0; r < a.q; ++r) rk(x);
-      double *o = const_cast<double *>(a.out.base) + (a.out.off + (long long)n * a.out.stride) * nx;
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        x[p] = x[p] + gr[d][p];
-        o[tid * P + p] = a.v.base ? vr[d][p] + x[p] : x[p];
-      }
-      load(n + D, gr[d], vr[d]);                  // slot d: D - 1 steps of lead
-    }
-  }
-}
-
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) reduce_kernel(const double *__restrict__ p, long long n,
                                                       double *out) {
@@ -1735,30 +1680,6 @@ cudaError_t launch_psi_sweep(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s) 
   MG_PSI_CFGS(MG_CASE)
 #undef MG_CASE
   return cudaErrorInvalidConfiguration;
-}
-
-template <class SC>
-static cudaError_t launch_rkc(SweepCfg c, const RKCoarseArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (2 * c.nt_threads * (SC::NL + SC::NR) + 4 +
-                                        16 * (c.nt_threads / 32) + 8 * 32 + 2);
-  if (c.nt_threads == 32 && c.p == 2) {
-    rk_coarse_kernel<SC, 32, 2><<<1, 32, smem, s>>>(a);
-  } else if (c.nt_threads == 32 && c.p == 4) {
-    rk_coarse_kernel<SC, 32, 4><<<1, 32, smem, s>>>(a);
-  } else if (c.nt_threads == 32 && c.p == 8) {
-    rk_coarse_kernel<SC, 32, 8><<<1, 32, smem, s>>>(a);
-  } else if (c.nt_threads == 64 && c.p == 8) {
-    rk_coarse_kernel<SC, 64, 8><<<1, 64, smem, s>>>(a);
-  } else if (c.nt_threads == 128 && c.p == 8) {
-    rk_coarse_kernel<SC, 128, 8><<<1, 128, smem, s>>>(a);
-  } else if (c.nt_threads == 256 && c.p == 8) {
-    rk_coarse_kernel<SC, 256, 8><<<1, 256, smem, s>>>(a);
-  } else if (c.nt_threads == 256 && c.p == 16) {
-    rk_coarse_kernel<SC, 256, 16><<<1, 256, smem, s>>>(a);
-  } else {
-    return cudaErrorInvalidConfiguration;
-  }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_rk_coarse(int scheme, SweepCfg c, const RKCoarseArgs &a, cudaStream_t s) {

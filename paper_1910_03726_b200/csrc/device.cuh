@@ -97,7 +97,39 @@ __device__ __forceinline__ void st_shared_pred(uint32_t addr, double v, bool pre
 // Halo exchange: L[k] = y of point (t*P - NL + k), R[k] = y of point (t*P + P + k).
 // `edge` holds 2 * NT * (NL+NR) doubles; `phase` toggles the half in use.
 // ---------------------------------------------------------------------------
+// Inflow/outflow closure of the homogeneous operator on a whole (non-periodic) row
+// (PAPER.md 4.5; R20): the thread owning the first points sees zero
+// inflow ghosts, the thread owning the last points sees the degree-(NL+NR) polynomial
+// extrapolation of the row's last NL+NR+1 values (Lagrange weights, exact integers).
+__host__ __device__ constexpr double extrap_weight(int p, int k, int j) {
+  // e_j with u(N + k) = sum_j e_j u(N - j), j = 0..p
+  double w = 1.0;
+  for (int l = 0; l <= p; ++l)
+    if (l != j) w *= (double)(k + l) / (double)(l - j);
+  return w;
+}
 template <int NL, int NR, int P, int NT>
+__device__ __forceinline__ void bounded_ghosts(const double (&y)[P], Arr<NL> &L, Arr<NR> &R) {
+  constexpr int PD = NL + NR;   // order p of U_p
+  static_assert(P >= PD + 1, "the last thread must own the p+1 extrapolation nodes");
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) L.v[k] = 0.0;
+  }
+  if constexpr (NR > 0) {
+    if (threadIdx.x == NT - 1) {
+#pragma unroll
+      for (int k = 0; k < NR; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j <= PD; ++j) acc = fma(extrap_weight(PD, k + 1, j), y[P - 1 - j], acc);
+        R.v[k] = acc;
+      }
+    }
+  }
+}
+
+template <int NL, int NR, int P, int NT, bool BND = false>
 __device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<NR> &R,
                                          double *edge, int &phase) {
   constexpr int NW = NT / 32;
@@ -108,6 +140,7 @@ __device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<N
     for (int k = 0; k < NL; ++k) L.v[k] = __shfl_sync(FULL, y[P - NL + k], (lane + 31) & 31);
 #pragma unroll
     for (int k = 0; k < NR; ++k) R.v[k] = __shfl_sync(FULL, y[k], (lane + 1) & 31);
+    if constexpr (BND) bounded_ghosts<NL, NR, P, NT>(y, L, R);
     return;
   }
 #pragma unroll
@@ -136,16 +169,17 @@ __device__ __forceinline__ void exchange(const double (&y)[P], Arr<NL> &L, Arr<N
     R.v[k] = (lane == 31) ? t : R.v[k];
   }
   phase ^= 1;
+  if constexpr (BND) bounded_ghosts<NL, NR, P, NT>(y, L, R);
 }
 
 // k = Z y, (Z y)_i = sum_{d=-NL}^{NR} z_d y_{i+d}, d ascending (oracle order).
-template <int NL, int NR, int P, int NT>
+template <int NL, int NR, int P, int NT, bool BND = false>
 __device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
                                         const double *__restrict__ z, double *edge,
                                         int &phase) {
   Arr<NL> L;
   Arr<NR> R;
-  exchange<NL, NR, P, NT>(y, L, R, edge, phase);
+  exchange<NL, NR, P, NT, BND>(y, L, R, edge, phase);
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     double acc = 0.0;
@@ -161,13 +195,13 @@ __device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
 }
 
 // k = base + Z y (the stencil accumulated onto `base`, d ascending).
-template <int NL, int NR, int P, int NT>
+template <int NL, int NR, int P, int NT, bool BND = false>
 __device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
                                         const double *__restrict__ z, double *edge,
                                         int &phase, const double (&base)[P]) {
   Arr<NL> L;
   Arr<NR> R;
-  exchange<NL, NR, P, NT>(y, L, R, edge, phase);
+  exchange<NL, NR, P, NT, BND>(y, L, R, edge, phase);
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     double acc = base[p];
@@ -195,31 +229,34 @@ __device__ __forceinline__ void apply_Z(const double (&y)[P], double (&k)[P],
 //    coefficient is rounded), so only per-operation rounding differs.
 // Measured drift against the stage-form oracle over the full cfg5 time length (65536 steps,
 // tests/test_gpu_fullsize_goldens.py) stays far inside the 1e-12 contract (R5).
-template <class SC, int P, int NT>
+// BND: the homogeneous inflow/outflow operator Phi_h (zero inflow ghosts, extrapolated outflow
+// ghosts of every vector Z acts on; both closures are linear, so the rearranged forms apply
+// the same operator as the stage form).
+template <class SC, int P, int NT, bool BND = false>
 __device__ __forceinline__ void erk_step(double (&x)[P], const RKCoeffs &c, double *edge,
                                          int &phase) {
   constexpr int S = SC::S;
   if constexpr (S == 3) {
     if (c.so3 == 1) {  // 3 stencils + 3 FP64 instructions per point (15 for U3) instead of 18
       double y[P], u[P], w[P];
-      apply_Z<SC::NL, SC::NR, P, NT>(x, y, c.soz[0], edge, phase, x);   // y1 = x + a10 Z x
+      apply_Z<SC::NL, SC::NR, P, NT, BND>(x, y, c.soz[0], edge, phase, x);   // y1 = x + a10 Z x
 #pragma unroll
       for (int p = 0; p < P; ++p) y[p] += x[p];                          // x + y1
-      apply_Z<SC::NL, SC::NR, P, NT>(y, u, c.soz[1], edge, phase, x);   // y2 = x + a21 Z(x + y1)
-      apply_Z<SC::NL, SC::NR, P, NT>(u, w, c.z, edge, phase, u);        // y2 + Z y2
+      apply_Z<SC::NL, SC::NR, P, NT, BND>(y, u, c.soz[1], edge, phase, x);   // y2 = x + a21 Z(x + y1)
+      apply_Z<SC::NL, SC::NR, P, NT, BND>(u, w, c.z, edge, phase, u);        // y2 + Z y2
 #pragma unroll
       for (int p = 0; p < P; ++p) x[p] = fma(c.so[1], w[p], c.so[0] * x[p]);
       return;
     }
     if (c.so3 == 2) {  // incremental form (a10 = 1): every full-size update is x + small
       double d[P], t[P], e[P];
-      apply_Z<SC::NL, SC::NR, P, NT>(x, d, c.z, edge, phase);           // d1 = Z x
+      apply_Z<SC::NL, SC::NR, P, NT, BND>(x, d, c.z, edge, phase);           // d1 = Z x
 #pragma unroll
       for (int p = 0; p < P; ++p) t[p] = fma(2.0, x[p], d[p]);           // x + y1 = 2x + d1
-      apply_Z<SC::NL, SC::NR, P, NT>(t, d, c.soz[1], edge, phase);      // d2 = a21 Z(x + y1)
+      apply_Z<SC::NL, SC::NR, P, NT, BND>(t, d, c.soz[1], edge, phase);      // d2 = a21 Z(x + y1)
 #pragma unroll
       for (int p = 0; p < P; ++p) t[p] = x[p] + d[p];                    // y2 = x + d2
-      apply_Z<SC::NL, SC::NR, P, NT>(t, e, c.z, edge, phase, d);        // d2 + Z y2
+      apply_Z<SC::NL, SC::NR, P, NT, BND>(t, e, c.z, edge, phase, d);        // d2 + Z y2
 #pragma unroll
       for (int p = 0; p < P; ++p) x[p] = fma(c.so[1], e[p], x[p]);      // x + b2 (d2 + Z y2)
       return;
@@ -240,13 +277,13 @@ __device__ __forceinline__ void erk_step(double (&x)[P], const RKCoeffs &c, doub
       // x += (b_{S-1} Z) y — NL + NR + 1 FMAs instead of a DMUL, NL + NR FMAs and one more
       // FMA per point (same result up to rounding)
       double t[P];
-      apply_Z<SC::NL, SC::NR, P, NT>(acc[i], t, c.bz, edge, phase, out);
+      apply_Z<SC::NL, SC::NR, P, NT, BND>(acc[i], t, c.bz, edge, phase, out);
 #pragma unroll
       for (int p = 0; p < P; ++p) out[p] = t[p];
       continue;
     }
     double k[P];
-    apply_Z<SC::NL, SC::NR, P, NT>(acc[i], k, c.z, edge, phase);
+    apply_Z<SC::NL, SC::NR, P, NT, BND>(acc[i], k, c.z, edge, phase);
 #pragma unroll
     for (int l = i + 1; l < S; ++l) {
       if (SC::a_nz(l, i)) {

@@ -39,7 +39,13 @@ struct SweepArgs {
   double *partials;  // [nitems*ntiles] sum(delta^2) over each tile's own outputs
   RKCoeffs co;
   SdirkCoef sd;      // implicit schemes: factored periodic stage solve (sdirk.cuh)
+  // inflow/outflow rows (bounded.cu): compact forcing rows b_n (FORC_LD doubles each, nb
+  // used); phase-1 step i of item j adds row f_off + j*f_stride + i - 1 (null: homogeneous)
+  const double *forc;
+  int nb;
+  long long f_off, f_stride;
 };
+constexpr int FORC_LD = 24;   // >= S*NL of every explicit scheme (ERK5+U5: 18)
 
 struct SweepCfg {
   int nt_threads;  // NT
@@ -131,12 +137,38 @@ struct RKCoarseArgs {
 };
 cudaError_t launch_rk_coarse(int scheme, SweepCfg cfg, const RKCoarseArgs &a, cudaStream_t s);
 
+// ---- Inflow/outflow boundaries (bounded.cu; PAPER.md 4.5, R20) ----
+// Host-derived tables of the inflow closure: t1[q][i] = dt^q (A^q 1)_i, t2[k][j] =
+// (k dx/alpha)^j / j!; z, A, b as in RKCoeffs; p = order of U_p, nq = p + S derivatives
+// g^(0..nq-1)(t_n) per time step.
+struct BndCoef {
+  int S, NL, NR, p, nq;
+  double t1[MAXS][MAXS];
+  double t2[4][MAXS];
+  double z[MAXZ];
+  double A[MAXS][MAXS];
+  double b[MAXS];
+};
+// b_n = Phi(0; t_n), n = 0..nt-1, from dg (nt x nq, device) into forc (nt x FORC_LD, device).
+cudaError_t launch_bnd_forcing(const BndCoef &c, const double *dg, long long nt, double *forc,
+                               cudaStream_t s);
+// Whole-row sweep with the boundary closures (explicit schemes; NT*P == nx, P >= p + 1).
+cudaError_t launch_rk_sweep_bnd(int scheme, SweepCfg cfg, const SweepArgs &a, cudaStream_t s);
+bool rk_sweep_bnd_supported(int scheme, SweepCfg cfg);
+cudaError_t launch_rk_coarse_bnd(int scheme, SweepCfg c, const RKCoarseArgs &a, cudaStream_t s);
+// Truncated-Toeplitz Psi: sequential solve (CoarseArgs semantics, out accumulated) and the
+// V-cycle level sweep / interpolation (PsiSweepArgs semantics of launch_psi_sweep).
+bool tpsi_cfg(int nx, bool seq, SweepCfg &cfg);
+cudaError_t launch_tpsi_seq(SweepCfg c, const CoarseArgs &a, cudaStream_t s);
+cudaError_t launch_tpsi_level(SweepCfg c, const PsiSweepArgs &a, cudaStream_t s);
+
 // Level-l (l >= 1) FULL-state primitives (levels.cu): rows n = n0 + j*nstride,
 // j = 0..nrows-1, y = Psi U[n-1] + g[n] (g null: 0).  mode 0: dst[n] = y;  mode 1:
 // r = y - U[n], per-block sum r^2 -> partials[j*bpr + b] (nullable), and if rstore is
 // set, r -> rstore row (roff + j).  bpr blocks of 256 threads per row (1..64).
 struct RowStepArgs {
   int nx, nrows, bpr, mode;
+  int trunc;       // 1: Psi truncated at the boundaries (no wrap), bounded.cu
   long long n0, nstride;
   const double *U;
   double *dst;

@@ -24,11 +24,16 @@ __global__ void __launch_bounds__(256) psi_rowstep_kernel(const __grid_constant_
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     double y = 0.0;
     int q = i + a.op.o0;
-    q %= nx;
-    if (q < 0) q += nx;
-    for (int k = 0; k < a.op.nu; ++k) {   // d = o0 + k ascending
-      y = fma(a.op.psi[k], src[q], y);
-      q = (q + 1 == nx) ? 0 : q + 1;
+    if (a.trunc) {   // Toeplitz, no wrap: taps outside [0, nx) read zero
+      for (int k = 0; k < a.op.nu; ++k, ++q)
+        if ((unsigned)q < (unsigned)nx) y = fma(a.op.psi[k], src[q], y);
+    } else {
+      q %= nx;
+      if (q < 0) q += nx;
+      for (int k = 0; k < a.op.nu; ++k) {   // d = o0 + k ascending
+        y = fma(a.op.psi[k], src[q], y);
+        q = (q + 1 == nx) ? 0 : q + 1;
+      }
     }
     if (g) y += g[i];
     if (a.mode == 0) {

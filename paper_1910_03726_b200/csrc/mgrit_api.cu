@@ -471,7 +471,7 @@ constexpr int kGraphHist = 4096;
 // Layout of the workspace (doubles unless noted).
 struct Layout {
   size_t u0, v0, g[MGRIT_MAX_LEVELS], u2[MGRIT_MAX_LEVELS], ul[MGRIT_MAX_LEVELS];
-  size_t partials, scal, sa, sb, hist, lstate, st_in, st_out, total;
+  size_t partials, scal, sa, sb, hist, lstate, st_in, st_out, forc, total;
   long long npart;
 };
 
@@ -509,6 +509,7 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
   L.sb = take(row);
   L.st_in = take(row);    // time shards: coarsest-chain state from the left neighbour
   L.st_out = take(row);   //              and to the right neighbour
+  L.forc = take((size_t)nt * FORC_LD * sizeof(double));   // inflow forcing rows b_n (R20)
   L.total = off;
   return true;
 }
@@ -518,6 +519,10 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
 struct mgrit_ctx {
   int nx, nt, m, levels, order, tableau, relax, scheme;
   int cycle = MGRIT_CYCLE_V;
+  // inflow/outflow boundaries (mgrit_set_inflow; PAPER.md 4.5, R20): Phi = Phi_h +
+  // forcing rows, every Psi truncated at the boundaries
+  int bc = 0;
+  double *forc = nullptr;   // workspace: nt x FORC_LD
   int final_sweep = MGRIT_FINAL_PREDICT;  // mgrit_set_final_sweep
   // mgrit_set_option: explicit replacements of measured defaults (n = 0: default)
   int opt_n[MGRIT_OPT_COUNT] = {0};
@@ -660,6 +665,17 @@ bool choose_fine(const mgrit_ctx *c, int steps, FineCfg &f) {
     cand[0][0] = c->opt_v[MGRIT_OPT_WHOLE_ROW][0];
     cand[0][1] = c->opt_v[MGRIT_OPT_WHOLE_ROW][1];
   }
+  if (c->bc) {  // inflow/outflow: whole rows whose last thread owns the p+1 extrapolation nodes
+    for (auto &cc : cand) {
+      if (cc[0] * cc[1] == nx && rk_sweep_bnd_supported(c->scheme, {cc[0], cc[1]})) {
+        f.cfg = {cc[0], cc[1]};
+        f.ntiles = 1;
+        f.HL = 0;
+        return true;
+      }
+    }
+    return false;
+  }
   for (auto &cc : cand) {
     if (cc[0] * cc[1] == nx && rk_sweep_supported(c->scheme, {cc[0], cc[1]})) {
       f.cfg = {cc[0], cc[1]};
@@ -774,6 +790,11 @@ int sweep(mgrit_ctx *c, int cls, SweepArgs a, int total_steps) {
   a.HL = f.HL;
   if (a.partials && (long long)a.nitems * a.ntiles > c->lay.npart)
     return fail(c, MGRIT_ENOMEM, "partials buffer too small");
+  if (c->bc) {  // forcing rows: phase-1 step i of item j adds b_n, n = f_off + j*f_stride + i - 1
+    a.forc = c->forc;
+    a.nb = c->tab.s * rk_scheme_reach_left(c->scheme);
+    return run(c, cls, [&] { return launch_rk_sweep_bnd(c->scheme, f.cfg, a, c->stream); });
+  }
   // halo tiles, even nx, no per-step writes: persistent TMA-pipelined kernel
   const bool tma = f.ntiles > 1 && (c->nx % 2 == 0) && (f.cfg.p % 2 == 1) && a.in.base;
   if (a.partials && tma && (long long)a.nitems * a.ntiles * (f.cfg.nt_threads / 32) > c->lay.npart)
@@ -927,7 +948,29 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
     SweepCfg cfg;
     if (!rk_coarse_cfg(c->nx, cfg))
       return fail(c, MGRIT_EUNSUPPORTED, "RK-form Psi supports nx in {64,128,...,4096}");
+    if (c->bc) {  // Psi = Phi_h^q with the boundary closures
+      if (c->nx == 4096 || !rk_sweep_bnd_supported(c->scheme, cfg))
+        return fail(c, MGRIT_EUNSUPPORTED, "inflow/outflow RK-form Psi: nx in {64,...,2048} and "
+                                           "points per thread > order");
+      return run(c, 2, [&] { return launch_rk_coarse_bnd(c->scheme, cfg, a, c->stream); });
+    }
     return run(c, 2, [&] { return launch_rk_coarse(c->scheme, cfg, a, c->stream); });
+  }
+  if (c->bc) {  // truncated Toeplitz Psi: one CTA, fixed coordinates (bounded.cu)
+    SweepCfg cfg;
+    if (!tpsi_cfg(c->nx, true, cfg))
+      return fail(c, MGRIT_EUNSUPPORTED, "inflow/outflow: nx in {64,128,...,4096}");
+    CoarseArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.nx = c->nx;
+    a.ntiles = 1;
+    a.nsteps = (int)N;
+    a.g = rm(c->g[l], 0, 1);
+    a.out = out;
+    a.state_in = state_in;
+    a.state_out = state_out;
+    a.op = c->op[l];
+    return run(c, 2, [&] { return launch_tpsi_seq(cfg, a, c->stream); });
   }
   const CoarsePlan pl = plan_coarse(c, l);
   if (pl.kind == CoarsePlan::NONE)
@@ -987,8 +1030,12 @@ int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout) {
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
   PsiCfg pc;
-  const bool tma = choose_level_tma(c->nx, m, 2 * m * (op.nu - 1), pc);
-  if (!tma && !choose_psi(c->nx, 2 * m * (op.nu - 1), true, pc))
+  const bool tma = !c->bc && choose_level_tma(c->nx, m, 2 * m * (op.nu - 1), pc);
+  if (c->bc) {
+    pc.ntiles = 1;
+    if (!tpsi_cfg(c->nx, false, pc.cfg))
+      return fail(c, MGRIT_EUNSUPPORTED, "inflow/outflow: nx in {64,128,...,4096}");
+  } else if (!tma && !choose_psi(c->nx, 2 * m * (op.nu - 1), true, pc))
     return fail(c, MGRIT_EUNSUPPORTED, "no level-sweep configuration");
   PsiSweepArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -1005,6 +1052,7 @@ int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout) {
   a.p2_items = p2_count(c, nc);
   a.v2 = a.out2 = kNone;
   a.op = op;
+  if (c->bc) return run(c, 1, [&] { return launch_tpsi_level(pc.cfg, a, c->stream); });
   if (tma) return run(c, 1, [&] { return launch_psi_level_tma(pc.cfg, a, c->stream); });
   return run(c, 1, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
 }
@@ -1017,8 +1065,12 @@ int level_interp(mgrit_ctx *c, int l, const double *usrc_rows, RowMap out_prev) 
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
   PsiCfg pc;
-  const bool tma = choose_level_tma(c->nx, m, (m - 1) * (op.nu - 1), pc);
-  if (!tma && !choose_psi(c->nx, (m - 1) * (op.nu - 1), true, pc))
+  const bool tma = !c->bc && choose_level_tma(c->nx, m, (m - 1) * (op.nu - 1), pc);
+  if (c->bc) {
+    pc.ntiles = 1;
+    if (!tpsi_cfg(c->nx, false, pc.cfg))
+      return fail(c, MGRIT_EUNSUPPORTED, "inflow/outflow: nx in {64,128,...,4096}");
+  } else if (!tma && !choose_psi(c->nx, (m - 1) * (op.nu - 1), true, pc))
     return fail(c, MGRIT_EUNSUPPORTED, "no interpolation configuration");
   PsiSweepArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -1035,8 +1087,9 @@ int level_interp(mgrit_ctx *c, int l, const double *usrc_rows, RowMap out_prev) 
   a.out2 = RowMap{out_prev.base, out_prev.off, out_prev.stride * m};
   a.v2 = tma ? kNone : a.out2;   // periodic kernel: out = v2 + x with v2 == out (in place)
   a.op = op;
-  int st = tma ? run(c, 3, [&] { return launch_psi_level_tma(pc.cfg, a, c->stream); })
-               : run(c, 3, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
+  int st = c->bc ? run(c, 3, [&] { return launch_tpsi_level(pc.cfg, a, c->stream); })
+           : tma ? run(c, 3, [&] { return launch_psi_level_tma(pc.cfg, a, c->stream); })
+                 : run(c, 3, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
   if (st) return st;
   // the last point n = nt_l (level l's last C-row): out[nt_l] += u_l[nc]
   const long long ntl = c->ntl[l];
@@ -1099,6 +1152,7 @@ RowStepArgs rowstep(const mgrit_ctx *c, int level, const double *U) {
   a.dst = const_cast<double *>(U);
   a.g = c->rhs[level];
   a.op = c->op[level];
+  a.trunc = c->bc;
   return a;
 }
 
@@ -1419,6 +1473,7 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
   c->hist_dev = (double *)(c->ws + c->lay.hist);
   c->st_in = (double *)(c->ws + c->lay.st_in);
   c->st_out = (double *)(c->ws + c->lay.st_out);
+  c->forc = (double *)(c->ws + c->lay.forc);
   c->lstate = (LoopState *)(c->ws + c->lay.lstate);
   c->guess = nullptr;
   c->have_iterate = false;
@@ -1483,6 +1538,72 @@ int mgrit_set_guess(mgrit_ctx *c, const double *guess_dev) {
   return MGRIT_OK;
 }
 
+int mgrit_set_inflow(mgrit_ctx *c, int enable, const double *dg_dev) {
+  if (!c) return MGRIT_EINVAL;
+  drop_graph(c);
+  if (!enable) {
+    c->bc = 0;
+    return MGRIT_OK;
+  }
+  if (c->implicit) return fail(c, MGRIT_EUNSUPPORTED, "inflow/outflow: explicit tableaux only (P:680)");
+  if (c->nranks > 1) return fail(c, MGRIT_EUNSUPPORTED, "inflow/outflow: not in time-shard mode");
+  const int old = c->bc;
+  c->bc = 1;
+  FineCfg f;
+  SweepCfg tc;
+  if (!choose_fine(c, c->m, f) || !tpsi_cfg(c->nx, true, tc)) {
+    c->bc = old;
+    return fail(c, MGRIT_EUNSUPPORTED,
+                "inflow/outflow needs whole rows: nx in {64,128,...,4096} with nx/32 > order "
+                "(nx >= 256 for order 5)");
+  }
+  if (!dg_dev) {  // homogeneous inflow u(-1, t) = 0
+    MG_CK(c, cudaMemsetAsync(c->forc, 0, (size_t)c->nt * FORC_LD * sizeof(double), c->stream));
+    return MGRIT_OK;
+  }
+  // tables of the Taylor / inverse-Lax-Wendroff ghost stage values (R20)
+  BndCoef b;
+  std::memset(&b, 0, sizeof(b));
+  const int S = c->tab.s;
+  b.S = S;
+  b.NL = rk_scheme_reach_left(c->scheme);
+  b.NR = rk_scheme_reach_right(c->scheme);
+  b.p = c->order;
+  b.nq = c->order + S;
+  double v[MAXS], w[MAXS];
+  for (int i = 0; i < S; ++i) v[i] = 1.0;
+  for (int q = 0; q < S; ++q) {   // v = A^q 1
+    for (int i = 0; i < S; ++i) b.t1[q][i] = std::pow(c->dt, q) * v[i];
+    for (int i = 0; i < S; ++i) {
+      double acc = 0.0;
+      for (int l = 0; l < S; ++l) acc += c->tab.A[i][l] * v[l];
+      w[i] = acc;
+    }
+    for (int i = 0; i < S; ++i) v[i] = w[i];
+  }
+  for (int k = 0; k < b.NL; ++k) {
+    double fact = 1.0;
+    for (int j = 0; j <= b.p; ++j) {
+      if (j > 0) fact *= j;
+      b.t2[k][j] = std::pow(k * c->dx / c->alpha, j) / fact;
+    }
+  }
+  std::memcpy(b.z, c->fine.z, sizeof(b.z));
+  for (int i = 0; i < MAXS; ++i) {
+    b.b[i] = c->tab.b[i];
+    for (int j = 0; j < MAXS; ++j) b.A[i][j] = c->tab.A[i][j];
+  }
+  return run(c, 5, [&] { return launch_bnd_forcing(b, dg_dev, c->nt, c->forc, c->stream); });
+}
+
+int mgrit_get_forcing(mgrit_ctx *c, double *out_dev) {
+  if (!c || !out_dev) return MGRIT_EINVAL;
+  if (!c->bc) return fail(c, MGRIT_EINVAL, "mgrit_set_inflow first");
+  MG_CK(c, cudaMemcpyAsync(out_dev, c->forc, (size_t)c->nt * FORC_LD * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c->stream));
+  return MGRIT_OK;
+}
+
 int mgrit_set_rhs(mgrit_ctx *c, int level, const double *g_dev) {
   if (!c) return MGRIT_EINVAL;
   if (level < 1 || level >= c->levels) return fail(c, MGRIT_EINVAL, "rhs level %d out of range", level);
@@ -1510,6 +1631,8 @@ int mgrit_relax(mgrit_ctx *c, int level, int kind, double *U) {
     a.nitems = (int)nc;
     a.nsteps1 = m - 1;
     a.in = rm(U, 0, m);
+    a.f_off = 0;
+    a.f_stride = m;
     a.each = rm(U, 0, m);
     a.each_step = 1;
     a.each_first = 1;
@@ -1521,6 +1644,8 @@ int mgrit_relax(mgrit_ctx *c, int level, int kind, double *U) {
     a.nitems = (int)nc;
     a.nsteps1 = 1;
     a.in = rm(U, m - 1, m);
+    a.f_off = m - 1;
+    a.f_stride = m;
     a.endw = rm(U, m, m);
     return sweep(c, 0, a, 1);
   };
@@ -1563,6 +1688,8 @@ static int residual0(mgrit_ctx *c, const double *U, double *n2_host, double *r_d
   a.nitems = c->nt;
   a.nsteps1 = 1;
   a.in = rm(U, 0, 1);
+  a.f_off = 0;
+  a.f_stride = 1;
   a.cmp = rm(U, 1, 1);
   a.partials = c->partials;
   if (r_dev) {
@@ -1710,6 +1837,8 @@ int mgrit_coarse_solve(mgrit_ctx *c, int level, double *U) {
   a.nitems = (int)nc;
   a.nsteps1 = 1;
   a.in = rm(U, m - 1, m);
+  a.f_off = m - 1;
+  a.f_stride = m;
   a.cmp = rm(U, m, m);
   a.dstore = rm(c->g[1], 1, 1);
   int st = sweep(c, 4, a, 1);
@@ -1757,6 +1886,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     SweepArgs a = base_sweep(c);
     a.nitems = (int)nc;
     a.nsteps1 = m;
+    a.f_off = 0;
+    a.f_stride = m;
     if (first && fcf) {
       a.in = rm(c->guess, 0, m);
       a.cmp = rm(c->guess, m, m);
@@ -1786,6 +1917,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     SweepArgs a = base_sweep(c);
     a.nitems = (int)nc;
     a.nsteps1 = m;
+    a.f_off = 0;
+    a.f_stride = m;
     a.in = rm(c->ucur, 0, 1);
     a.cmp = rm(c->ucur, 1, 1);
     a.partials = c->partials;
@@ -1909,6 +2042,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       SweepArgs a = base_sweep(c);
       a.nitems = (int)nc;
       a.nsteps1 = m - 1;
+      a.f_off = 0;
+      a.f_stride = m;
       a.in = rm(c->ucur, 0, 1);
       a.each = rm(out_dev, 0, m);
       a.each_step = 1;
@@ -2073,6 +2208,8 @@ int mgrit_solve_shard(mgrit_ctx *c, const mgrit_comm *comm, double tol, int max_
     SweepArgs a = base_sweep(c);
     a.nitems = (int)nc;
     a.nsteps1 = m;
+    a.f_off = 0;
+    a.f_stride = m;
     if (first && fcf) {
       a.in = rm(c->guess, 0, m);
       a.cmp = rm(c->guess, m, m);
@@ -2135,6 +2272,8 @@ int mgrit_solve_shard(mgrit_ctx *c, const mgrit_comm *comm, double tol, int max_
       SweepArgs a = base_sweep(c);
       a.nitems = (int)nc;
       a.nsteps1 = m - 1;
+      a.f_off = 0;
+      a.f_stride = m;
       a.in = rm(c->ucur, 0, 1);
       a.each = rm(out_dev, 0, m);
       a.each_step = 1;

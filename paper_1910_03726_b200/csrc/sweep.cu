@@ -14,142 +14,12 @@
 // all-row residual) and the final F-point materialisation via RowMaps.
 #include "kernels.h"
 #include "tma.cuh"
+#include "rows.cuh"
 
 #include <algorithm>
 #include <type_traits>
 
 namespace mg {
-
-// One step of Phi: explicit stage form, or SDIRK with periodic banded stage solves.
-template <class SC, int P, int NT, class FS = FusedRT>
-__device__ __forceinline__ void phi_step(double (&x)[P], const SweepArgs &a, double *edge,
-                                         int &phase, double *wbuf, int &wphase) {
-  if constexpr (SC::implicit)
-    dirk_step<SC, P, NT, FS>(x, a.co, a.sd, edge, phase, wbuf, wphase);
-  else
-    erk_step<SC, P, NT>(x, a.co, edge, phase);
-}
-
-// Persistent: each CTA walks work items (item, tile) with a grid stride and prefetches
-// the next item's input / comparison windows with per-thread cp.async copies (padded
-// layout) into the other buffer pair while it computes the current one, so a whole-row
-// CTA (one per SM for the 512-thread SDIRK and ERK5 rows) never idles on a cold load.
-template <class SC, int NT, int P, class FS = FusedRT>
-__global__ void __launch_bounds__(NT, 1) rk_sweep_kernel(const __grid_constant__ SweepArgs a) {
-  constexpr int SP = Pad<P>::SP;
-  constexpr int W = NT * P;
-  constexpr int NW = NT / 32;
-  extern __shared__ double smem[];
-  double *bufA = smem;                   // [2][NT*SP] input windows
-  double *bufB = bufA + 2 * NT * SP;     // [2][NT*SP] comparison windows
-  double *edge = bufB + 2 * NT * SP;
-  double *red = edge + 2 * NT * (SC::NL + SC::NR) + 2;
-  double *wbuf = red + NW + 2;  // 16*NW (SDIRK recurrences: 2 phases x <= 8 slots) + lane tables
-  int wphase = 0;
-  const int nx = a.nx;
-  const int total = a.nitems * a.ntiles;
-  const int tid = threadIdx.x;
-  int phase = 0;
-
-  auto rowp = [&](const RowMap &r, long long j) -> const double * {
-    return r.base + (r.off + j * r.stride) * (long long)nx;
-  };
-  auto span = [&](int w, int &item, int &abeg, int &T, int &start) {
-    item = w / a.ntiles;
-    const int tile = w - item * a.ntiles;
-    abeg = (int)(((long long)tile * nx) / a.ntiles);
-    T = (int)(((long long)(tile + 1) * nx) / a.ntiles) - abeg;
-    start = abeg - a.HL;
-    if (start < 0) start += nx;
-  };
-  // this thread's copies of item w's windows into buffer pair b (one cp.async group)
-  auto issue = [&](int w, int b) {
-    if (w < total) {
-      int item, abeg, T, start;
-      span(w, item, abeg, T, start);
-      const double *ri = a.in.base ? rowp(a.in, item) : nullptr;
-      const double *rc = a.cmp.base ? rowp(a.cmp, item) : nullptr;
-      for (int q = tid; q < W; q += NT) {
-        int g = start + q;
-        if (g >= nx) g -= nx;
-        if (ri) cp_async8(bufA + b * NT * SP + pidx<P>(q), ri + g);
-        if (rc) cp_async8(bufB + b * NT * SP + pidx<P>(q), rc + g);
-      }
-    }
-    cp_async_commit();
-  };
-  if constexpr (SC::implicit)
-    if (a.sd.fused) fused_lane_tables<SC::NL, SC::NR, NT>(a.sd, wbuf);
-  issue(blockIdx.x, 0);
-  int it = 0;
-#pragma unroll 1
-  for (int w = blockIdx.x; w < total; w += gridDim.x, ++it) {
-    const int b = it & 1;
-    issue(w + gridDim.x, b ^ 1);          // buffers b^1 were released by the last barrier
-    cp_async_wait<1>();                   // this thread's copies of item w landed
-    __syncthreads();                      // ... and everybody else's
-    double *sA = bufA + b * NT * SP, *sB = bufB + b * NT * SP;
-    int item, abeg, T, start;
-    span(w, item, abeg, T, start);
-    // Store the T owned outputs [abeg, aend) of a register vector (coalesced via sA).
-    auto store_slice = [&](double *row, const double(&v)[P]) {
-      __syncthreads();
-#pragma unroll
-      for (int p = 0; p < P; ++p) sA[tid * SP + p] = v[p];
-      __syncthreads();
-      for (int q = tid; q < T; q += NT) row[abeg + q] = sA[pidx<P>(a.HL + q)];
-    };
-    double x[P];
-#pragma unroll
-    for (int p = 0; p < P; ++p) x[p] = a.in.base ? sA[tid * SP + p] : 0.0;
-
-    // ---- phase 1: nsteps1 steps of Phi --------------------------------------
-    if (a.each_first == 0 && a.each_last >= 0)
-      store_slice(const_cast<double *>(a.each.base) +
-                      (a.each.off + item * a.each.stride) * (long long)nx, x);
-#pragma unroll 1
-    for (int i = 1; i <= a.nsteps1; ++i) {
-      phi_step<SC, P, NT, FS>(x, a, edge, phase, wbuf, wphase);
-      if (i >= a.each_first && i <= a.each_last)
-        store_slice(const_cast<double *>(a.each.base) +
-                        (a.each.off + item * a.each.stride + i * a.each_step) * (long long)nx,
-                    x);
-    }
-    if (a.endw.base) store_slice(const_cast<double *>(rowp(a.endw, item)), x);
-
-    if (a.cmp.base) {
-      double d[P];
-#pragma unroll
-      for (int p = 0; p < P; ++p) d[p] = x[p] - sB[tid * SP + p];
-      if (a.partials) {
-        double s = 0.0;
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const int l = tid * P + p;
-          if (l >= a.HL && l < a.HL + T) s = fma(d[p], d[p], s);
-        }
-        s = block_sum<NT>(s, red);
-        if (tid == 0) a.partials[w] = s;
-      }
-      if (a.dstore.base) {
-        const int jj = item + a.d_phase;
-        if (jj % a.d_every == 0)
-          store_slice(const_cast<double *>(rowp(a.dstore, jj / a.d_every)), d);
-      }
-      // ---- phase 2: r = Phi^m delta ------------------------------------------
-      if (a.nsteps2 > 0 && item < a.p2_items) {
-#pragma unroll
-        for (int p = 0; p < P; ++p) x[p] = d[p];
-#pragma unroll 1
-        for (int i = 1; i <= a.nsteps2; ++i) phi_step<SC, P, NT, FS>(x, a, edge, phase, wbuf, wphase);
-        store_slice(const_cast<double *>(rowp(a.r2, item)), x);
-      }
-    }
-    __syncthreads();                      // buffers b (and the staging in sA) are free
-  }
-  cp_async_wait<0>();
-}
-
 
 // ---------------------------------------------------------------------------
 // Persistent, TMA-pipelined variant for halo-tile mode (odd P => contiguous
@@ -555,28 +425,6 @@ int rk_scheme_stages(int scheme) {
   return (scheme >= 0 && scheme < 9) ? t[scheme] : -1;
 }
 bool rk_scheme_implicit(int scheme) { return scheme >= 5 && scheme < 9; }
-
-template <class SC, int NT, int P, class FS = FusedRT>
-static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
-  constexpr int SP = Pad<P>::SP;
-  const size_t smem = sizeof(double) * (4 * NT * SP + 2 * NT * (SC::NL + SC::NR) + 2 +
-                                        NT / 32 + 2 + 16 * (NT / 32) + 8 * 32 + 2);
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(rk_sweep_kernel<SC, NT, P, FS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, rk_sweep_kernel<SC, NT, P, FS>, NT, smem);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long total = (long long)a.nitems * a.ntiles;
-  if (total <= 0) return cudaSuccess;
-  const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
-  rk_sweep_kernel<SC, NT, P, FS><<<(unsigned)grid, NT, smem, s>>>(a);
-  return cudaGetLastError();
-}
 
 #define MG_CFGS(X)                                                                          \
   X(32, 2) X(32, 4) X(32, 8) X(64, 8) X(128, 8) X(256, 8) X(512, 8) X(128, 11) X(256, 11) X(128, 15)
