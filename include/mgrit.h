@@ -259,6 +259,13 @@ int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
  *   MGRIT_OPT_STAGE_FORM     0 | 1               1: explicit steps in the plain Runge-Kutta
  *                                                stage form (no folded last stage, no
  *                                                Shu-Osher SSP-RK3; R5)
+ *   MGRIT_OPT_OVERLAP        C                   two-level host-loop solves: the sequential
+ *                                                coarse chain in C chunks on a private
+ *                                                high-priority stream, each followed at once
+ *                                                by the next iteration's sweep over the
+ *                                                intervals it corrected (bitwise the serial
+ *                                                iteration); 0 or 1: serial; default 8 for
+ *                                                chains of >= 1024 steps
  * Errors: EINVAL (unknown option, wrong count, negative value); EUNSUPPORTED if the new
  * whole-row / SDIRK setting cannot factor the stage solves (the old setting is kept).
  */
@@ -272,7 +279,8 @@ typedef enum {
   MGRIT_OPT_SDIRK_PRODUCT = 6,
   MGRIT_OPT_STAGE_FORM = 7,
   MGRIT_OPT_GRAPH = 8,
-  MGRIT_OPT_COUNT = 9
+  MGRIT_OPT_OVERLAP = 9,
+  MGRIT_OPT_COUNT = 10
 } mgrit_option;
 int mgrit_set_option(mgrit_ctx *ctx, int option, const int *values, int n);
 

@@ -44,6 +44,9 @@ struct SweepArgs {
   const double *forc;
   int nb;
   long long f_off, f_stride;
+  // SMs left free for a concurrently running kernel (the overlapped two-level coarse
+  // solve's 16-CTA cluster): the persistent grid is sized for sms - reserve_sms
+  int reserve_sms;
 };
 constexpr int FORC_LD = 24;   // >= S*NL of every explicit scheme (ERK5+U5: 18)
 

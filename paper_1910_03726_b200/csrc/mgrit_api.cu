@@ -554,6 +554,10 @@ struct mgrit_ctx {
   LoopState *lstate;      // graph mode: k, stop flags, tol
   cudaGraphExec_t gexec = nullptr;   // cached loop graph (invalidated by setters)
   long long glaunch[2] = {0, 0};     // kernels per captured iteration body (A, B)
+  // overlapped two-level iteration: the coarse chain's chunks run on a private
+  // high-priority stream while the next sweep's chunks follow on the caller's stream
+  cudaStream_t hstream = nullptr;
+  std::vector<cudaEvent_t> hev;
   cudaStream_t gstream = nullptr;    // private capture/launch stream (the caller's may be
   cudaEvent_t gevent = nullptr;      //   the legacy default stream, which cannot capture)
   double *ucur, *unext;   // fine C-rows: current iterate / next (FCF ping-pong of u0b, v0b)
@@ -931,9 +935,12 @@ static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
   return pl;
 }
 
+// (n0, nsteps >= 0): only steps n0+1 .. n0+nsteps of the chain (a chunk of the overlapped
+// two-level iteration; stencil Psi with a cluster / single-CTA plan), nsteps < 0: all.
 int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
-                       const double *state_in = nullptr, double *state_out = nullptr) {
-  const long long N = c->ntl[l];
+                       const double *state_in = nullptr, double *state_out = nullptr,
+                       long long n0 = 0, long long nsteps = -1) {
+  const long long N = nsteps >= 0 ? nsteps : c->ntl[l];
   if (c->psi_kind != MGRIT_PSI_STENCIL) {
     RKCoarseArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -980,7 +987,7 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
   a.nx = c->nx;
   a.ntiles = pl.ntiles;
   a.nsteps = (int)N;
-  a.n0 = 0;
+  a.n0 = n0;
   a.g = rm(c->g[l], 0, 1);
   a.out = out;
   a.state_in = state_in;
@@ -1499,6 +1506,8 @@ void mgrit_destroy(mgrit_ctx *c) {
   drop_graph(c);
   if (c->gevent) cudaEventDestroy(c->gevent);
   if (c->gstream) cudaStreamDestroy(c->gstream);
+  for (auto e : c->hev) cudaEventDestroy(e);
+  if (c->hstream) cudaStreamDestroy(c->hstream);
   delete c;
 }
 
@@ -1758,8 +1767,8 @@ int mgrit_set_final_sweep(mgrit_ctx *c, int mode) {
 
 int mgrit_set_option(mgrit_ctx *c, int option, const int *values, int n) {
   if (!c) return MGRIT_EINVAL;
-  static const int kMin[MGRIT_OPT_COUNT] = {2, 2, 3, 1, 1, 2, 1, 1, 1};
-  static const int kMax[MGRIT_OPT_COUNT] = {3, 2, 3, 1, 1, 2, 1, 1, 1};
+  static const int kMin[MGRIT_OPT_COUNT] = {2, 2, 3, 1, 1, 2, 1, 1, 1, 1};
+  static const int kMax[MGRIT_OPT_COUNT] = {3, 2, 3, 1, 1, 2, 1, 1, 1, 1};
   if (option < 0 || option >= MGRIT_OPT_COUNT) return fail(c, MGRIT_EINVAL, "unknown option %d", option);
   if (n != 0 && (n < kMin[option] || n > kMax[option] || !values))
     return fail(c, MGRIT_EINVAL, "option %d takes %d..%d values", option, kMin[option], kMax[option]);
@@ -1882,31 +1891,91 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   if (!choose_fine(c, fcf ? 2 * m : m, f)) return fail(c, MGRIT_EUNSUPPORTED, "no sweep cfg");
   // FCF sweep: reads the current C-rows (the guess's at k = 0), writes v into `unext`
   // (the next iterate before its coarse correction), delta norm, r -> g_1.
-  auto do_sweep = [&](bool first, bool want_norm) -> int {
+  // (j0, cnt): only the intervals j0 .. j0+cnt-1 (a chunk of the overlapped iteration, with
+  // `reserve` SMs left to the concurrent coarse chain); cnt < 0: all.
+  auto do_sweep = [&](bool first, bool want_norm, long long j0 = 0, long long cnt = -1,
+                      int reserve = 0) -> int {
+    if (cnt < 0) cnt = nc - j0;
     SweepArgs a = base_sweep(c);
-    a.nitems = (int)nc;
+    a.nitems = (int)cnt;
     a.nsteps1 = m;
-    a.f_off = 0;
+    a.f_off = j0 * m;
     a.f_stride = m;
+    a.reserve_sms = reserve;
     if (first && fcf) {
-      a.in = rm(c->guess, 0, m);
-      a.cmp = rm(c->guess, m, m);
+      a.in = rm(c->guess, j0 * m, m);
+      a.cmp = rm(c->guess, (j0 + 1) * m, m);
     } else {
-      a.in = rm(c->ucur, 0, 1);
-      a.cmp = rm(c->ucur, 1, 1);
+      a.in = rm(c->ucur, j0, 1);
+      a.cmp = rm(c->ucur, j0 + 1, 1);
     }
-    a.partials = want_norm ? c->partials : nullptr;
+    a.partials = want_norm ? c->partials + partial_count(c, j0, fcf ? 2 * m : m) : nullptr;
     if (fcf) {
-      a.endw = rm(c->unext, 1, 1);
+      a.endw = rm(c->unext, j0 + 1, 1);
       a.nsteps2 = m;
-      a.p2_items = (int)nc - 1;
-      a.r2 = rm(c->g[1], 2, 1);
+      a.p2_items = (int)std::max<long long>(0, std::min<long long>(cnt, nc - 1 - j0));
+      a.r2 = rm(c->g[1], j0 + 2, 1);
     } else {
-      a.dstore = rm(c->g[1], 1, 1);
+      a.dstore = rm(c->g[1], j0 + 1, 1);
       a.d_every = 1;
       a.d_phase = 0;
     }
     return sweep(c, 0, a, fcf ? 2 * m : m);
+  };
+  // Overlapped two-level iteration (option MGRIT_OPT_OVERLAP = number of chunks C, default 8
+  // for long chains): the sequential coarse chain runs as C chunks of nc/C steps on a
+  // private high-priority stream (the chain state is carried from chunk to chunk); as soon
+  // as chunk i has corrected its C-rows, the next iteration's fused sweep over those
+  // intervals follows on the caller's stream, beside chunk i+1, on the SMs the 16-CTA
+  // cluster leaves free.  Ordering is by CUDA events only (no kernel waits on another).
+  // Sweep chunk i covers the intervals [iL-1, (i+1)L-1) (the last one up to nc): it reads
+  // the C-rows <= (i+1)L, which chunk i has corrected, and overwrites the coarse right-hand
+  // side rows <= (i+1)L, which chunk i has consumed.  Same kernels on the same data in the
+  // same order per row: results are bitwise those of the serial iteration.
+  int nchunks = 0;
+  if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL && !c->bc && !c->prof) {
+    const CoarsePlan pl = plan_coarse(c, 1);
+    const bool chain = pl.kind == CoarsePlan::CLUSTER || pl.kind == CoarsePlan::CLUSTER_CA ||
+                       pl.kind == CoarsePlan::SEQ;
+    int want = opt(c, MGRIT_OPT_OVERLAP) ? c->opt_v[MGRIT_OPT_OVERLAP][0] : (nc >= 1024 ? 8 : 0);
+    while (want > 1 && (nc % want || nc / want < 32)) --want;
+    if (chain && want > 1) nchunks = want;
+  }
+  auto overlapped_iteration = [&]() -> int {
+    const int C_ = nchunks;
+    const long long L = nc / C_;
+    if (!c->hstream) {
+      int lo = 0, hi = 0;
+      MG_CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      MG_CK(c, cudaStreamCreateWithPriority(&c->hstream, cudaStreamNonBlocking, hi));
+    }
+    while ((int)c->hev.size() < C_ + 1) {
+      cudaEvent_t e = nullptr;
+      MG_CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->hev.push_back(e);
+    }
+    const cudaStream_t user = c->stream;
+    double *corr = fcf ? c->unext : c->ucur;   // C-rows receiving += e
+    MG_CK(c, cudaEventRecord(c->hev[C_], user));            // the previous sweep is complete
+    MG_CK(c, cudaStreamWaitEvent(c->hstream, c->hev[C_], 0));
+    if (fcf) std::swap(c->ucur, c->unext);                  // the sweeps below read `corr`
+    double *st2[2] = {c->sa, c->sb};
+    int s2 = MGRIT_OK;
+    for (int i = 0; i < C_ && !s2; ++i) {
+      c->stream = c->hstream;
+      s2 = coarse_solve_level(c, 1, rm(corr, 0, 1), rm(corr, 0, 1),
+                              i == 0 ? nullptr : st2[(i + 1) & 1],
+                              i + 1 < C_ ? st2[i & 1] : nullptr, i * L, L);
+      c->stream = user;
+      if (s2) break;
+      MG_CK(c, cudaEventRecord(c->hev[i], c->hstream));
+      MG_CK(c, cudaStreamWaitEvent(user, c->hev[i], 0));
+      const long long j0 = i == 0 ? 0 : i * L - 1;
+      const long long j1 = i + 1 < C_ ? (i + 1) * L - 1 : nc;
+      s2 = do_sweep(false, true, j0, j1 - j0, i + 1 < C_ ? 16 : 0);
+    }
+    c->stream = user;
+    return s2;
   };
   // Check+materialise sweep: phase 1 of the fused sweep (same tiles, so the same norm
   // partials, bit for bit) with per-step writes of the FULL iterate into out_dev and no
@@ -1995,22 +2064,27 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       Range nv_it("iteration");
       // coarse-grid correction: (FCF) unext += E, then unext becomes the iterate;
       // (F) ucur += e in place
-      st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
-      if (st) return st;
-      if (fcf) std::swap(c->ucur, c->unext);
-      c->have_iterate = true;
-      ++k;
-      if (crows_hist)
-        MG_CK(c, cudaMemcpyAsync(crows_hist + (size_t)(k - 1) * (nc + 1) * nx, c->ucur,
-                                 (nc + 1) * row, cudaMemcpyDeviceToDevice, c->stream));
-      // residual of iterate k (computed by the next sweep).  Predicted last: the
+      // residual of iterate k+1 (computed by the next sweep).  Predicted last: the
       // previous two residuals extrapolated geometrically fall below tol.
+      ++k;
       bool last = false;
       if (out_dev && c->final_sweep != MGRIT_FINAL_OFF) {
         if (k >= max_iter || c->final_sweep == MGRIT_FINAL_ALWAYS) last = true;
         else if (k >= 2 && h[k - 1] < h[k - 2]) last = h[k - 1] * (h[k - 1] / h[k - 2]) < tol;
       }
-      st = last ? check_sweep() : do_sweep(false, true);
+      const bool ovl = nchunks > 1 && !last;
+      if (ovl) {
+        st = overlapped_iteration();   // coarse chunks || the next sweep's chunks
+      } else {
+        st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
+        if (!st && fcf) std::swap(c->ucur, c->unext);
+      }
+      if (st) return st;
+      c->have_iterate = true;
+      if (crows_hist)
+        MG_CK(c, cudaMemcpyAsync(crows_hist + (size_t)(k - 1) * (nc + 1) * nx, c->ucur,
+                                 (nc + 1) * row, cudaMemcpyDeviceToDevice, c->stream));
+      if (!ovl) st = last ? check_sweep() : do_sweep(false, true);
       if (st) return st;
       double n2;
       st = reduce_norm(c, partial_count(c, nc, fcf ? 2 * m : m), &n2);

@@ -257,7 +257,8 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long total = (long long)a.nitems * a.ntiles;
   if (total <= 0) return cudaSuccess;
-  const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
+  const long long grid = std::min<long long>(
+      total, (long long)std::max(1, sms - a.reserve_sms) * blocks_per_sm);
   rk_sweep_tma_kernel<SC, NT, P, MINB><<<(unsigned)grid, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -381,7 +382,8 @@ static cudaError_t launch_residual_one(const SweepArgs &a, int chunk, cudaStream
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long total = (long long)((a.nitems + chunk - 1) / chunk) * a.ntiles;
   if (total <= 0) return cudaSuccess;
-  const long long grid = std::min<long long>(total, (long long)sms * blocks_per_sm);
+  const long long grid = std::min<long long>(
+      total, (long long)std::max(1, sms - a.reserve_sms) * blocks_per_sm);
   rk_residual_tma_kernel<SC, NT, P><<<(unsigned)grid, NT, smem, s>>>(a, chunk);
   return cudaGetLastError();
 }
