@@ -260,12 +260,14 @@ int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
  *                                                stage form (no folded last stage, no
  *                                                Shu-Osher SSP-RK3; R5)
  *   MGRIT_OPT_OVERLAP        C                   two-level host-loop solves: the sequential
- *                                                coarse chain in C chunks on a private
- *                                                high-priority stream, each followed at once
- *                                                by the next iteration's sweep over the
- *                                                intervals it corrected (bitwise the serial
- *                                                iteration); 0 or 1: serial; default 8 for
- *                                                chains of >= 1024 steps
+ *                                                coarse chain runs on a private high-priority
+ *                                                stream and publishes its progress every
+ *                                                nc/C steps; the next iteration's sweep over
+ *                                                the intervals already corrected follows
+ *                                                beside it, released by stream-ordered memory
+ *                                                waits (bitwise the serial iteration); 0 or
+ *                                                1: serial; default 16 (chains >= 2048
+ *                                                steps) / 8 (>= 1024)
  * Errors: EINVAL (unknown option, wrong count, negative value); EUNSUPPORTED if the new
  * whole-row / SDIRK setting cannot factor the stage solves (the old setting is kept).
  */

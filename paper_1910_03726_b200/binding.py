@@ -18,6 +18,8 @@ LIB_PATH = os.path.join(HERE, "libmgrit.so")
 # ABI, random sleeps at the asynchronous protocol points).  No CPU fallback either way.
 if os.environ.get("MGRIT_LIBRARY") == "jitter":
     LIB_PATH = os.path.join(HERE, "libmgrit_jitter.so")
+elif os.environ.get("MGRIT_LIBRARY") == "trace":   # -DMG_TRACE build (tools/trace_overlap.sh)
+    LIB_PATH = os.path.join(HERE, "libmgrit_trace.so")
 
 TABLEAU = {"erk1": 0, "erk2": 1, "erk3_ssp": 2, "erk3_kutta": 3, "erk4": 4, "erk5": 5,
            "sdirk1": 6, "sdirk2": 7, "sdirk3": 8, "sdirk4": 9}

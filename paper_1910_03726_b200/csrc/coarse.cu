@@ -1027,6 +1027,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
       bulk_wait_read_all();
       __syncwarp();
       if (q == 0) mbar_arrive(&ofree[t % 3]);
+      // progress: rows <= n0 + 4(t+1) of this CTA's slice are complete in global memory once
+      // the issuing lanes' bulk groups have completed (not only read); release at system
+      // scope for the stream-ordered wait
+      if (a.progress && (4 * (t + 1)) % a.prog_every == 0) {
+        bulk_wait_all();
+        __syncwarp();
+        if (q == 0) {
+          __threadfence_system();
+          atomicAdd_system(a.progress, 1ull);
+        }
+      }
       // g set of half t read by every compute thread -> reload it with half t + 3
       if (t + 3 < H) {
         mbar_wait(&gfree[t % 3], (uint32_t)((t / 3) & 1));

@@ -89,6 +89,11 @@ struct CoarseArgs {
   RowMap out;      // out row n (accumulated)
   const double *state_in;  // x_{n0} (nx), null: zero
   double *state_out;       // x_{n0+nsteps} (nx), null: not stored
+  // progress counter (psi_seq_cluster_tb_kernel; null: none): every CTA of the cluster adds 1
+  // once its slice of the rows out_n, n <= n0 + k*prog_every, is complete in global memory
+  // (k = 1, 2, ...); a stream-ordered cuStreamWaitValue64 releases dependent work
+  unsigned long long *progress;
+  int prog_every;          // steps per publication (multiple of 4, divides nsteps)
   PsiOp op;
 };
 cudaError_t launch_psi_coarse(SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);

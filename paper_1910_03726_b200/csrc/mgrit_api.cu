@@ -471,7 +471,7 @@ constexpr int kGraphHist = 4096;
 // Layout of the workspace (doubles unless noted).
 struct Layout {
   size_t u0, v0, g[MGRIT_MAX_LEVELS], u2[MGRIT_MAX_LEVELS], ul[MGRIT_MAX_LEVELS];
-  size_t partials, scal, sa, sb, hist, lstate, st_in, st_out, forc, total;
+  size_t partials, scal, sa, sb, hist, lstate, st_in, st_out, forc, prog, total;
   long long npart;
 };
 
@@ -510,6 +510,7 @@ bool make_layout(int nx, int nt, int m, int levels, Layout &L) {
   L.st_in = take(row);    // time shards: coarsest-chain state from the left neighbour
   L.st_out = take(row);   //              and to the right neighbour
   L.forc = take((size_t)nt * FORC_LD * sizeof(double));   // inflow forcing rows b_n (R20)
+  L.prog = take(64);      // progress counter of the overlapped two-level chain
   L.total = off;
   return true;
 }
@@ -558,6 +559,8 @@ struct mgrit_ctx {
   // high-priority stream while the next sweep's chunks follow on the caller's stream
   cudaStream_t hstream = nullptr;
   std::vector<cudaEvent_t> hev;
+  unsigned long long *prog = nullptr;      // workspace: chain progress counter
+  void *wait_value_fn = nullptr;           // cuStreamWaitValue64 (driver entry point)
   cudaStream_t gstream = nullptr;    // private capture/launch stream (the caller's may be
   cudaEvent_t gevent = nullptr;      //   the legacy default stream, which cannot capture)
   double *ucur, *unext;   // fine C-rows: current iterate / next (FCF ping-pong of u0b, v0b)
@@ -939,7 +942,8 @@ static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
 // two-level iteration; stencil Psi with a cluster / single-CTA plan), nsteps < 0: all.
 int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
                        const double *state_in = nullptr, double *state_out = nullptr,
-                       long long n0 = 0, long long nsteps = -1) {
+                       long long n0 = 0, long long nsteps = -1,
+                       unsigned long long *progress = nullptr, int prog_every = 0) {
   const long long N = nsteps >= 0 ? nsteps : c->ntl[l];
   if (c->psi_kind != MGRIT_PSI_STENCIL) {
     RKCoarseArgs a;
@@ -993,6 +997,12 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
   a.state_in = state_in;
   a.state_out = state_out;
   a.op = c->op[l];
+  if (progress) {
+    if (!(pl.kind == CoarsePlan::CLUSTER_CA && pl.tb))
+      return fail(c, MGRIT_EUNSUPPORTED, "progress counter: warp-specialised cluster solve only");
+    a.progress = progress;
+    a.prog_every = prog_every;
+  }
   switch (pl.kind) {
     case CoarsePlan::CLUSTER:
       return run(c, 2, [&] { return launch_psi_seq_cluster(pl.cl, pl.cfg, a, c->stream); });
@@ -1481,6 +1491,9 @@ int mgrit_setup(mgrit_ctx **out, int nx, int nt, int m, double alpha, double cfl
   c->st_in = (double *)(c->ws + c->lay.st_in);
   c->st_out = (double *)(c->ws + c->lay.st_out);
   c->forc = (double *)(c->ws + c->lay.forc);
+  c->prog = (unsigned long long *)(c->ws + c->lay.prog);
+  if (cudaMemsetAsync(c->prog, 0, 64, c->stream) != cudaSuccess)
+    return bad(MGRIT_ECUDA, "memset of the progress counter failed");
   c->lstate = (LoopState *)(c->ws + c->lay.lstate);
   c->guess = nullptr;
   c->have_iterate = false;
@@ -1923,23 +1936,37 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     return sweep(c, 0, a, fcf ? 2 * m : m);
   };
   // Overlapped two-level iteration (option MGRIT_OPT_OVERLAP = number of chunks C, default 8
-  // for long chains): the sequential coarse chain runs as C chunks of nc/C steps on a
-  // private high-priority stream (the chain state is carried from chunk to chunk); as soon
-  // as chunk i has corrected its C-rows, the next iteration's fused sweep over those
-  // intervals follows on the caller's stream, beside chunk i+1, on the SMs the 16-CTA
-  // cluster leaves free.  Ordering is by CUDA events only (no kernel waits on another).
+  // for long chains): the sequential coarse chain runs as ONE launch of the 16-CTA
+  // cluster kernel on a private high-priority stream and publishes a progress counter every
+  // L = nc/C steps; as soon as chunk i's C-rows are corrected, the next iteration's fused
+  // sweep over those intervals follows on the caller's stream, beside the running chain, on
+  // the SMs the cluster leaves free.  The sweeps are released by stream-ordered memory waits
+  // (cuStreamWaitValue64 on the counter): no kernel waits on another, so there is no
+  // co-residency requirement.
   // Sweep chunk i covers the intervals [iL-1, (i+1)L-1) (the last one up to nc): it reads
   // the C-rows <= (i+1)L, which chunk i has corrected, and overwrites the coarse right-hand
   // side rows <= (i+1)L, which chunk i has consumed.  Same kernels on the same data in the
   // same order per row: results are bitwise those of the serial iteration.
   int nchunks = 0;
-  if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL && !c->bc && !c->prof) {
+  if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL && !c->bc && !c->prof && c->nranks == 1) {
     const CoarsePlan pl = plan_coarse(c, 1);
-    const bool chain = pl.kind == CoarsePlan::CLUSTER || pl.kind == CoarsePlan::CLUSTER_CA ||
-                       pl.kind == CoarsePlan::SEQ;
-    int want = opt(c, MGRIT_OPT_OVERLAP) ? c->opt_v[MGRIT_OPT_OVERLAP][0] : (nc >= 1024 ? 8 : 0);
-    while (want > 1 && (nc % want || nc / want < 32)) --want;
+    const bool chain = pl.kind == CoarsePlan::CLUSTER_CA && pl.tb;
+    // default: 16 chunks of >= 128 steps (measured, profiles/r02_overlap_ab.txt)
+    int want = opt(c, MGRIT_OPT_OVERLAP) ? c->opt_v[MGRIT_OPT_OVERLAP][0]
+                                         : (nc >= 2048 ? 16 : (nc >= 1024 ? 8 : 0));
+    while (want > 1 && (nc % want || (nc / want) % 4 || nc / want < 32)) --want;
     if (chain && want > 1) nchunks = want;
+    if (nchunks && !c->wait_value_fn) {   // stream-ordered memory wait (driver entry point)
+      cudaDriverEntryPointQueryResult qr;
+      void *fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+          qr != cudaDriverEntryPointSuccess || !fn) {
+        cudaGetLastError();
+        nchunks = 0;                      // not available: serial iteration
+      } else {
+        c->wait_value_fn = fn;
+      }
+    }
   }
   auto overlapped_iteration = [&]() -> int {
     const int C_ = nchunks;
@@ -1949,32 +1976,62 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       MG_CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
       MG_CK(c, cudaStreamCreateWithPriority(&c->hstream, cudaStreamNonBlocking, hi));
     }
-    while ((int)c->hev.size() < C_ + 1) {
+    while ((int)c->hev.size() < 1) {
       cudaEvent_t e = nullptr;
       MG_CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       c->hev.push_back(e);
     }
     const cudaStream_t user = c->stream;
+#ifdef MG_TRACE   // tools/trace_overlap.sh: timeline of the chunks (timing events)
+    std::vector<cudaEvent_t> tev(C_ + 2);
+    for (auto &e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[C_], user);
+#endif
     double *corr = fcf ? c->unext : c->ucur;   // C-rows receiving += e
-    MG_CK(c, cudaEventRecord(c->hev[C_], user));            // the previous sweep is complete
-    MG_CK(c, cudaStreamWaitEvent(c->hstream, c->hev[C_], 0));
+    // counter := 0 on the caller's stream, before the event the chain waits for and before
+    // the memory waits below (so no wait can see the previous chain's value)
+    MG_CK(c, cudaMemsetAsync(c->prog, 0, sizeof(unsigned long long), user));
+    MG_CK(c, cudaEventRecord(c->hev[0], user));             // the previous sweep is complete
+    MG_CK(c, cudaStreamWaitEvent(c->hstream, c->hev[0], 0));
     if (fcf) std::swap(c->ucur, c->unext);                  // the sweeps below read `corr`
-    double *st2[2] = {c->sa, c->sb};
-    int s2 = MGRIT_OK;
+    // the whole chain, one launch on the high-priority stream: every CTA of the cluster
+    // bumps the progress counter when its slice of another L rows is complete
+    c->stream = c->hstream;
+    int s2 = coarse_solve_level(c, 1, rm(corr, 0, 1), rm(corr, 0, 1), nullptr, nullptr, 0, -1,
+                                c->prog, (int)L);
+    c->stream = user;
+    if (s2) return s2;
+#ifdef MG_TRACE
+    cudaEventRecord(tev[C_ + 1], c->hstream);
+#endif
+    typedef int (*wait_fn_t)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);
+    const wait_fn_t wait_value = (wait_fn_t)c->wait_value_fn;
     for (int i = 0; i < C_ && !s2; ++i) {
-      c->stream = c->hstream;
-      s2 = coarse_solve_level(c, 1, rm(corr, 0, 1), rm(corr, 0, 1),
-                              i == 0 ? nullptr : st2[(i + 1) & 1],
-                              i + 1 < C_ ? st2[i & 1] : nullptr, i * L, L);
-      c->stream = user;
-      if (s2) break;
-      MG_CK(c, cudaEventRecord(c->hev[i], c->hstream));
-      MG_CK(c, cudaStreamWaitEvent(user, c->hev[i], 0));
+      // user stream: wait until all 16 CTAs have published chunk i (GEQ = flag 0)
+      const int wr = wait_value(user, (unsigned long long)(uintptr_t)c->prog,
+                                16ull * (unsigned long long)(i + 1), 0u);
+      if (wr) return fail(c, MGRIT_ECUDA, "cuStreamWaitValue64 failed (%d)", wr);
       const long long j0 = i == 0 ? 0 : i * L - 1;
       const long long j1 = i + 1 < C_ ? (i + 1) * L - 1 : nc;
       s2 = do_sweep(false, true, j0, j1 - j0, i + 1 < C_ ? 16 : 0);
+#ifdef MG_TRACE
+      cudaEventRecord(tev[i], user);
+#endif
     }
-    c->stream = user;
+#ifdef MG_TRACE
+    cudaStreamSynchronize(user);
+    cudaStreamSynchronize(c->hstream);
+    float tc = 0;
+    cudaEventElapsedTime(&tc, tev[C_], tev[C_ + 1]);
+    fprintf(stderr, "overlap trace (ms since iteration start): chain end %.3f; sweep-chunk ends", tc);
+    for (int i = 0; i < C_; ++i) {
+      float b = 0;
+      cudaEventElapsedTime(&b, tev[C_], tev[i]);
+      fprintf(stderr, " %.3f", b);
+    }
+    fprintf(stderr, "\n");
+    for (auto &e : tev) cudaEventDestroy(e);
+#endif
     return s2;
   };
   // Check+materialise sweep: phase 1 of the fused sweep (same tiles, so the same norm
