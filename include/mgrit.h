@@ -259,7 +259,7 @@ int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
  *   MGRIT_OPT_STAGE_FORM     0 | 1               1: explicit steps in the plain Runge-Kutta
  *                                                stage form (no folded last stage, no
  *                                                Shu-Osher SSP-RK3; R5)
- *   MGRIT_OPT_OVERLAP        C                   two-level host-loop solves: the sequential
+ *   MGRIT_OPT_OVERLAP        C[, spec]           two-level host-loop solves: the sequential
  *                                                coarse chain runs on a private high-priority
  *                                                stream and publishes its progress every
  *                                                nc/C steps; the next iteration's sweep over
@@ -267,7 +267,13 @@ int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
  *                                                beside it, released by stream-ordered memory
  *                                                waits (bitwise the serial iteration); 0 or
  *                                                1: serial; default 16 (chains >= 2048
- *                                                steps) / 8 (>= 1024)
+ *                                                steps) / 8 (>= 1024, or speculative).
+ *                                                Optional second value: 1 / 0 = speculative
+ *                                                chain on / off (FCF: the chain of iteration
+ *                                                k+1 is launched behind the sweep chunks of
+ *                                                iteration k, gated on a flag the stream
+ *                                                writes after each chunk; default: on when
+ *                                                the chain is estimated >= 1.5x the sweep)
  * Errors: EINVAL (unknown option, wrong count, negative value); EUNSUPPORTED if the new
  * whole-row / SDIRK setting cannot factor the stage solves (the old setting is kept).
  */

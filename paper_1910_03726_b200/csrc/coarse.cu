@@ -1002,7 +1002,31 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
     // ---- producer warp: lanes q = 0..3 handle row 4t+1+q of half t --------------------
     const int q = tid - ncomp;
     const int n1g = (seg0 + GWa <= nx) ? GWa : nx - seg0;
+    // gate (speculative chain): rows up to 4t+4 needed -> floor(row / wait_every) + 1 chunks
+    // of the producing sweep complete.  Lane 0 polls the flag (acquire, system scope: the
+    // stream wrote it after the producing kernel completed); a proxy fence orders the bulk
+    // copies (async proxy) behind it.  Rows only grow with t, so the gate of issue_g(t)
+    // also covers the reduce-adds of the halves before it.
+    int gate_done = 0;
+    auto gate = [&](int t) {
+      if (!a.wait_flag) return;
+      const int row = min(N, 4 * t + 4);
+      const int need = min(a.wait_chunks, row / a.wait_every + 1);
+      if (need > gate_done) {
+        if (q == 0) {
+          unsigned long long v;
+          do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.wait_flag) : "memory");
+            if (v < a.wait_base + (unsigned long long)need) __nanosleep(256);
+          } while (v < a.wait_base + (unsigned long long)need);
+        }
+        __syncwarp();
+        asm volatile("fence.proxy.async;" ::: "memory");
+        gate_done = need;
+      }
+    };
     auto issue_g = [&](int t) {  // half t -> set t % 3
+      gate(t);
       if (q == 0) mbar_expect_tx(&gfull[t % 3], (uint32_t)((min(N, 4 * t + 4) - 4 * t) * GWa) * 8u);
       __syncwarp();
       const int r = 4 * t + 1 + q;

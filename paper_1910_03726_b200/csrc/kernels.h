@@ -94,6 +94,13 @@ struct CoarseArgs {
   // (k = 1, 2, ...); a stream-ordered cuStreamWaitValue64 releases dependent work
   unsigned long long *progress;
   int prog_every;          // steps per publication (multiple of 4, divides nsteps)
+  // input gate of a chain launched ahead of its inputs (speculative chain of the next
+  // iteration): the rows g_n, out_n with n <= k*wait_every - 1 may be touched
+  // once *wait_flag >= wait_base + k (all rows once it is >= wait_base + wait_chunks); the
+  // flag is written by the stream after each producer kernel (cuStreamWriteValue64)
+  const unsigned long long *wait_flag;
+  unsigned long long wait_base;
+  int wait_every, wait_chunks;
   PsiOp op;
 };
 cudaError_t launch_psi_coarse(SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);

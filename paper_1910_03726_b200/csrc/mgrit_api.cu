@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -557,10 +558,12 @@ struct mgrit_ctx {
   long long glaunch[2] = {0, 0};     // kernels per captured iteration body (A, B)
   // overlapped two-level iteration: the coarse chain's chunks run on a private
   // high-priority stream while the next sweep's chunks follow on the caller's stream
-  cudaStream_t hstream = nullptr;
+  cudaStream_t hstream[2] = {nullptr, nullptr};   // chains alternate (two may be in flight)
   std::vector<cudaEvent_t> hev;
-  unsigned long long *prog = nullptr;      // workspace: chain progress counter
+  unsigned long long *prog = nullptr;      // workspace: prog[0], prog[1] chain progress counters,
+                                           //   prog[2] the sweep-chunk flag of a speculative chain
   void *wait_value_fn = nullptr;           // cuStreamWaitValue64 (driver entry point)
+  void *write_value_fn = nullptr;          // cuStreamWriteValue64
   cudaStream_t gstream = nullptr;    // private capture/launch stream (the caller's may be
   cudaEvent_t gevent = nullptr;      //   the legacy default stream, which cannot capture)
   double *ucur, *unext;   // fine C-rows: current iterate / next (FCF ping-pong of u0b, v0b)
@@ -943,7 +946,9 @@ static CoarsePlan plan_coarse(const mgrit_ctx *c, int l) {
 int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
                        const double *state_in = nullptr, double *state_out = nullptr,
                        long long n0 = 0, long long nsteps = -1,
-                       unsigned long long *progress = nullptr, int prog_every = 0) {
+                       unsigned long long *progress = nullptr, int prog_every = 0,
+                       const unsigned long long *wait_flag = nullptr,
+                       unsigned long long wait_base = 0, int wait_chunks = 0) {
   const long long N = nsteps >= 0 ? nsteps : c->ntl[l];
   if (c->psi_kind != MGRIT_PSI_STENCIL) {
     RKCoarseArgs a;
@@ -1002,6 +1007,10 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
       return fail(c, MGRIT_EUNSUPPORTED, "progress counter: warp-specialised cluster solve only");
     a.progress = progress;
     a.prog_every = prog_every;
+    a.wait_flag = wait_flag;
+    a.wait_base = wait_base;
+    a.wait_every = prog_every;
+    a.wait_chunks = wait_chunks;
   }
   switch (pl.kind) {
     case CoarsePlan::CLUSTER:
@@ -1520,7 +1529,7 @@ void mgrit_destroy(mgrit_ctx *c) {
   if (c->gevent) cudaEventDestroy(c->gevent);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   for (auto e : c->hev) cudaEventDestroy(e);
-  if (c->hstream) cudaStreamDestroy(c->hstream);
+  for (auto hs : c->hstream) if (hs) cudaStreamDestroy(hs);
   delete c;
 }
 
@@ -1781,7 +1790,7 @@ int mgrit_set_final_sweep(mgrit_ctx *c, int mode) {
 int mgrit_set_option(mgrit_ctx *c, int option, const int *values, int n) {
   if (!c) return MGRIT_EINVAL;
   static const int kMin[MGRIT_OPT_COUNT] = {2, 2, 3, 1, 1, 2, 1, 1, 1, 1};
-  static const int kMax[MGRIT_OPT_COUNT] = {3, 2, 3, 1, 1, 2, 1, 1, 1, 1};
+  static const int kMax[MGRIT_OPT_COUNT] = {3, 2, 3, 1, 1, 2, 1, 1, 1, 2};
   if (option < 0 || option >= MGRIT_OPT_COUNT) return fail(c, MGRIT_EINVAL, "unknown option %d", option);
   if (n != 0 && (n < kMin[option] || n > kMax[option] || !values))
     return fail(c, MGRIT_EINVAL, "option %d takes %d..%d values", option, kMin[option], kMax[option]);
@@ -1948,91 +1957,151 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   // side rows <= (i+1)L, which chunk i has consumed.  Same kernels on the same data in the
   // same order per row: results are bitwise those of the serial iteration.
   int nchunks = 0;
+  // Speculation pays when the chain is much longer than the sweep it hides behind (two chains
+  // in flight cost the sweeps 32 SMs): cost model fitted to the measured kernels
+  // (profiles/r02_overlap_ab.txt) -- chain step = 230 ns + 4.5 x its FP64 floor (nu * nx/16
+  // FMAs per SM at 64 per clock), sweep = stage-form flops at 23 TF/s (explicit) or 10 TF/s
+  // (SDIRK).  cfg3: 0.75 vs 0.60 ms -> no; cfg4: 2.1 vs 0.7 ms -> yes.
+  bool spec_default = false;
+  if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL) {
+    const double floor_ns = c->op[1].nu * (nx / 16.0) / 64.0 / 1.965;
+    const double chain_ms = nc * (230.0 + 4.5 * floor_ns) * 1e-6;
+    int nnz = 0;
+    for (int i = 0; i < c->tab.s; ++i) {
+      nnz += c->tab.b[i] != 0.0;
+      for (int l = 0; l < c->tab.s; ++l) nnz += c->tab.A[i][l] != 0.0;
+    }
+    const double flops = c->tab.s * (2.0 * c->zn - 1.0) + 2.0 * nnz;
+    const double sweep_ms = (double)nc * m * (fcf ? 2 : 1) * nx * flops / (c->implicit ? 10e12 : 23e12) * 1e3;
+    spec_default = chain_ms >= 1.5 * sweep_ms;
+  }
   if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL && !c->bc && !c->prof && c->nranks == 1) {
     const CoarsePlan pl = plan_coarse(c, 1);
     const bool chain = pl.kind == CoarsePlan::CLUSTER_CA && pl.tb;
-    // default: 16 chunks of >= 128 steps (measured, profiles/r02_overlap_ab.txt)
+    // default (measured, profiles/r02_overlap_ab.txt): 16 chunks of >= 128 steps, 8 with a
+    // speculative chain (its sweeps run on fewer SMs: coarser chunks quantise better)
     int want = opt(c, MGRIT_OPT_OVERLAP) ? c->opt_v[MGRIT_OPT_OVERLAP][0]
-                                         : (nc >= 2048 ? 16 : (nc >= 1024 ? 8 : 0));
+                                         : (nc >= 2048 && !(spec_default && fcf) ? 16 : (nc >= 1024 ? 8 : 0));
     while (want > 1 && (nc % want || (nc / want) % 4 || nc / want < 32)) --want;
     if (chain && want > 1) nchunks = want;
-    if (nchunks && !c->wait_value_fn) {   // stream-ordered memory wait (driver entry point)
+    if (nchunks && !c->wait_value_fn) {   // stream-ordered memory operations (driver entry points)
       cudaDriverEntryPointQueryResult qr;
-      void *fn = nullptr;
+      void *fn = nullptr, *fn2 = nullptr;
       if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
-          qr != cudaDriverEntryPointSuccess || !fn) {
+          qr != cudaDriverEntryPointSuccess || !fn ||
+          cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn2, cudaEnableDefault, &qr) != cudaSuccess ||
+          qr != cudaDriverEntryPointSuccess || !fn2) {
         cudaGetLastError();
         nchunks = 0;                      // not available: serial iteration
       } else {
         c->wait_value_fn = fn;
+        c->write_value_fn = fn2;
       }
     }
   }
-  auto overlapped_iteration = [&]() -> int {
-    const int C_ = nchunks;
-    const long long L = nc / C_;
-    if (!c->hstream) {
+  // Speculative chain (FCF only; option MGRIT_OPT_OVERLAP second value 0 disables): while
+  // iteration k's sweep chunks run, the chain of iteration k+1 is already resident on the
+  // other high-priority stream; its producer warps are gated, chunk by chunk, on a flag the
+  // caller's stream writes after each sweep chunk (cuStreamWriteValue64).  It only modifies
+  // the buffer of iterate k+1 (v' + e), never iterate k, so a solve that converges at k simply
+  // ignores it.  Two chains in flight halve the iteration period.
+  typedef int (*mem_fn_t)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);
+  if (nchunks > 1)   // sweep-chunk flag := 0 (the previous solve's drain left it released)
+    MG_CK(c, cudaMemsetAsync(c->prog + 2, 0, sizeof(unsigned long long), c->stream));
+  const bool spec_ok = nchunks > 1 && fcf &&
+                       (opt(c, MGRIT_OPT_OVERLAP, 2) ? c->opt_v[MGRIT_OPT_OVERLAP][1] != 0 : spec_default);
+  bool spec_inflight = false;       // the chain of the next correction is already launched
+  int spec_par = 0;                 // ... on hstream[spec_par] with counter prog[spec_par]
+  unsigned long long flag_seq = 0;  // value of the sweep-chunk flag prog[2] after the last write
+  // release and drain a chain in flight (error paths, end of the solve)
+  auto drain_chains = [&]() {
+    if (c->write_value_fn && nchunks > 1) {
+      ((mem_fn_t)c->write_value_fn)(c->stream, (unsigned long long)(uintptr_t)(c->prog + 2),
+                                   1ull << 62, 0u);
+      for (auto hs : c->hstream) if (hs) cudaStreamSynchronize(hs);
+    }
+    spec_inflight = false;
+  };
+  struct Drain {
+    std::function<void()> f;
+    ~Drain() { f(); }
+  } drain_guard{drain_chains};
+  auto ensure_streams = [&]() -> int {
+    for (auto &hs : c->hstream) {
+      if (hs) continue;
       int lo = 0, hi = 0;
       MG_CK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      MG_CK(c, cudaStreamCreateWithPriority(&c->hstream, cudaStreamNonBlocking, hi));
+      MG_CK(c, cudaStreamCreateWithPriority(&hs, cudaStreamNonBlocking, hi));
     }
-    while ((int)c->hev.size() < 1) {
+    while ((int)c->hev.size() < 2) {
       cudaEvent_t e = nullptr;
       MG_CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       c->hev.push_back(e);
     }
-    const cudaStream_t user = c->stream;
-#ifdef MG_TRACE   // tools/trace_overlap.sh: timeline of the chunks (timing events)
-    std::vector<cudaEvent_t> tev(C_ + 2);
-    for (auto &e : tev) cudaEventCreate(&e);
-    cudaEventRecord(tev[C_], user);
-#endif
-    double *corr = fcf ? c->unext : c->ucur;   // C-rows receiving += e
-    // counter := 0 on the caller's stream, before the event the chain waits for and before
-    // the memory waits below (so no wait can see the previous chain's value)
-    MG_CK(c, cudaMemsetAsync(c->prog, 0, sizeof(unsigned long long), user));
-    MG_CK(c, cudaEventRecord(c->hev[0], user));             // the previous sweep is complete
-    MG_CK(c, cudaStreamWaitEvent(c->hstream, c->hev[0], 0));
-    if (fcf) std::swap(c->ucur, c->unext);                  // the sweeps below read `corr`
-    // the whole chain, one launch on the high-priority stream: every CTA of the cluster
-    // bumps the progress counter when its slice of another L rows is complete
-    c->stream = c->hstream;
-    int s2 = coarse_solve_level(c, 1, rm(corr, 0, 1), rm(corr, 0, 1), nullptr, nullptr, 0, -1,
-                                c->prog, (int)L);
-    c->stream = user;
+    return MGRIT_OK;
+  };
+  // wait on the caller's stream until the chain with counter prog[par] has published `chunks`
+  auto wait_chain = [&](int par, int chunks) -> int {
+    const int wr = ((mem_fn_t)c->wait_value_fn)(c->stream, (unsigned long long)(uintptr_t)(c->prog + par),
+                                                16ull * (unsigned long long)chunks, 0u /* GEQ */);
+    return wr ? fail(c, MGRIT_ECUDA, "cuStreamWaitValue64 failed (%d)", wr) : MGRIT_OK;
+  };
+  // correction k (k = the iteration being performed, already incremented) overlapped with the
+  // sweep that measures ||r^(k)||; may_spec: iteration k+1 may follow (k < max_iter)
+  auto overlapped_iteration = [&](bool may_spec) -> int {
+    const int C_ = nchunks;
+    const long long L = nc / C_;
+    int s2 = ensure_streams();
     if (s2) return s2;
-#ifdef MG_TRACE
-    cudaEventRecord(tev[C_ + 1], c->hstream);
-#endif
-    typedef int (*wait_fn_t)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);
-    const wait_fn_t wait_value = (wait_fn_t)c->wait_value_fn;
-    for (int i = 0; i < C_ && !s2; ++i) {
-      // user stream: wait until all 16 CTAs have published chunk i (GEQ = flag 0)
-      const int wr = wait_value(user, (unsigned long long)(uintptr_t)c->prog,
-                                16ull * (unsigned long long)(i + 1), 0u);
-      if (wr) return fail(c, MGRIT_ECUDA, "cuStreamWaitValue64 failed (%d)", wr);
+    const cudaStream_t user = c->stream;
+    double *corr = fcf ? c->unext : c->ucur;   // C-rows receiving += e
+    int par;
+    if (spec_inflight) {
+      par = spec_par;                          // chain k is already running
+      spec_inflight = false;
+    } else {
+      par = spec_par ^ 1;
+      spec_par = par;
+      // counter := 0 on the caller's stream, before the event the chain waits for and before
+      // the memory waits below (so no wait can see an earlier chain's value)
+      MG_CK(c, cudaMemsetAsync(c->prog + par, 0, sizeof(unsigned long long), user));
+      MG_CK(c, cudaEventRecord(c->hev[par], user));          // the previous sweep is complete
+      MG_CK(c, cudaStreamWaitEvent(c->hstream[par], c->hev[par], 0));
+      c->stream = c->hstream[par];
+      s2 = coarse_solve_level(c, 1, rm(corr, 0, 1), rm(corr, 0, 1), nullptr, nullptr, 0, -1,
+                              c->prog + par, (int)L);
+      c->stream = user;
+      if (s2) return s2;
+    }
+    if (fcf) std::swap(c->ucur, c->unext);                  // the sweeps below read `corr`
+    const bool spec = spec_ok && may_spec;
+    if (spec) {  // chain k+1: corrects the rows the sweep chunks below write (now `unext`)
+      const int p2 = par ^ 1;
+      MG_CK(c, cudaMemsetAsync(c->prog + p2, 0, sizeof(unsigned long long), user));
+      MG_CK(c, cudaEventRecord(c->hev[p2], user));
+      MG_CK(c, cudaStreamWaitEvent(c->hstream[p2], c->hev[p2], 0));
+      c->stream = c->hstream[p2];
+      s2 = coarse_solve_level(c, 1, rm(c->unext, 0, 1), rm(c->unext, 0, 1), nullptr, nullptr, 0, -1,
+                              c->prog + p2, (int)L, c->prog + 2, flag_seq, C_);
+      c->stream = user;
+      if (s2) return s2;
+      spec_inflight = true;
+      spec_par = p2;
+    }
+    for (int i = 0; i < C_; ++i) {
+      s2 = wait_chain(par, i + 1);
+      if (s2) return s2;
       const long long j0 = i == 0 ? 0 : i * L - 1;
       const long long j1 = i + 1 < C_ ? (i + 1) * L - 1 : nc;
-      s2 = do_sweep(false, true, j0, j1 - j0, i + 1 < C_ ? 16 : 0);
-#ifdef MG_TRACE
-      cudaEventRecord(tev[i], user);
-#endif
+      s2 = do_sweep(false, true, j0, j1 - j0, i + 1 < C_ ? (spec ? 32 : 16) : (spec ? 16 : 0));
+      if (s2) return s2;
+      if (spec) {
+        const int wr = ((mem_fn_t)c->write_value_fn)(user, (unsigned long long)(uintptr_t)(c->prog + 2),
+                                                     ++flag_seq, 0u);
+        if (wr) return fail(c, MGRIT_ECUDA, "cuStreamWriteValue64 failed (%d)", wr);
+      }
     }
-#ifdef MG_TRACE
-    cudaStreamSynchronize(user);
-    cudaStreamSynchronize(c->hstream);
-    float tc = 0;
-    cudaEventElapsedTime(&tc, tev[C_], tev[C_ + 1]);
-    fprintf(stderr, "overlap trace (ms since iteration start): chain end %.3f; sweep-chunk ends", tc);
-    for (int i = 0; i < C_; ++i) {
-      float b = 0;
-      cudaEventElapsedTime(&b, tev[C_], tev[i]);
-      fprintf(stderr, " %.3f", b);
-    }
-    fprintf(stderr, "\n");
-    for (auto &e : tev) cudaEventDestroy(e);
-#endif
-    return s2;
+    return MGRIT_OK;
   };
   // Check+materialise sweep: phase 1 of the fused sweep (same tiles, so the same norm
   // partials, bit for bit) with per-step writes of the FULL iterate into out_dev and no
@@ -2131,7 +2200,11 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       }
       const bool ovl = nchunks > 1 && !last;
       if (ovl) {
-        st = overlapped_iteration();   // coarse chunks || the next sweep's chunks
+        st = overlapped_iteration(k < max_iter);   // chain || the next sweep's chunks
+      } else if (spec_inflight) {  // the correction is already running (speculative chain)
+        st = wait_chain(spec_par, nchunks);
+        spec_inflight = false;
+        if (!st && fcf) std::swap(c->ucur, c->unext);
       } else {
         st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
         if (!st && fcf) std::swap(c->ucur, c->unext);

@@ -275,6 +275,12 @@ static cudaError_t dispatch_tma(SweepCfg c, const SweepArgs &a, cudaStream_t s) 
 #undef MG_CASE
   if (c.nt_threads == 128 && c.p == 15 && c.minb == 3) return launch_tma_one<SC, 128, 15, 3>(a, s);
   if (c.nt_threads == 128 && c.p == 15 && c.minb == 2) return launch_tma_one<SC, 128, 15, 2>(a, s);
+  // one-warp tiles (shuffle-only neighbour exchange, no CTA barrier per stage): experiment
+  if constexpr (std::is_same<SC, ERK3U3>::value) {
+    if (c.nt_threads == 32 && c.p == 15 && c.minb == 16) return launch_tma_one<SC, 32, 15, 16>(a, s);
+    if (c.nt_threads == 32 && c.p == 19 && c.minb == 12) return launch_tma_one<SC, 32, 19, 12>(a, s);
+    if (c.nt_threads == 32 && c.p == 23 && c.minb == 10) return launch_tma_one<SC, 32, 23, 10>(a, s);
+  }
   return cudaErrorInvalidConfiguration;
 }
 

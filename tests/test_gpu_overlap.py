@@ -43,14 +43,14 @@ def _setup(B, order, tab, c, nx, nt, m, nu, relax, seed, options):
 def test_overlap_bitwise_equals_serial(order, tab, c, nx, nt, m, nu, relax, final):
     B = _cuda()
     res, outs = [], []
-    for chunks in (0, 8, 4):
+    for chunks in ([0], [8], [4], [8, 0], [16, 1]):   # [C] / [C, speculative chain on/off]
         s, U, phi, fit = _setup(B, order, tab, c, nx, nt, m, nu, relax, 11,
-                                {"graph": [0], "overlap": [chunks]})
+                                {"graph": [0], "overlap": chunks})
         s.set_final_sweep(final)
         Ug = torch.from_numpy(U).cuda()
         s.set_guess(Ug)
         out = torch.empty_like(Ug)
-        r = s.solve(1e-10, 12, out=out, keep_crows=(chunks != 4))
+        r = s.solve(1e-10, 12, out=out, keep_crows=(chunks != [4]))
         res.append(r)
         outs.append(out)
     for r, o in zip(res[1:], outs[1:]):
