@@ -253,8 +253,10 @@ int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
  *   MGRIT_OPT_GRAPH          0 | 1               mgrit_solve's iterations as one CUDA graph with
  *                                                a device-side WHILE loop (one host sync per
  *                                                solve) | per-iteration host loop; default:
- *                                                graph for nx*nt <= 2^23 (latency-bound), host
- *                                                loop otherwise (it predicts the last
+ *                                                graph for nx*nt <= 2^23 (latency-bound)
+ *                                                unless the overlapped iteration with a
+ *                                                speculative chain applies (MGRIT_OPT_OVERLAP),
+ *                                                host loop otherwise (it predicts the last
  *                                                iteration and fuses materialisation)
  *   MGRIT_OPT_STAGE_FORM     0 | 1               1: explicit steps in the plain Runge-Kutta
  *                                                stage form (no folded last stage, no
@@ -274,6 +276,15 @@ int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
  *                                                iteration k, gated on a flag the stream
  *                                                writes after each chunk; default: on when
  *                                                the chain is estimated >= 1.5x the sweep)
+ *   MGRIT_OPT_VOVERLAP       C[, n[, spec]]      V-cycle host-loop solves (halo-tile kernels):
+ *                                                the HBM-bound level-1 interpolation in C
+ *                                                chunks on a high-priority stream, the
+ *                                                FP64-bound fine sweep over the corrected
+ *                                                intervals beside it with at most n CTAs per
+ *                                                SM, and (spec = 1) the next V-cycle's level-1
+ *                                                sweep behind it; ordered by events, bitwise
+ *                                                the serial iteration; C = 0 or 1: serial;
+ *                                                default 8, 3, 1
  * Errors: EINVAL (unknown option, wrong count, negative value); EUNSUPPORTED if the new
  * whole-row / SDIRK setting cannot factor the stage solves (the old setting is kept).
  */
@@ -288,7 +299,8 @@ typedef enum {
   MGRIT_OPT_STAGE_FORM = 7,
   MGRIT_OPT_GRAPH = 8,
   MGRIT_OPT_OVERLAP = 9,
-  MGRIT_OPT_COUNT = 10
+  MGRIT_OPT_VOVERLAP = 10,
+  MGRIT_OPT_COUNT = 11
 } mgrit_option;
 int mgrit_set_option(mgrit_ctx *ctx, int option, const int *values, int n);
 

@@ -28,7 +28,7 @@ PSI_KIND = {"stencil": 0, "ideal": 1, "redisc": 2}
 STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENONFINITE", -5: "EUNSUPPORTED",
           -6: "ECOMM"}
 OPTION = {"fine_tile": 0, "whole_row": 1, "seq_cluster": 2, "seq_s": 3, "coarse_kernel": 4,
-          "seq_cfg": 5, "sdirk_product": 6, "stage_form": 7, "graph": 8, "overlap": 9}
+          "seq_cfg": 5, "sdirk_product": 6, "stage_form": 7, "graph": 8, "overlap": 9, "voverlap": 10}
 PROF_CLASSES = ("fine_sweep", "level_sweep", "coarse_solve", "interp", "residual", "other")
 MAX_LEVELS = 8
 

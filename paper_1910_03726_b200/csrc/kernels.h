@@ -47,6 +47,9 @@ struct SweepArgs {
   // SMs left free for a concurrently running kernel (the overlapped two-level coarse
   // solve's 16-CTA cluster): the persistent grid is sized for sms - reserve_sms
   int reserve_sms;
+  // at most this many CTAs per SM in the persistent grid (0: what fits), leaving registers
+  // and shared memory to a concurrent kernel (the overlapped V-cycle's level kernels)
+  int max_per_sm;
 };
 constexpr int FORC_LD = 24;   // >= S*NL of every explicit scheme (ERK5+U5: 18)
 

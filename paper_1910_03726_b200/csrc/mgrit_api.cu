@@ -564,6 +564,7 @@ struct mgrit_ctx {
                                            //   prog[2] the sweep-chunk flag of a speculative chain
   void *wait_value_fn = nullptr;           // cuStreamWaitValue64 (driver entry point)
   void *write_value_fn = nullptr;          // cuStreamWriteValue64
+  bool lsweep1_done = false;               // overlapped V-cycle: the next level-1 sweep already ran
   cudaStream_t gstream = nullptr;    // private capture/launch stream (the caller's may be
   cudaEvent_t gevent = nullptr;      //   the legacy default stream, which cannot capture)
   double *ucur, *unext;   // fine C-rows: current iterate / next (FCF ping-pong of u0b, v0b)
@@ -1051,10 +1052,13 @@ int p2_count(const mgrit_ctx *c, long long nc) {
   return (int)(c->rank < c->nranks - 1 ? nc : nc - 1);
 }
 
-int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout) {
+// (J0, cnt >= 0): only the level-l intervals J0 .. J0+cnt-1 (a chunk of the overlapped V-cycle).
+int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout, long long J0 = 0,
+                long long cnt = -1) {
   const PsiOp &op = c->op[l];
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
+  if (cnt < 0) cnt = nc - J0;
   PsiCfg pc;
   const bool tma = !c->bc && choose_level_tma(c->nx, m, 2 * m * (op.nu - 1), pc);
   if (c->bc) {
@@ -1066,16 +1070,16 @@ int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout) {
   PsiSweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.nx = c->nx;
-  a.nitems = (int)nc;
+  a.nitems = (int)cnt;
   a.ntiles = pc.ntiles;
   a.m = m;
   a.interp = 0;
-  a.u = uin ? rm(uin, 0, 1) : kNone;
-  a.ucmp = uin ? rm(uin, 1, 1) : kNone;
-  a.g = rm(c->g[l], 0, m);
-  a.v = rm(vout, 1, 1);   // v_{j+1} is the uncorrected C-row; the coarse levels add E
-  a.r2 = rm(c->g[l + 1], 2, 1);
-  a.p2_items = p2_count(c, nc);
+  a.u = uin ? rm(uin, J0, 1) : kNone;
+  a.ucmp = uin ? rm(uin, J0 + 1, 1) : kNone;
+  a.g = rm(c->g[l], J0 * m, m);
+  a.v = rm(vout, J0 + 1, 1);   // v_{j+1} is the uncorrected C-row; the coarse levels add E
+  a.r2 = rm(c->g[l + 1], J0 + 2, 1);
+  a.p2_items = (int)std::max<long long>(0, std::min<long long>(cnt, p2_count(c, nc) - J0));
   a.v2 = a.out2 = kNone;
   a.op = op;
   if (c->bc) return run(c, 1, [&] { return launch_tpsi_level(pc.cfg, a, c->stream); });
@@ -1086,10 +1090,14 @@ int level_sweep(mgrit_ctx *c, int l, const double *uin, double *vout) {
 // Level-l interpolation: from corrected C-rows u_l, F-relax with g_l and add the level-l
 // values to level l-1's C-rows in place: out_{l-1}[n] += U_l[n], n = 0..nt_l (out_{l-1}
 // holds v_{l-1} written by the level-(l-1) sweep; P:212 correction fused).
-int level_interp(mgrit_ctx *c, int l, const double *usrc_rows, RowMap out_prev) {
+// (J0, cnt >= 0): only the level-l intervals J0 .. J0+cnt-1; the last point n = nt_l is added
+// with the chunk that ends at nc.
+int level_interp(mgrit_ctx *c, int l, const double *usrc_rows, RowMap out_prev, long long J0 = 0,
+                 long long cnt = -1) {
   const PsiOp &op = c->op[l];
   const int m = c->m;
   const long long nc = c->ntl[l] / m;
+  if (cnt < 0) cnt = nc - J0;
   PsiCfg pc;
   const bool tma = !c->bc && choose_level_tma(c->nx, m, (m - 1) * (op.nu - 1), pc);
   if (c->bc) {
@@ -1101,22 +1109,22 @@ int level_interp(mgrit_ctx *c, int l, const double *usrc_rows, RowMap out_prev) 
   PsiSweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.nx = c->nx;
-  a.nitems = (int)nc;
+  a.nitems = (int)cnt;
   a.ntiles = pc.ntiles;
   a.m = m;
   a.interp = 1;
   a.accumulate = 1;
-  a.u = rm(usrc_rows, 0, 1);
+  a.u = rm(usrc_rows, J0, 1);
   a.ucmp = kNone;
-  a.g = rm(c->g[l], 0, m);
+  a.g = rm(c->g[l], J0 * m, m);
   a.v = a.r2 = kNone;
-  a.out2 = RowMap{out_prev.base, out_prev.off, out_prev.stride * m};
+  a.out2 = RowMap{out_prev.base, out_prev.off + J0 * m * out_prev.stride, out_prev.stride * m};
   a.v2 = tma ? kNone : a.out2;   // periodic kernel: out = v2 + x with v2 == out (in place)
   a.op = op;
   int st = c->bc ? run(c, 3, [&] { return launch_tpsi_level(pc.cfg, a, c->stream); })
            : tma ? run(c, 3, [&] { return launch_psi_level_tma(pc.cfg, a, c->stream); })
                  : run(c, 3, [&] { return launch_psi_sweep(pc.cfg, a, c->stream); });
-  if (st) return st;
+  if (st || J0 + cnt < nc) return st;
   // the last point n = nt_l (level l's last C-row): out[nt_l] += u_l[nc]
   const long long ntl = c->ntl[l];
   double *dst = const_cast<double *>(out_prev.base) +
@@ -1138,7 +1146,9 @@ int level_cycle(mgrit_ctx *c, int l, bool fcyc, RowMap dst) {
   Range nv(kLevel[l]);
   const int L = c->levels;
   if (l == L - 1) return coarse_solve_level(c, l, dst, dst);
-  int st = level_sweep(c, l, nullptr, c->ul[l]);
+  int st = MGRIT_OK;
+  if (l == 1 && c->lsweep1_done) c->lsweep1_done = false;   // ran behind the last fine sweep
+  else st = level_sweep(c, l, nullptr, c->ul[l]);
   if (st) return st;
   st = level_cycle(c, l + 1, fcyc, rm(c->ul[l], 0, 1));
   if (st) return st;
@@ -1789,8 +1799,8 @@ int mgrit_set_final_sweep(mgrit_ctx *c, int mode) {
 
 int mgrit_set_option(mgrit_ctx *c, int option, const int *values, int n) {
   if (!c) return MGRIT_EINVAL;
-  static const int kMin[MGRIT_OPT_COUNT] = {2, 2, 3, 1, 1, 2, 1, 1, 1, 1};
-  static const int kMax[MGRIT_OPT_COUNT] = {3, 2, 3, 1, 1, 2, 1, 1, 1, 2};
+  static const int kMin[MGRIT_OPT_COUNT] = {2, 2, 3, 1, 1, 2, 1, 1, 1, 1, 1};
+  static const int kMax[MGRIT_OPT_COUNT] = {3, 2, 3, 1, 1, 2, 1, 1, 1, 2, 3};
   if (option < 0 || option >= MGRIT_OPT_COUNT) return fail(c, MGRIT_EINVAL, "unknown option %d", option);
   if (n != 0 && (n < kMin[option] || n > kMax[option] || !values))
     return fail(c, MGRIT_EINVAL, "option %d takes %d..%d values", option, kMin[option], kMax[option]);
@@ -1916,7 +1926,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   // (j0, cnt): only the intervals j0 .. j0+cnt-1 (a chunk of the overlapped iteration, with
   // `reserve` SMs left to the concurrent coarse chain); cnt < 0: all.
   auto do_sweep = [&](bool first, bool want_norm, long long j0 = 0, long long cnt = -1,
-                      int reserve = 0) -> int {
+                      int reserve = 0, int per_sm = 0) -> int {
     if (cnt < 0) cnt = nc - j0;
     SweepArgs a = base_sweep(c);
     a.nitems = (int)cnt;
@@ -1924,6 +1934,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     a.f_off = j0 * m;
     a.f_stride = m;
     a.reserve_sms = reserve;
+    a.max_per_sm = per_sm;
     if (first && fcf) {
       a.in = rm(c->guess, j0 * m, m);
       a.cmp = rm(c->guess, (j0 + 1) * m, m);
@@ -1980,8 +1991,9 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     const bool chain = pl.kind == CoarsePlan::CLUSTER_CA && pl.tb;
     // default (measured, profiles/r02_overlap_ab.txt): 16 chunks of >= 128 steps, 8 with a
     // speculative chain (its sweeps run on fewer SMs: coarser chunks quantise better)
+    const bool sp = spec_default && fcf;
     int want = opt(c, MGRIT_OPT_OVERLAP) ? c->opt_v[MGRIT_OPT_OVERLAP][0]
-                                         : (nc >= 2048 && !(spec_default && fcf) ? 16 : (nc >= 1024 ? 8 : 0));
+                                         : (nc >= 2048 ? (sp ? 8 : 16) : (nc >= 1024 ? (sp ? 4 : 8) : 0));
     while (want > 1 && (nc % want || (nc / want) % 4 || nc / want < 32)) --want;
     if (chain && want > 1) nchunks = want;
     if (nchunks && !c->wait_value_fn) {   // stream-ordered memory operations (driver entry points)
@@ -2015,12 +2027,12 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   unsigned long long flag_seq = 0;  // value of the sweep-chunk flag prog[2] after the last write
   // release and drain a chain in flight (error paths, end of the solve)
   auto drain_chains = [&]() {
-    if (c->write_value_fn && nchunks > 1) {
+    if (c->write_value_fn && nchunks > 1)
       ((mem_fn_t)c->write_value_fn)(c->stream, (unsigned long long)(uintptr_t)(c->prog + 2),
                                    1ull << 62, 0u);
-      for (auto hs : c->hstream) if (hs) cudaStreamSynchronize(hs);
-    }
+    for (auto hs : c->hstream) if (hs) cudaStreamSynchronize(hs);
     spec_inflight = false;
+    c->lsweep1_done = false;
   };
   struct Drain {
     std::function<void()> f;
@@ -2103,6 +2115,91 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     }
     return MGRIT_OK;
   };
+  // Overlapped V-cycle (option MGRIT_OPT_VOVERLAP = C chunks, CTAs per SM of the concurrent
+  // fine sweep, speculative level-1 sweep 0/1; default 8, 3, 1 for the halo-tile kernels): the
+  // top of the V-cycle is HBM-bound (level-1 interpolation: 86 % of the DRAM peak, no FP64
+  // work to speak of) and the fused fine sweep is FP64-bound (HBM at 40 %), so they run side
+  // by side.  The level-1 interpolation goes in C chunks on a high-priority stream; after the
+  // event of chunk i the fine sweep over the fine intervals [4iL-2, 4(i+1)L-2) follows on the
+  // caller's stream with one CTA slot per SM left free; behind it, on a second stream, the
+  // level-1 sweep of the NEXT V-cycle over the level-1 intervals [iL-1, (i+1)L-1) (it only
+  // writes coarse scratch rows, so it is harmless if the solve stops).  The shifted chunk
+  // boundaries make every read see rows that are final and every write hit rows that are
+  // consumed (same argument as the two-level overlap).  CUDA events only.  Same kernels on the
+  // same rows: bitwise the serial iteration.
+  int vchunks = 0, v_per_sm = 3;
+  bool v_spec = true;
+  c->lsweep1_done = false;
+  if (c->levels >= 3 && c->psi_kind == MGRIT_PSI_STENCIL && c->cycle == MGRIT_CYCLE_V && fcf &&
+      !c->bc && !c->prof && c->nranks == 1 && f.ntiles > 1) {
+    const long long nc1 = c->ntl[1] / m;
+    PsiCfg pc;
+    int want = opt(c, MGRIT_OPT_VOVERLAP) ? c->opt_v[MGRIT_OPT_VOVERLAP][0] : 8;
+    if (opt(c, MGRIT_OPT_VOVERLAP, 2)) v_per_sm = c->opt_v[MGRIT_OPT_VOVERLAP][1];
+    if (opt(c, MGRIT_OPT_VOVERLAP, 3)) v_spec = c->opt_v[MGRIT_OPT_VOVERLAP][2] != 0;
+    while (want > 1 && (nc1 % want || nc1 / want < 64)) --want;
+    if (want > 1 && choose_level_tma(nx, m, 2 * m * (c->op[1].nu - 1), pc)) vchunks = want;
+  }
+  bool v_side_pending = false;   // work on the side streams the caller's stream has not joined
+  auto v_join = [&]() -> int {   // caller's stream waits for both side streams
+    if (!v_side_pending) return MGRIT_OK;
+    for (int sidx = 0; sidx < 2; ++sidx) {
+      MG_CK(c, cudaEventRecord(c->hev[sidx], c->hstream[sidx]));
+      MG_CK(c, cudaStreamWaitEvent(c->stream, c->hev[sidx], 0));
+    }
+    v_side_pending = false;
+    return MGRIT_OK;
+  };
+  auto vcycle_overlapped = [&](bool may_spec) -> int {
+    const int C_ = vchunks;
+    const long long nc1 = c->ntl[1] / m, L = nc1 / C_;
+    int s2 = ensure_streams();
+    if (s2) return s2;
+    while ((int)c->hev.size() < 2 + 2 * C_) {
+      cudaEvent_t e = nullptr;
+      MG_CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->hev.push_back(e);
+    }
+    const cudaStream_t user = c->stream, hi = c->hstream[0], hs = c->hstream[1];
+    double *dst = c->unext;     // holds v of the last fine sweep, receives += E
+    s2 = v_join();              // the speculative level-1 sweep (if any) is complete
+    if (s2) return s2;
+    // down leg and the levels below level 1: serial on the caller's stream
+    if (c->lsweep1_done) c->lsweep1_done = false;
+    else s2 = level_sweep(c, 1, nullptr, c->ul[1]);
+    if (!s2) s2 = level_cycle(c, 2, false, rm(c->ul[1], 0, 1));
+    if (s2) return s2;
+    std::swap(c->ucur, c->unext);                 // the fine sweep chunks read `dst`
+    MG_CK(c, cudaEventRecord(c->hev[0], user));
+    MG_CK(c, cudaStreamWaitEvent(hi, c->hev[0], 0));
+    const bool spec = v_spec && may_spec;
+    for (int i = 0; i < C_; ++i) {
+      c->stream = hi;
+      s2 = level_interp(c, 1, c->ul[1], rm(dst, 0, 1), i * L, L);
+      c->stream = user;
+      if (s2) return s2;
+      cudaEvent_t ei = c->hev[2 + 2 * i], fi = c->hev[3 + 2 * i];
+      MG_CK(c, cudaEventRecord(ei, hi));
+      MG_CK(c, cudaStreamWaitEvent(user, ei, 0));
+      const long long j0 = i == 0 ? 0 : 4 * i * L - 2;
+      const long long j1 = i + 1 < C_ ? 4 * (i + 1) * L - 2 : nc;
+      s2 = do_sweep(false, true, j0, j1 - j0, 0, i + 1 < C_ || spec ? v_per_sm : 0);
+      if (s2) return s2;
+      if (spec) {  // the next V-cycle's level-1 sweep over the intervals whose g_1 rows are final
+        MG_CK(c, cudaEventRecord(fi, user));
+        MG_CK(c, cudaStreamWaitEvent(hs, fi, 0));
+        const long long J0 = i == 0 ? 0 : i * L - 1;
+        const long long J1 = i + 1 < C_ ? (i + 1) * L - 1 : nc1;
+        c->stream = hs;
+        s2 = level_sweep(c, 1, nullptr, c->ul[1], J0, J1 - J0);
+        c->stream = user;
+        if (s2) return s2;
+      }
+    }
+    v_side_pending = true;
+    if (spec) c->lsweep1_done = true;
+    return MGRIT_OK;
+  };
   // Check+materialise sweep: phase 1 of the fused sweep (same tiles, so the same norm
   // partials, bit for bit) with per-step writes of the FULL iterate into out_dev and no
   // coarse RHS.  Used for the sweep that measures ||r^(k)|| when iteration k is known
@@ -2129,7 +2226,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   // as one CUDA graph with a device-side WHILE loop (graph.cu), one host sync per solve
   const bool graph = !c->prof && !crows_hist && max_iter < kGraphHist &&
                      (opt(c, MGRIT_OPT_GRAPH) ? c->opt_v[MGRIT_OPT_GRAPH][0] == 1
-                                              : (long long)nx * c->nt <= (1ll << 23));
+                                              : ((long long)nx * c->nt <= (1ll << 23) && !spec_ok));
   // one iteration after the first sweep: coarse correction, (FCF: swap), fused sweep, norm
   auto iteration = [&]() -> int {
     int s2 = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
@@ -2198,15 +2295,18 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
         if (k >= max_iter || c->final_sweep == MGRIT_FINAL_ALWAYS) last = true;
         else if (k >= 2 && h[k - 1] < h[k - 2]) last = h[k - 1] * (h[k - 1] / h[k - 2]) < tol;
       }
-      const bool ovl = nchunks > 1 && !last;
-      if (ovl) {
+      const bool ovl = (nchunks > 1 || vchunks > 1) && !last;
+      if (ovl && vchunks > 1) {
+        st = vcycle_overlapped(k < max_iter);      // level-1 interpolation || fine sweep || next level-1 sweep
+      } else if (ovl) {
         st = overlapped_iteration(k < max_iter);   // chain || the next sweep's chunks
       } else if (spec_inflight) {  // the correction is already running (speculative chain)
         st = wait_chain(spec_par, nchunks);
         spec_inflight = false;
         if (!st && fcf) std::swap(c->ucur, c->unext);
       } else {
-        st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
+        st = v_join();
+        if (!st) st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
         if (!st && fcf) std::swap(c->ucur, c->unext);
       }
       if (st) return st;

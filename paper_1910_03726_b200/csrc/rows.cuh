@@ -176,7 +176,8 @@ static cudaError_t launch_one(const SweepArgs &a, cudaStream_t s) {
   const long long total = (long long)a.nitems * a.ntiles;
   if (total <= 0) return cudaSuccess;
   const long long grid = std::min<long long>(
-      total, (long long)std::max(1, sms - a.reserve_sms) * blocks_per_sm);
+      total, (long long)std::max(1, sms - a.reserve_sms) *
+                 (a.max_per_sm > 0 ? std::min(a.max_per_sm, blocks_per_sm) : blocks_per_sm));
   rk_sweep_kernel<SC, NT, P, FS, BND><<<(unsigned)grid, NT, smem, s>>>(a);
   return cudaGetLastError();
 }

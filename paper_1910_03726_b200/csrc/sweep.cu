@@ -258,7 +258,8 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   const long long total = (long long)a.nitems * a.ntiles;
   if (total <= 0) return cudaSuccess;
   const long long grid = std::min<long long>(
-      total, (long long)std::max(1, sms - a.reserve_sms) * blocks_per_sm);
+      total, (long long)std::max(1, sms - a.reserve_sms) *
+                 (a.max_per_sm > 0 ? std::min(a.max_per_sm, blocks_per_sm) : blocks_per_sm));
   rk_sweep_tma_kernel<SC, NT, P, MINB><<<(unsigned)grid, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -275,12 +276,6 @@ static cudaError_t dispatch_tma(SweepCfg c, const SweepArgs &a, cudaStream_t s) 
 #undef MG_CASE
   if (c.nt_threads == 128 && c.p == 15 && c.minb == 3) return launch_tma_one<SC, 128, 15, 3>(a, s);
   if (c.nt_threads == 128 && c.p == 15 && c.minb == 2) return launch_tma_one<SC, 128, 15, 2>(a, s);
-  // one-warp tiles (shuffle-only neighbour exchange, no CTA barrier per stage): experiment
-  if constexpr (std::is_same<SC, ERK3U3>::value) {
-    if (c.nt_threads == 32 && c.p == 15 && c.minb == 16) return launch_tma_one<SC, 32, 15, 16>(a, s);
-    if (c.nt_threads == 32 && c.p == 19 && c.minb == 12) return launch_tma_one<SC, 32, 19, 12>(a, s);
-    if (c.nt_threads == 32 && c.p == 23 && c.minb == 10) return launch_tma_one<SC, 32, 23, 10>(a, s);
-  }
   return cudaErrorInvalidConfiguration;
 }
 
@@ -389,7 +384,8 @@ static cudaError_t launch_residual_one(const SweepArgs &a, int chunk, cudaStream
   const long long total = (long long)((a.nitems + chunk - 1) / chunk) * a.ntiles;
   if (total <= 0) return cudaSuccess;
   const long long grid = std::min<long long>(
-      total, (long long)std::max(1, sms - a.reserve_sms) * blocks_per_sm);
+      total, (long long)std::max(1, sms - a.reserve_sms) *
+                 (a.max_per_sm > 0 ? std::min(a.max_per_sm, blocks_per_sm) : blocks_per_sm));
   rk_residual_tma_kernel<SC, NT, P><<<(unsigned)grid, NT, smem, s>>>(a, chunk);
   return cudaGetLastError();
 }

@@ -80,3 +80,32 @@ def test_overlap_default_matches_oracle():
     for k in range(rep.iterations):
         assert np.max(np.abs(cg[k] - rep.states[k])) <= 1e-12 * np.max(np.abs(rep.states[k]))
     assert np.max(np.abs(out.cpu().numpy() - Uo)) <= 1e-12 * np.max(np.abs(Uo))
+
+
+@pytest.mark.parametrize("nx,nt,levels", [(8192, 16384, 4), (16384, 8192, 3), (6144, 16384, 5)])
+@pytest.mark.parametrize("final", ["off", "predict"])
+def test_vcycle_overlap_bitwise_equals_serial(nx, nt, levels, final):
+    """MGRIT_OPT_VOVERLAP: level-1 interpolation chunks || fine sweep chunks || the next
+    level-1 sweep, ordered by events, against the serial V-cycle iteration (cfg5 recipe,
+    halo-tile kernels): identical histories, C-rows and solutions, bit for bit."""
+    B = _cuda()
+    from paper_1910_03726_b200 import problem
+    w = W.CFG5.scaled(nx, nt, levels=levels)
+    lib = problem.psi_inputs(w)
+    U = torch.from_numpy(w.guess()).cuda()
+    res, outs = [], []
+    for vo in ([0], [8, 3, 1], [4, 2, 0], [8, 4, 1], None):
+        opts = {} if vo is None else {"voverlap": vo}
+        s = B.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels, lib, w.relax,
+                    options=opts)
+        s.set_final_sweep(final)
+        s.set_guess(U)
+        out = torch.empty_like(U)
+        res.append(s.solve(w.tol, 12, out=out, keep_crows=(vo != [8, 4, 1])))
+        outs.append(out)
+        del s
+    for r, o in zip(res[1:], outs[1:]):
+        assert r["iterations"] == res[0]["iterations"]
+        assert r["history"] == res[0]["history"]
+        assert torch.equal(o, outs[0])
+    assert torch.equal(res[1]["crows"], res[0]["crows"])
