@@ -283,8 +283,9 @@ int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
  *                                                intervals beside it with at most n CTAs per
  *                                                SM, and (spec = 1) the next V-cycle's level-1
  *                                                sweep behind it; ordered by events, bitwise
- *                                                the serial iteration; C = 0 or 1: serial;
- *                                                default 8, 3, 1
+ *                                                the serial iteration; C = 0 or 1: serial
+ *                                                (the default: measured gain <= 1.5 %,
+ *                                                DESIGN.md 6.11)
  * Errors: EINVAL (unknown option, wrong count, negative value); EUNSUPPORTED if the new
  * whole-row / SDIRK setting cannot factor the stage solves (the old setting is kept).
  */

@@ -1583,6 +1583,7 @@ static cudaError_t launch_level_one(const PsiSweepArgs &a, cudaStream_t s) {
   if (!attr) {
     cudaFuncSetAttribute(psi_level_kernel<NT, P, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)L::bytes(L::NROW_MAX));
+    cudaFuncSetAttribute(psi_level_kernel<NT, P, NU>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
   const int m = a.m;

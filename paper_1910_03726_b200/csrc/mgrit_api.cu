@@ -2116,10 +2116,12 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     return MGRIT_OK;
   };
   // Overlapped V-cycle (option MGRIT_OPT_VOVERLAP = C chunks, CTAs per SM of the concurrent
-  // fine sweep, speculative level-1 sweep 0/1; default 8, 3, 1 for the halo-tile kernels): the
-  // top of the V-cycle is HBM-bound (level-1 interpolation: 86 % of the DRAM peak, no FP64
-  // work to speak of) and the fused fine sweep is FP64-bound (HBM at 40 %), so they run side
-  // by side.  The level-1 interpolation goes in C chunks on a high-priority stream; after the
+  // fine sweep, speculative level-1 sweep 0/1; OFF by default): the top of the V-cycle is
+  // HBM-bound (level-1 interpolation: 86 % of the DRAM peak, no FP64 work to speak of) and the
+  // fused fine sweep is FP64-bound (HBM at 40 %), so in principle they can run side by side.
+  // Measured (profiles/r02_voverlap.txt): co-resident, the two kernels slow each other down by
+  // as much as the overlap saves (cfg5 34.65 -> 34.1-34.2 ms at best, the gain coming from
+  // filled kernel tails), so the serial iteration stays the default.  The level-1 interpolation goes in C chunks on a high-priority stream; after the
   // event of chunk i the fine sweep over the fine intervals [4iL-2, 4(i+1)L-2) follows on the
   // caller's stream with one CTA slot per SM left free; behind it, on a second stream, the
   // level-1 sweep of the NEXT V-cycle over the level-1 intervals [iL-1, (i+1)L-1) (it only
@@ -2134,7 +2136,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       !c->bc && !c->prof && c->nranks == 1 && f.ntiles > 1) {
     const long long nc1 = c->ntl[1] / m;
     PsiCfg pc;
-    int want = opt(c, MGRIT_OPT_VOVERLAP) ? c->opt_v[MGRIT_OPT_VOVERLAP][0] : 8;
+    int want = opt(c, MGRIT_OPT_VOVERLAP) ? c->opt_v[MGRIT_OPT_VOVERLAP][0] : 0;
     if (opt(c, MGRIT_OPT_VOVERLAP, 2)) v_per_sm = c->opt_v[MGRIT_OPT_VOVERLAP][1];
     if (opt(c, MGRIT_OPT_VOVERLAP, 3)) v_spec = c->opt_v[MGRIT_OPT_VOVERLAP][2] != 0;
     while (want > 1 && (nc1 % want || nc1 / want < 64)) --want;
@@ -2170,6 +2172,11 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     if (!s2) s2 = level_cycle(c, 2, false, rm(c->ul[1], 0, 1));
     if (s2) return s2;
     std::swap(c->ucur, c->unext);                 // the fine sweep chunks read `dst`
+#ifdef MG_TRACE
+    std::vector<cudaEvent_t> tev(3 * C_ + 1);
+    for (auto &e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[3 * C_], user);
+#endif
     MG_CK(c, cudaEventRecord(c->hev[0], user));
     MG_CK(c, cudaStreamWaitEvent(hi, c->hev[0], 0));
     const bool spec = v_spec && may_spec;
@@ -2180,11 +2187,17 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       if (s2) return s2;
       cudaEvent_t ei = c->hev[2 + 2 * i], fi = c->hev[3 + 2 * i];
       MG_CK(c, cudaEventRecord(ei, hi));
+#ifdef MG_TRACE
+      cudaEventRecord(tev[3 * i], hi);
+#endif
       MG_CK(c, cudaStreamWaitEvent(user, ei, 0));
       const long long j0 = i == 0 ? 0 : 4 * i * L - 2;
       const long long j1 = i + 1 < C_ ? 4 * (i + 1) * L - 2 : nc;
       s2 = do_sweep(false, true, j0, j1 - j0, 0, i + 1 < C_ || spec ? v_per_sm : 0);
       if (s2) return s2;
+#ifdef MG_TRACE
+      cudaEventRecord(tev[3 * i + 1], user);
+#endif
       if (spec) {  // the next V-cycle's level-1 sweep over the intervals whose g_1 rows are final
         MG_CK(c, cudaEventRecord(fi, user));
         MG_CK(c, cudaStreamWaitEvent(hs, fi, 0));
@@ -2194,8 +2207,23 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
         s2 = level_sweep(c, 1, nullptr, c->ul[1], J0, J1 - J0);
         c->stream = user;
         if (s2) return s2;
+#ifdef MG_TRACE
+        cudaEventRecord(tev[3 * i + 2], hs);
+#endif
       }
     }
+#ifdef MG_TRACE
+    cudaDeviceSynchronize();
+    fprintf(stderr, "voverlap trace (ms since the fork): interp end / fine sweep end / level-1 sweep end\n");
+    for (int i = 0; i < C_; ++i) {
+      float a = 0, b = 0, d = 0;
+      cudaEventElapsedTime(&a, tev[3 * C_], tev[3 * i]);
+      cudaEventElapsedTime(&b, tev[3 * C_], tev[3 * i + 1]);
+      if (spec) cudaEventElapsedTime(&d, tev[3 * C_], tev[3 * i + 2]);
+      fprintf(stderr, "  chunk %d: %.3f / %.3f / %.3f\n", i, a, b, d);
+    }
+    for (auto &e : tev) cudaEventDestroy(e);
+#endif
     v_side_pending = true;
     if (spec) c->lsweep1_done = true;
     return MGRIT_OK;

@@ -247,7 +247,9 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
     cudaFuncSetAttribute(rk_sweep_tma_kernel<SC, NT, P, MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 116 * 1024));
+    cudaFuncSetAttribute(rk_sweep_tma_kernel<SC, NT, P, MINB>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
                                                   rk_sweep_tma_kernel<SC, NT, P, MINB>, NT, smem);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
@@ -257,10 +259,20 @@ static cudaError_t launch_tma_one(const SweepArgs &a, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long total = (long long)a.nitems * a.ntiles;
   if (total <= 0) return cudaSuccess;
-  const long long grid = std::min<long long>(
-      total, (long long)std::max(1, sms - a.reserve_sms) *
-                 (a.max_per_sm > 0 ? std::min(a.max_per_sm, blocks_per_sm) : blocks_per_sm));
-  rk_sweep_tma_kernel<SC, NT, P, MINB><<<(unsigned)grid, NT, smem, s>>>(a);
+  // max_per_sm == 3 (overlapped V-cycle): the grid alone does not keep a fourth
+  // CTA off an SM, so the launch asks for just enough shared memory that four CTAs no longer
+  // fit (4 x (57472 + 1024) > 228 KiB) while three of them leave room for one 128 x 9 level
+  // kernel CTA (3 x 58496 + 57728 <= 233472 bytes)
+  size_t smem_l = smem;
+  int per_sm = blocks_per_sm;
+  if (a.max_per_sm > 0 && a.max_per_sm < blocks_per_sm) {
+    per_sm = a.max_per_sm;
+    // smallest request (multiple of 128) with (per_sm + 1) x (request + 1 KiB) > 228 KiB
+    const size_t need = ((233472 / (per_sm + 1) - 1024) / 128 + 1) * 128;
+    smem_l = std::max(smem, need);
+  }
+  const long long grid = std::min<long long>(total, (long long)std::max(1, sms - a.reserve_sms) * per_sm);
+  rk_sweep_tma_kernel<SC, NT, P, MINB><<<(unsigned)grid, NT, smem_l, s>>>(a);
   return cudaGetLastError();
 }
 

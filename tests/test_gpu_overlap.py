@@ -94,7 +94,7 @@ def test_vcycle_overlap_bitwise_equals_serial(nx, nt, levels, final):
     lib = problem.psi_inputs(w)
     U = torch.from_numpy(w.guess()).cuda()
     res, outs = [], []
-    for vo in ([0], [8, 3, 1], [4, 2, 0], [8, 4, 1], None):
+    for vo in ([0], [8, 3, 1], [4, 2, 0], [8, 4, 1]):
         opts = {} if vo is None else {"voverlap": vo}
         s = B.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels, lib, w.relax,
                     options=opts)
