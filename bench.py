@@ -378,7 +378,7 @@ def run_ours(args, w):
         "config": {"workload": w.name, "nx": w.nx, "nt": w.nt, "scheme": f"{w.tableau}+U{w.order}",
                    "cfl": w.cfl, "m": w.m, "levels": w.levels, "relax": w.relax,
                    "psi_widths": list(w.psi_widths), "tol": w.tol, "iterations": K,
-                   "cycle": args.cycle,
+                   "cycle": args.cycle, "boundary": getattr(w, "boundary", "periodic"),
                    "time_to_residual_ms": round(ms, 4),
                    "final_residual": res["history"][-1],
                    "history": [float(f"{h:.4e}") for h in res["history"]],
@@ -414,7 +414,7 @@ def run_ours(args, w):
     }
     if rank == 0:
         line["clocks"] = _clock_summary(clk_path, local)
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and getattr(w, "boundary", "periodic") == "periodic":
             line["cpu_baseline"] = oracle_sample(w, args.cpu_budget)
             line["cpu_sequential"] = sequential_sample(w, args.cpu_budget / 2)
         print(json.dumps(line), flush=True)

@@ -1014,10 +1014,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
       const int need = min(a.wait_chunks, row / a.wait_every + 1);
       if (need > gate_done) {
         if (q == 0) {
-          unsigned long long v;
+          // The producing sweeps run concurrently on other SMs.  If kernels are being
+          // serialised (a profiler's kernel replay, CUDA_LAUNCH_BLOCKING=1) they never run
+          // while this kernel is resident: give up after 10 s with a launch failure instead
+          // of hanging the GPU (use MGRIT_OPT_OVERLAP = C, 0 under such tools).
+          unsigned long long v, t0, t1;
+          asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
           do {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a.wait_flag) : "memory");
-            if (v < a.wait_base + (unsigned long long)need) __nanosleep(256);
+            if (v < a.wait_base + (unsigned long long)need) {
+              __nanosleep(256);
+              asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+              if (t1 - t0 > 10000000000ull) __trap();
+            }
           } while (v < a.wait_base + (unsigned long long)need);
         }
         __syncwarp();

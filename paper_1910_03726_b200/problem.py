@@ -28,9 +28,16 @@ def psi_inputs(w, device: bool = False) -> List[Dict]:
 
 def make_solver(w, psi: Optional[List[Dict]] = None, stream=None,
                 options: Optional[Dict] = None) -> binding.MGRIT:
-    return binding.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels,
-                         psi if psi is not None else psi_inputs(w), w.relax, stream=stream,
-                         options=options)
+    s = binding.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels,
+                      psi if psi is not None else psi_inputs(w), w.relax, stream=stream,
+                      options=options)
+    if getattr(w, "boundary", "periodic") == "inflow":   # PAPER.md 4.5: u(-1, t) = sin^4(pi t)
+        import torch
+        import workloads as W
+        stages = s.coefficients()[1].shape[0]
+        dg = W.inflow_sin4_derivatives(np.arange(w.nt) * w.dt, w.order + stages)
+        s.set_inflow(torch.from_numpy(dg).to(s.workspace.device))
+    return s
 
 
 def device_guess(w, device="cuda"):

@@ -136,6 +136,7 @@ class Workload:
     tol: float = 1e-10
     max_iter: int = 128
     alpha: float = 1.0
+    boundary: str = "periodic"   # "inflow": inflow u(-1,t) = sin^4(pi t) / outflow (PAPER.md 4.5)
 
     @property
     def dx(self) -> float:
@@ -152,6 +153,8 @@ class Workload:
             return u0_fourier(self.nx, self.u0_seed)
         if self.u0_kind == "gauss":
             return u0_gauss(self.nx)
+        if self.u0_kind == "sin4_inflow":   # sin^4(pi x) on the unknowns x_1..x_nx
+            return np.sin(np.pi * inflow_grid(self.nx)) ** 4
         raise ValueError(self.u0_kind)
 
     def guess(self) -> np.ndarray:
@@ -182,7 +185,18 @@ CFG5 = Workload("cfg5", 16384, 65536, 0.85, "ERK", 3, "erk3_ssp", 4, 6, "FCF", "
                 psi_widths=(9, 13, 17, 21, 25), u0_kind="fourier", u0_seed=6, guess_seed=7,
                 max_iter=64)
 
-ALL = {w.name: w for w in (CFG1_REDISC, CFG1_IDEAL, CFG2, CFG3, CFG4_LITERAL, CFG4, CFG5)}
+# Inflow/outflow runs shaped like tab:LSQlin_ERK_inflow: ERKp+Up, 2^12 x 2^14
+# two-level m = 4 and a 2^10 x 2^12 four-level V-cycle, the periodic problem's LSQ Psi truncated
+# at the boundaries (widths as for the periodic configs, R8).  Not BASELINE.json configs:
+# measurement cases of SURVEY 8(f) NEXT-4.
+INFLOW_ERK3 = Workload("inflow_erk3", 4096, 16384, 0.85, "ERK", 3, "erk3_ssp", 4, 2, "FCF", "stencil",
+                       psi_widths=(9,), u0_kind="sin4_inflow", guess_seed=8, boundary="inflow")
+INFLOW_ERK3_ML = Workload("inflow_erk3_ml", 1024, 4096, 0.85, "ERK", 3, "erk3_ssp", 4, 4, "FCF",
+                          "stencil", psi_widths=(9, 13, 17), u0_kind="sin4_inflow", guess_seed=9,
+                          boundary="inflow")
+
+ALL = {w.name: w for w in (CFG1_REDISC, CFG1_IDEAL, CFG2, CFG3, CFG4_LITERAL, CFG4, CFG5,
+                           INFLOW_ERK3, INFLOW_ERK3_ML)}
 
 
 # ----------------------------------------------------------------------------
