@@ -959,6 +959,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
   const bool active = !producer && l0 < Wc + ER;
   const bool own = !producer && l0 >= 0 && l0 < Wc;
   const bool lhalo = !producer && l0 < 0, rhalo = !producer && l0 >= Wc && active;
+  // truncated Psi: the halo points of the first / last CTA lie beyond the row
+  // ends; they hold zero at every step (whatever the wrap neighbour sends or g contains there)
+  const bool ghost = a.trunc && ((rank == 0 && lhalo) || (rank == CL - 1 && rhalo));
   const int own0 = (int)rank * Wc;                  // global index of local point 0
   int gx = own0 + l0;
   if (gx < 0) gx += nx;
@@ -1093,7 +1096,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
           const double *rj = R + (j & 1) * CS::EMAX + (lhalo ? EL + l0 : EL + (l0 - Wc));
           double hv[P];
 #pragma unroll
-          for (int p = 0; p < P; ++p) hv[p] = rj[p];
+          for (int p = 0; p < P; ++p) hv[p] = ghost ? 0.0 : rj[p];
           put(cur, hv);
         }
         if (tid == 0) mbar_expect_tx(&hb[j % 3], hbytes);  // re-arm for exchange j + 3
@@ -1127,7 +1130,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
         }
         const double *gs = gring + (size_t)slot * GW + tid * P;
 #pragma unroll
-        for (int p = 0; p < P; ++p) x[p] = (acc0[p] + acc1[p]) + gs[p];  // x_i = Psi x_{i-1} + g_i
+        for (int p = 0; p < P; ++p) x[p] = ghost ? 0.0 : (acc0[p] + acc1[p]) + gs[p];  // x_i = Psi x_{i-1} + g_i
         put(nxt, x);
         if (own) {
           double *os = oring + (size_t)slot * Wc + l0;

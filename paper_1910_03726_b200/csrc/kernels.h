@@ -104,6 +104,9 @@ struct CoarseArgs {
   const unsigned long long *wait_flag;
   unsigned long long wait_base;
   int wait_every, wait_chunks;
+  // 1: Psi truncated at the row ends (Toeplitz, no wrap; inflow/outflow rows, bounded.cu):
+  // psi_seq_cluster_tb_kernel keeps the halo points beyond the row ends at zero
+  int trunc;
   PsiOp op;
 };
 cudaError_t launch_psi_coarse(SweepCfg cfg, const CoarseArgs &a, cudaStream_t s);

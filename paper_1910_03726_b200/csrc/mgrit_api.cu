@@ -973,7 +973,14 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
     }
     return run(c, 2, [&] { return launch_rk_coarse(c->scheme, cfg, a, c->stream); });
   }
-  if (c->bc) {  // truncated Toeplitz Psi: one CTA, fixed coordinates (bounded.cu)
+  // truncated Toeplitz Psi on a long chain: the warp-specialised 16-CTA cluster kernel with the
+  // halo points beyond the row ends held at zero (CoarseArgs::trunc); otherwise one CTA
+  const bool bc_cluster = c->bc && [&] {
+    const CoarsePlan pl = plan_coarse(c, l);
+    return pl.kind == CoarsePlan::CLUSTER_CA && pl.tb;
+  }();
+  if (c->bc && !bc_cluster) {  // one CTA, fixed coordinates (bounded.cu)
+    if (progress) return fail(c, MGRIT_EUNSUPPORTED, "progress counter: cluster solve only");
     SweepCfg cfg;
     if (!tpsi_cfg(c->nx, true, cfg))
       return fail(c, MGRIT_EUNSUPPORTED, "inflow/outflow: nx in {64,128,...,4096}");
@@ -1003,6 +1010,7 @@ int coarse_solve_level(mgrit_ctx *c, int l, RowMap v, RowMap out,
   a.state_in = state_in;
   a.state_out = state_out;
   a.op = c->op[l];
+  a.trunc = c->bc;
   if (progress) {
     if (!(pl.kind == CoarsePlan::CLUSTER_CA && pl.tb))
       return fail(c, MGRIT_EUNSUPPORTED, "progress counter: warp-specialised cluster solve only");
@@ -1986,7 +1994,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     const double sweep_ms = (double)nc * m * (fcf ? 2 : 1) * nx * flops / (c->implicit ? 10e12 : 23e12) * 1e3;
     spec_default = chain_ms >= 1.5 * sweep_ms;
   }
-  if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL && !c->bc && !c->prof && c->nranks == 1) {
+  if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL && !c->prof && c->nranks == 1) {
     const CoarsePlan pl = plan_coarse(c, 1);
     const bool chain = pl.kind == CoarsePlan::CLUSTER_CA && pl.tb;
     // default (measured, profiles/r02_overlap_ab.txt): 16 chunks of >= 128 steps, 8 with a

@@ -268,3 +268,28 @@ def test_inflow_unsupported_combinations():
     s3 = B.MGRIT(256, 64, 4, 1.0, 4.0, 3, "sdirk3", 2, lib3, "FCF")
     with pytest.raises(B.MgritError):      # implicit tableau
         s3.set_inflow(None)
+
+
+def test_inflow_long_chain_cluster_overlap():
+    """A long two-level chain (nc = 1024) takes the 16-CTA cluster kernel with the halo points
+    beyond the row ends held at zero, overlapped with the next sweep and with a speculative
+    chain by default: against the oracle, and bitwise against the serial iteration."""
+    B = _cuda()
+    nx, nt, m = 1024, 4096, 4
+    rep, res = _compare_solve(B, 3, "erk3_ssp", 0.85, nx, nt, m, 2, (9,))
+    assert rep.converged
+    ph, dgs, u0, g0, U = _problem(3, "erk3_ssp", 0.85, nx, nt, seed=1)
+    lib, _ = _fits(3, "erk3_ssp", 0.85, nx, m, (9,))
+    outs = []
+    for opts in ({"graph": [0], "overlap": [0]}, {"graph": [0], "overlap": [8, 1]},
+                 {"graph": [0], "overlap": [4, 0]}, {"graph": [1]}):
+        s = B.MGRIT(nx, nt, m, 1.0, 0.85, 3, "erk3_ssp", 2, lib, "FCF", options=opts)
+        s.set_inflow(torch.from_numpy(dgs).cuda())
+        Ug = torch.from_numpy(U).cuda()
+        s.set_guess(Ug)
+        out = torch.empty_like(Ug)
+        r = s.solve(1e-10, 40, out=out)
+        outs.append((r["history"], out))
+    for h, o in outs[1:]:
+        assert h == outs[0][0]
+        assert torch.equal(o, outs[0][1])
