@@ -371,6 +371,27 @@ int mgrit_psi_fit(int nx, int order, int tableau, double cfl, int m, int levels,
                   double *coeffs_out, double *imag_out, void *workspace_dev,
                   size_t workspace_bytes, void *stream);
 
+/*
+ * mgrit_psi_fit_nl — the nonlinear least-squares coarse operator of PAPER.md Appendix B
+ * (eq. (nlsq)) on the device: minimise F(psi) = (1/nx) sum_k ||E_k(psi)||^2 with
+ * ||E_k|| the two-level FCF estimate (Dobrev_bounds) P:283-293 of Fourier mode k, over the
+ * real nonzeros psi of a circulant Psi with the contiguous pattern `offsets`, by
+ * Levenberg-Marquardt (identity scaling, l_0 = 0.01, x10 / /10, stop at relative decrease
+ * or step 1e-6, at most max_iter trials; the paper allows 30) from the start value in
+ * `coeffs` (the linear fit of mgrit_psi_fit).  Explicit tableaux, two-level.
+ *   coeffs          host, nnz: start value in, result out.
+ *   iters_out       nullable: trials used.   objective_out  nullable: F at the result.
+ *   history_out     nullable, max_iter + 1: F after every trial (entry 0: the start value).
+ * The modes are evaluated one thread per k (the geometric sum of the estimate by Horner), the
+ * Gauss-Newton matrix J^T J and J^T r are accumulated and factored in double-double.
+ * Synchronous on `stream`.  Errors: EINVAL, ENOMEM, EUNSUPPORTED (SDIRK), ECUDA.
+ */
+size_t mgrit_psi_fit_nl_workspace_bytes(int nx);
+int mgrit_psi_fit_nl(int nx, int order, int tableau, double cfl, int m, int nt, int nnz,
+                     const int *offsets, double *coeffs, int max_iter, int *iters_out,
+                     double *objective_out, double *history_out, void *workspace_dev,
+                     size_t workspace_bytes, void *stream);
+
 /* C-rows (nt/m+1) x nx of the current iterate after mgrit_solve. */
 int mgrit_get_crows(mgrit_ctx *ctx, double *out_dev);
 

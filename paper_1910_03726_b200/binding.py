@@ -90,6 +90,11 @@ _SIGS = [
                                 C.POINTER(C.c_int), C.c_double, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), C.POINTER(C.c_double),
                                 C.POINTER(C.c_double), C.c_void_p, C.c_size_t, C.c_void_p]),
+    ("mgrit_psi_fit_nl_workspace_bytes", C.c_size_t, [C.c_int]),
+    ("mgrit_psi_fit_nl", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_int,
+                                   C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.c_void_p, C.c_size_t, C.c_void_p]),
     ("mgrit_profile_enable", C.c_int, [C.c_void_p, C.c_int]),
     ("mgrit_profile_read", C.c_int, [C.c_void_p, C.POINTER(C.c_longlong),
                                      C.POINTER(C.c_double)]),
@@ -169,6 +174,32 @@ def psi_fit_device(order: int, tableau: str, cfl: float, nx: int, m: int, levels
         out.append({"kind": "stencil", "offsets": [offs[l * T + a] for a in range(n)],
                     "coeffs": [cof[l * T + a] for a in range(n)], "imag": imag[l]})
     return out
+
+
+def psi_fit_nl_device(order: int, tableau: str, cfl: float, nx: int, m: int, nt: int,
+                      offsets: Sequence[int], coeffs: Sequence[float], max_iter: int = 30,
+                      stream=None):
+    """mgrit_psi_fit_nl: the nonlinear least-squares Psi of PAPER.md Appendix B on the GPU, by
+    Levenberg-Marquardt from `coeffs` (the linear fit).  Returns a library input dict with
+    "objective", "iterations" and the objective "history"."""
+    import torch
+    L = lib()
+    nb = L.mgrit_psi_fit_nl_workspace_bytes(nx)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    n = len(offsets)
+    offs = (C.c_int * n)(*[int(d) for d in offsets])
+    cof = (C.c_double * n)(*[float(v) for v in coeffs])
+    its = C.c_int()
+    obj = C.c_double()
+    hist = (C.c_double * (max_iter + 1))()
+    st = L.mgrit_psi_fit_nl(nx, order, TABLEAU[tableau], cfl, m, nt, n, offs, cof, max_iter,
+                            C.byref(its), C.byref(obj), hist, ws.data_ptr(), nb,
+                            C.c_void_p(_stream(stream)))
+    if st:
+        raise MgritError(st, "mgrit_psi_fit_nl")
+    return {"kind": "stencil", "offsets": list(offsets), "coeffs": [cof[a] for a in range(n)],
+            "objective": obj.value, "iterations": its.value,
+            "history": [hist[i] for i in range(its.value + 1)]}
 
 
 def fill_guess(dst, seed: int, lo: float = -1.0, u0=None, row0: int = 0, stream=None):

@@ -251,6 +251,144 @@ __global__ void fit_solve_kernel(int nu, const double *part_hi, const double *pa
   out[nu] = imag;
 }
 
+// ---------------------------------------------------------------------------
+// Nonlinear least squares (Appendix B, eq. (nlsq); R21):
+//   F(psi) = (1/nx) sum_k |r_k|^2,  r_k = C_k g(|mu_k|) (lambda_k^m - mu_k),
+//   C_k = sqrt(m) |lambda_k|^m,  g(a) = sum_{j=0}^{N-2} a^j (N = nt/m; Horner),
+// the two-level FCF estimate (Dobrev_bounds) P:283-293 per Fourier mode.
+// nl_mode_kernel: one thread per mode k -> mu_k, r_k and the two factors of the Jacobian row
+//   dr_k/dpsi_a = P_k rho_ka - Q_k E_ka,  E_ka = e^{i theta_k d_a},  rho_ka = Re(conj(mu_k) E_ka),
+//   P_k = C_k g'(a_k)/a_k (lambda_k^m - mu_k)  (complex),  Q_k = C_k g(a_k)  (real).
+// nl_sums_kernel: double-double partial sums per k-chunk of G_ab = sum_k Re(conj(J_ka) J_kb),
+//   h_a = sum_k Re(conj(J_ka) r_k) and sum_k |r_k|^2 (fixed order).
+// nl_step_kernel: one thread, (G + l I) delta = -h by Cholesky in double-double,
+//   psi_trial = psi + delta, |delta|, |psi|.
+// ---------------------------------------------------------------------------
+__global__ void nl_mode_kernel(int nx, int nu, int o0, int m, int nterms, const double *psi,
+                               const double *lam_re, const double *lam_im, const double *t_re,
+                               const double *t_im, double *mu_re, double *mu_im, double *r_re,
+                               double *r_im, double *P_re, double *P_im, double *Q) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nx) return;
+  double mr = 0.0, mi = 0.0;
+  for (int a = 0; a < nu; ++a) {
+    double c, s;
+    expi(k, o0 + a, nx, c, s);
+    mr = fma(psi[a], c, mr);
+    mi = fma(psi[a], s, mi);
+  }
+  const double am = hypot(mr, mi);
+  double g = 1.0, dg = 0.0;
+  for (int j = 1; j < nterms; ++j) {
+    dg = fma(dg, am, g);
+    g = fma(g, am, 1.0);
+  }
+  const double al = hypot(lam_re[k], lam_im[k]);
+  double C = sqrt((double)m);
+  for (int q = 0; q < m; ++q) C *= al;
+  const double dr = t_re[k] - mr, di = t_im[k] - mi;
+  mu_re[k] = mr;
+  mu_im[k] = mi;
+  r_re[k] = C * g * dr;
+  r_im[k] = C * g * di;
+  const double pf = am > 0.0 ? C * dg / am : 0.0;
+  P_re[k] = pf * dr;
+  P_im[k] = pf * di;
+  Q[k] = C * g;
+}
+
+// entries: G_ab (np = nu(nu+1)/2 row-packed pairs b <= a), h_a (nu), F (1)
+__global__ void nl_sums_kernel(int nx, int nu, int o0, const double *mu_re, const double *mu_im,
+                               const double *r_re, const double *r_im, const double *P_re,
+                               const double *P_im, const double *Q, double *part_hi,
+                               double *part_lo, int nchunks, int f_only) {
+  const int e = blockIdx.y * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x;
+  const int np = nu * (nu + 1) / 2;
+  if (e >= np + nu + 1) return;
+  if (f_only && e != np + nu) return;
+  int ia = 0, ib = 0;
+  if (e < np) {
+    while ((ia + 1) * (ia + 2) / 2 <= e) ++ia;
+    ib = e - ia * (ia + 1) / 2;
+  } else if (e < np + nu) {
+    ia = e - np;
+  }
+  dd s = {0.0, 0.0};
+  const int k0 = c * kChunk, k1 = min(nx, k0 + kChunk);
+  for (int k = k0; k < k1; ++k) {
+    if (e == np + nu) {
+      s = dd_add(s, dd_add(dd_prod(r_re[k], r_re[k]), dd_prod(r_im[k], r_im[k])));
+      continue;
+    }
+    double ca, sa;
+    expi(k, o0 + ia, nx, ca, sa);
+    const double rho_a = mu_re[k] * ca + mu_im[k] * sa;          // Re(conj(mu) E_a)
+    const double ja_re = P_re[k] * rho_a - Q[k] * ca, ja_im = P_im[k] * rho_a - Q[k] * sa;
+    if (e < np) {
+      double cb, sb;
+      expi(k, o0 + ib, nx, cb, sb);
+      const double rho_b = mu_re[k] * cb + mu_im[k] * sb;
+      const double jb_re = P_re[k] * rho_b - Q[k] * cb, jb_im = P_im[k] * rho_b - Q[k] * sb;
+      s = dd_add(s, dd_add(dd_prod(ja_re, jb_re), dd_prod(ja_im, jb_im)));
+    } else {
+      s = dd_add(s, dd_add(dd_prod(ja_re, r_re[k]), dd_prod(ja_im, r_im[k])));
+    }
+  }
+  part_hi[e * nchunks + c] = s.hi;
+  part_lo[e * nchunks + c] = s.lo;
+}
+
+// out[0..nu): psi + delta, out[nu]: |delta|, out[nu+1]: |psi|, out[nu+2]: sum |r|^2 (of the
+// point the sums were formed at).  sum_only: just out[nu+2].
+__global__ void nl_step_kernel(int nu, const double *psi, double lmb, const double *part_hi,
+                               const double *part_lo, int nchunks, int sum_only, double *out) {
+  extern __shared__ dd sm[];
+  if (threadIdx.x || blockIdx.x) return;
+  dd *h = sm, *G = h + MAX_PSI;
+  const int np = nu * (nu + 1) / 2;
+  for (int e = sum_only ? np + nu : 0; e < np + nu + 1; ++e) {
+    dd s = {0.0, 0.0};
+    for (int c = 0; c < nchunks; ++c) s = dd_add(s, {part_hi[e * nchunks + c], part_lo[e * nchunks + c]});
+    if (e < np) G[e] = s;
+    else if (e < np + nu) h[e - np] = dd_neg(s);
+    else out[nu + 2] = s.hi + s.lo;
+  }
+  if (sum_only) return;
+  auto at = [&](int i, int j) -> dd & { return G[i * (i + 1) / 2 + j]; };
+  for (int j = 0; j < nu; ++j) at(j, j) = dd_add(at(j, j), {lmb, 0.0});
+  for (int j = 0; j < nu; ++j) {
+    dd d = at(j, j);
+    for (int k = 0; k < j; ++k) d = dd_add(d, dd_neg(dd_mul(at(j, k), at(j, k))));
+    const dd ljj = dd_sqrt(d);
+    at(j, j) = ljj;
+    for (int i = j + 1; i < nu; ++i) {
+      dd v = at(i, j);
+      for (int k = 0; k < j; ++k) v = dd_add(v, dd_neg(dd_mul(at(i, k), at(j, k))));
+      at(i, j) = dd_div(v, ljj);
+    }
+  }
+  for (int i = 0; i < nu; ++i) {
+    dd v = h[i];
+    for (int k = 0; k < i; ++k) v = dd_add(v, dd_neg(dd_mul(at(i, k), h[k])));
+    h[i] = dd_div(v, at(i, i));
+  }
+  for (int i = nu - 1; i >= 0; --i) {
+    dd v = h[i];
+    for (int k = i + 1; k < nu; ++k) v = dd_add(v, dd_neg(dd_mul(at(k, i), h[k])));
+    h[i] = dd_div(v, at(i, i));
+  }
+  double nd = 0.0, npsi = 0.0;
+  for (int a = 0; a < nu; ++a) {
+    const double d = h[a].hi + h[a].lo;
+    out[a] = psi[a] + d;
+    nd = fma(d, d, nd);
+    npsi = fma(psi[a], psi[a], npsi);
+  }
+  out[nu] = sqrt(nd);
+  out[nu + 1] = sqrt(npsi);
+}
+
 // Real part of the first column of Phi^m: col_j = (1/nx) sum_k t_k e^{2 pi i jk/nx}.
 __global__ void fit_idft_kernel(int nx, const double *t_re, const double *t_im, double *col) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -366,6 +504,118 @@ int mgrit_psi_fit(int nx, int order, int tableau, double cfl, int m, int levels,
     sym.zn = nu;
     for (int a = 0; a < nu; ++a) sym.z[a] = hout[a];
   }
+  return MGRIT_OK;
+}
+
+size_t mgrit_psi_fit_nl_workspace_bytes(int nx) {
+  if (nx < 2) return 0;
+  const size_t nch = (size_t)(nx + kChunk - 1) / kChunk;
+  const size_t ne = (size_t)MAX_PSI * (MAX_PSI + 1) / 2 + MAX_PSI + 1;
+  return sizeof(double) * (12 * (size_t)nx + 2 * ne * nch + 3 * MAX_PSI + 16) + 256;
+}
+
+int mgrit_psi_fit_nl(int nx, int order, int tableau, double cfl, int m, int nt, int nnz,
+                     const int *offsets, double *coeffs, int max_iter, int *iters_out,
+                     double *objective_out, double *history_out, void *workspace_dev,
+                     size_t workspace_bytes, void *stream_) {
+  if (nx < 8 || m < 2 || nt < 2 * m || nt % m || nnz < 1 || nnz > MGRIT_MAX_PSI_TAPS || nnz > nx / 2 ||
+      !offsets || !coeffs || !workspace_dev || max_iter < 0)
+    return MGRIT_EINVAL;
+  for (int a = 1; a < nnz; ++a)
+    if (offsets[a] != offsets[0] + a) return MGRIT_EINVAL;   // contiguous patterns (R8, P:786 hull)
+  if (workspace_bytes < mgrit_psi_fit_nl_workspace_bytes(nx)) return MGRIT_ENOMEM;
+  cudaStream_t st = (cudaStream_t)stream_;
+  int s = 0, zlo = 0, zn = 0;
+  double z[8], A[36], b[6];
+  if (mgrit_scheme_coefficients(order, tableau, cfl, &s, &zlo, &zn, z, A, b)) return MGRIT_EINVAL;
+  if (tableau >= MGRIT_TAB_SDIRK1) return MGRIT_EUNSUPPORTED;   // explicit schemes only
+  const int nch = (nx + kChunk - 1) / kChunk, nu = nnz, o0 = offsets[0];
+  const int np = nu * (nu + 1) / 2, nent = np + nu + 1;
+  double *w0 = (double *)workspace_dev;
+  double *lr = w0, *li = lr + nx, *tr = li + nx, *ti = tr + nx, *ww = ti + nx;
+  double *mur = ww + nx, *mui = mur + nx, *rr = mui + nx, *ri = rr + nx, *Pr = ri + nx, *Pi = Pr + nx,
+         *Qq = Pi + nx;
+  const size_t ne = (size_t)MAX_PSI * (MAX_PSI + 1) / 2 + MAX_PSI + 1;
+  double *phi = Qq + nx, *plo = phi + ne * nch, *psi_d = plo + ne * nch, *trial_d = psi_d + MAX_PSI,
+         *res = trial_d + MAX_PSI;
+  FitSym sym;
+  std::memset(&sym, 0, sizeof(sym));
+  sym.nx = nx;
+  sym.m = m;
+  sym.s = s;
+  sym.zlo = zlo;
+  sym.zn = zn;
+  for (int j = 0; j < zn; ++j) sym.z[j] = z[j];
+  for (int i = 0; i < s; ++i) {
+    sym.b[i] = b[i];
+    for (int j = 0; j < s; ++j) sym.A[i][j] = A[i * 6 + j];
+  }
+  fit_symbol_kernel<<<(nx + 255) / 256, 256, 0, st>>>(sym, lr, li, tr, ti, ww);
+  if (cudaGetLastError() != cudaSuccess) return MGRIT_ECUDA;
+  const int nterms = nt / m - 1;
+  const size_t smem = sizeof(double) * 2 * (MAX_PSI * (MAX_PSI + 1) / 2 + MAX_PSI);
+  std::vector<double> psi(coeffs, coeffs + nu), hout(nu + 3);
+#define NL_CK(x) do { if ((x) != cudaSuccess) return MGRIT_ECUDA; } while (0)
+  // modes and sums at `p` (device array); f_only: just sum |r|^2
+  auto eval = [&](const double *p, int f_only) -> cudaError_t {
+    nl_mode_kernel<<<(nx + 127) / 128, 128, 0, st>>>(nx, nu, o0, m, nterms, p, lr, li, tr, ti, mur, mui,
+                                                   rr, ri, Pr, Pi, Qq);
+    dim3 grid(nch, (nent + 127) / 128);
+    nl_sums_kernel<<<grid, 128, 0, st>>>(nx, nu, o0, mur, mui, rr, ri, Pr, Pi, Qq, phi, plo, nch, f_only);
+    return cudaGetLastError();
+  };
+  auto sum_f = [&](double &F) -> cudaError_t {
+    nl_step_kernel<<<1, 32, smem, st>>>(nu, psi_d, 0.0, phi, plo, nch, 1, res);
+    cudaError_t e = cudaMemcpyAsync(hout.data(), res, (nu + 3) * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    F = hout[nu + 2] / nx;
+    return e;
+  };
+  NL_CK(cudaMemcpyAsync(psi_d, psi.data(), nu * sizeof(double), cudaMemcpyHostToDevice, st));
+  NL_CK(eval(psi_d, 0));
+  double F = 0.0;
+  NL_CK(sum_f(F));
+  if (history_out) history_out[0] = F;
+  double lmb = 0.01;
+  int it = 0;
+  bool done = false;
+  while (it < max_iter && !done) {
+    // G, h, F are those of psi_d (formed by the last full eval)
+    while (it < max_iter) {
+      ++it;
+      nl_step_kernel<<<1, 32, smem, st>>>(nu, psi_d, lmb, phi, plo, nch, 0, res);
+      NL_CK(cudaGetLastError());
+      NL_CK(cudaMemcpyAsync(hout.data(), res, (nu + 3) * sizeof(double), cudaMemcpyDeviceToHost, st));
+      NL_CK(cudaStreamSynchronize(st));
+      const double nd = hout[nu], npsi = hout[nu + 1];
+      std::vector<double> trial(hout.begin(), hout.begin() + nu);
+      // the sums of psi_d are still needed if the trial is rejected: evaluate the trial's
+      // F into the upper half of the partial arrays' F entry only (f_only touches entry F)
+      NL_CK(cudaMemcpyAsync(trial_d, trial.data(), nu * sizeof(double), cudaMemcpyHostToDevice, st));
+      NL_CK(eval(trial_d, 1));
+      double Fn = 0.0;
+      NL_CK(sum_f(Fn));
+      if (Fn < F) {
+        const bool small = (F - Fn) <= 1e-6 * F || nd <= 1e-6 * (1.0 + npsi);
+        psi = trial;
+        NL_CK(cudaMemcpyAsync(psi_d, trial_d, nu * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        F = Fn;
+        lmb /= 10.0;
+        if (history_out) history_out[it] = F;
+        done = small;
+        if (!done && it < max_iter) NL_CK(eval(psi_d, 0));   // G, h at the accepted point
+        break;
+      }
+      lmb *= 10.0;
+      if (history_out) history_out[it] = Fn;
+      // rejected: the mode arrays hold the trial's values, but G and h (partials) are intact;
+      // only the F entry of the partials was overwritten, and F is kept on the host
+    }
+  }
+#undef NL_CK
+  for (int a = 0; a < nu; ++a) coeffs[a] = psi[a];
+  if (iters_out) *iters_out = it;
+  if (objective_out) *objective_out = F;
   return MGRIT_OK;
 }
 

@@ -45,3 +45,48 @@ def test_solve_with_device_fit(name):
         out.append(s.solve(w.tol, w.max_iter))
     assert out[0]["iterations"] == out[1]["iterations"] and out[1]["converged"]
     np.testing.assert_allclose(out[1]["history"], out[0]["history"], rtol=1e-6)
+
+
+@pytest.mark.parametrize("order,tab,nx,nt,m,nu", [(1, "erk1", 256, 1024, 2, 2), (1, "erk1", 256, 1024, 8, 4),
+                                                 (3, "erk3_ssp", 256, 512, 4, 9),
+                                                 (3, "erk3_kutta", 1024, 4096, 4, 9),
+                                                 (5, "erk5", 4096, 16384, 8, 15)])
+def test_device_nonlinear_fit_matches_oracle(order, tab, nx, nt, m, nu):
+    """mgrit_psi_fit_nl (App. B, eq. (nlsq)) against oracle/nlsq.py from the same
+    linear-LSQ start: the same Levenberg-Marquardt trial sequence (accept / reject pattern and
+    trial count), objective history and coefficients."""
+    from oracle import nlsq as N
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1910_03726_b200 import binding as B
+    phi = D.make_phi(order, tab, 0.85, nx)
+    fit = OP.fit_hierarchy(phi, nx, m, 0.85, (nu,))[0]
+    e0 = np.zeros(nx)
+    e0[0] = 1.0
+    lam = OP.eigenvalues(phi(e0))
+    ref = N.nlsq_psi(fit.coeffs, fit.offsets, lam, m, nt)
+    got = B.psi_fit_nl_device(order, tab, 0.85, nx, m, nt, fit.offsets, list(fit.coeffs))
+    assert got["iterations"] == ref.iterations
+    assert len(got["history"]) == len(ref.history)
+    for a, b in zip(got["history"], ref.history):
+        assert abs(a - b) <= 1e-8 * abs(b), (got["history"], ref.history)
+    assert got["objective"] < ref.history[0]
+    np.testing.assert_allclose(got["coeffs"], ref.coeffs, rtol=0, atol=1e-8 * np.max(np.abs(ref.coeffs)))
+
+
+@pytest.mark.parametrize("m,nu,kref", [(2, 2, 10), (4, 3, 6), (8, 4, 6)])
+def test_paper_nonlinear_table_through_the_library(m, nu, kref):
+    """tab:LSQnonlin_ERK, ERK1+U1 2^8 x 2^10, m = 2, 4, 8 -> 10, 6, 6: linear fit
+    and nonlinear refinement both on the device, then mgrit_solve (U[0,1) guess, R3)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1910_03726_b200 import binding as B
+    nx, nt = 256, 1024
+    lin = B.psi_fit_device(1, "erk1", 0.85, nx, m, 2, (nu,))[0]
+    nl = B.psi_fit_nl_device(1, "erk1", 0.85, nx, m, nt, lin["offsets"], lin["coeffs"])
+    assert nl["objective"] < nl["history"][0]
+    s = B.MGRIT(nx, nt, m, 1.0, 0.85, 1, "erk1", 2, [nl], "FCF")
+    U = torch.from_numpy(W.initial_iterate(0, nx, nt, W.u0_sin4(nx), 0.0)).cuda()
+    s.set_guess(U)
+    r = s.solve(1e-10, 60)
+    assert r["converged"] and r["iterations"] == kref, r["iterations"]
