@@ -1963,6 +1963,28 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     }
     return sweep(c, 0, a, fcf ? 2 * m : m);
   };
+  // Check+materialise sweep: phase 1 of the fused sweep (same tiles, so the same norm
+  // partials, bit for bit) with per-step writes of the FULL iterate into out_dev and no
+  // coarse RHS.  Used for the sweep that measures ||r^(k)|| when iteration k is known
+  // (k == max_iter) or predicted to be the last, so a converged solve needs neither the
+  // unused r = Phi^m delta nor a separate materialisation pass.
+  auto check_sweep = [&](long long j0 = 0, long long cnt = -1, int reserve = 0) -> int {
+    if (cnt < 0) cnt = nc - j0;
+    SweepArgs a = base_sweep(c);
+    a.nitems = (int)cnt;
+    a.nsteps1 = m;
+    a.f_off = j0 * m;
+    a.f_stride = m;
+    a.reserve_sms = reserve;
+    a.in = rm(c->ucur, j0, 1);
+    a.cmp = rm(c->ucur, j0 + 1, 1);
+    a.partials = c->partials + partial_count(c, j0, fcf ? 2 * m : m);
+    a.each = rm(out_dev, j0 * m, m);
+    a.each_step = 1;
+    a.each_first = 0;
+    a.each_last = m - 1;
+    return sweep(c, 3, a, fcf ? 2 * m : m);
+  };
   // Overlapped two-level iteration (option MGRIT_OPT_OVERLAP = number of chunks C, default 8
   // for long chains): the sequential coarse chain runs as ONE launch of the 16-CTA
   // cluster kernel on a private high-priority stream and publishes a progress counter every
@@ -2068,7 +2090,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   };
   // correction k (k = the iteration being performed, already incremented) overlapped with the
   // sweep that measures ||r^(k)||; may_spec: iteration k+1 may follow (k < max_iter)
-  auto overlapped_iteration = [&](bool may_spec) -> int {
+  // final: the sweep chunks are check-sweep chunks (residual + FULL solution, no coarse RHS)
+  auto overlapped_iteration = [&](bool may_spec, bool final = false) -> int {
     const int C_ = nchunks;
     const long long L = nc / C_;
     int s2 = ensure_streams();
@@ -2094,7 +2117,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       if (s2) return s2;
     }
     if (fcf) std::swap(c->ucur, c->unext);                  // the sweeps below read `corr`
-    const bool spec = spec_ok && may_spec;
+    const bool spec = spec_ok && may_spec && !final;
     if (spec) {  // chain k+1: corrects the rows the sweep chunks below write (now `unext`)
       const int p2 = par ^ 1;
       MG_CK(c, cudaMemsetAsync(c->prog + p2, 0, sizeof(unsigned long long), user));
@@ -2113,7 +2136,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       if (s2) return s2;
       const long long j0 = i == 0 ? 0 : i * L - 1;
       const long long j1 = i + 1 < C_ ? (i + 1) * L - 1 : nc;
-      s2 = do_sweep(false, true, j0, j1 - j0, i + 1 < C_ ? (spec ? 32 : 16) : (spec ? 16 : 0));
+      const int reserve = i + 1 < C_ ? (spec ? 32 : 16) : (spec ? 16 : 0);
+      s2 = final ? check_sweep(j0, j1 - j0, reserve) : do_sweep(false, true, j0, j1 - j0, reserve);
       if (s2) return s2;
       if (spec) {
         const int wr = ((mem_fn_t)c->write_value_fn)(user, (unsigned long long)(uintptr_t)(c->prog + 2),
@@ -2236,26 +2260,6 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     if (spec) c->lsweep1_done = true;
     return MGRIT_OK;
   };
-  // Check+materialise sweep: phase 1 of the fused sweep (same tiles, so the same norm
-  // partials, bit for bit) with per-step writes of the FULL iterate into out_dev and no
-  // coarse RHS.  Used for the sweep that measures ||r^(k)|| when iteration k is known
-  // (k == max_iter) or predicted to be the last, so a converged solve needs neither the
-  // unused r = Phi^m delta nor a separate materialisation pass.
-  auto check_sweep = [&]() -> int {
-    SweepArgs a = base_sweep(c);
-    a.nitems = (int)nc;
-    a.nsteps1 = m;
-    a.f_off = 0;
-    a.f_stride = m;
-    a.in = rm(c->ucur, 0, 1);
-    a.cmp = rm(c->ucur, 1, 1);
-    a.partials = c->partials;
-    a.each = rm(out_dev, 0, m);
-    a.each_step = 1;
-    a.each_first = 0;
-    a.each_last = m - 1;
-    return sweep(c, 3, a, fcf ? 2 * m : m);
-  };
   bool materialised = false;
   std::vector<double> h(1, r0);
   // graph mode (option MGRIT_OPT_GRAPH; default: latency-bound problems): the iterations run
@@ -2317,8 +2321,38 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     if (fcf && (k & 1)) std::swap(c->ucur, c->unext);   // odd k: the iterate is in v0b
     c->have_iterate = true;
   } else if (!conv && !nonfinite && max_iter > 0) {
-    st = do_sweep(true, false);
-    if (st) return st;
+    if (spec_ok && !(out_dev && c->final_sweep != MGRIT_FINAL_OFF &&
+                     (max_iter <= 1 || c->final_sweep == MGRIT_FINAL_ALWAYS))) {
+      // the chain of iteration 1 is launched first, gated on the chunks of the first sweep
+      const int C_ = nchunks;
+      const long long L = nc / C_;
+      st = ensure_streams();
+      if (st) return st;
+      const int p2 = spec_par ^ 1;
+      MG_CK(c, cudaMemsetAsync(c->prog + p2, 0, sizeof(unsigned long long), c->stream));
+      MG_CK(c, cudaEventRecord(c->hev[p2], c->stream));
+      MG_CK(c, cudaStreamWaitEvent(c->hstream[p2], c->hev[p2], 0));
+      const cudaStream_t user = c->stream;
+      c->stream = c->hstream[p2];
+      st = coarse_solve_level(c, 1, rm(c->unext, 0, 1), rm(c->unext, 0, 1), nullptr, nullptr, 0, -1,
+                              c->prog + p2, (int)L, c->prog + 2, flag_seq, C_);
+      c->stream = user;
+      if (st) return st;
+      spec_inflight = true;
+      spec_par = p2;
+      for (int i = 0; i < C_; ++i) {
+        const long long j0 = i == 0 ? 0 : i * L - 1;
+        const long long j1 = i + 1 < C_ ? (i + 1) * L - 1 : nc;
+        st = do_sweep(true, false, j0, j1 - j0, 16);
+        if (st) return st;
+        const int wr = ((mem_fn_t)c->write_value_fn)(user, (unsigned long long)(uintptr_t)(c->prog + 2),
+                                                     ++flag_seq, 0u);
+        if (wr) return fail(c, MGRIT_ECUDA, "cuStreamWriteValue64 failed (%d)", wr);
+      }
+    } else {
+      st = do_sweep(true, false);
+      if (st) return st;
+    }
     while (true) {
       Range nv_it("iteration");
       // coarse-grid correction: (FCF) unext += E, then unext becomes the iterate;
@@ -2331,15 +2365,12 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
         if (k >= max_iter || c->final_sweep == MGRIT_FINAL_ALWAYS) last = true;
         else if (k >= 2 && h[k - 1] < h[k - 2]) last = h[k - 1] * (h[k - 1] / h[k - 2]) < tol;
       }
-      const bool ovl = (nchunks > 1 || vchunks > 1) && !last;
+      const bool ovl = nchunks > 1 || (vchunks > 1 && !last);
       if (ovl && vchunks > 1) {
         st = vcycle_overlapped(k < max_iter);      // level-1 interpolation || fine sweep || next level-1 sweep
       } else if (ovl) {
-        st = overlapped_iteration(k < max_iter);   // chain || the next sweep's chunks
-      } else if (spec_inflight) {  // the correction is already running (speculative chain)
-        st = wait_chain(spec_par, nchunks);
-        spec_inflight = false;
-        if (!st && fcf) std::swap(c->ucur, c->unext);
+        // chain || the sweep chunks that measure ||r^(k)|| (check-sweep chunks if predicted last)
+        st = overlapped_iteration(k < max_iter, last);
       } else {
         st = v_join();
         if (!st) st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
