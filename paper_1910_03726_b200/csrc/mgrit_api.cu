@@ -2004,6 +2004,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
   // FMAs per SM at 64 per clock), sweep = stage-form flops at 23 TF/s (explicit) or 10 TF/s
   // (SDIRK).  cfg3: 0.75 vs 0.60 ms -> no; cfg4: 2.1 vs 0.7 ms -> yes.
   bool spec_default = false;
+  double sweep_est_ms = 0.0;
   if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL) {
     const double floor_ns = c->op[1].nu * (nx / 16.0) / 64.0 / 1.965;
     const double chain_ms = nc * (230.0 + 4.5 * floor_ns) * 1e-6;
@@ -2015,6 +2016,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     const double flops = c->tab.s * (2.0 * c->zn - 1.0) + 2.0 * nnz;
     const double sweep_ms = (double)nc * m * (fcf ? 2 : 1) * nx * flops / (c->implicit ? 10e12 : 23e12) * 1e3;
     spec_default = chain_ms >= 1.5 * sweep_ms;
+    sweep_est_ms = sweep_ms;
   }
   if (c->levels == 2 && c->psi_kind == MGRIT_PSI_STENCIL && !c->prof && c->nranks == 1) {
     const CoarsePlan pl = plan_coarse(c, 1);
@@ -2321,8 +2323,10 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     if (fcf && (k & 1)) std::swap(c->ucur, c->unext);   // odd k: the iterate is in v0b
     c->have_iterate = true;
   } else if (!conv && !nonfinite && max_iter > 0) {
-    if (spec_ok && !(out_dev && c->final_sweep != MGRIT_FINAL_OFF &&
-                     (max_iter <= 1 || c->final_sweep == MGRIT_FINAL_ALWAYS))) {
+    // (worth the extra launches only for sweeps of some length: cfg2's 26 us sweep is not)
+    if (spec_ok && sweep_est_ms >= 0.1 &&
+        !(out_dev && c->final_sweep != MGRIT_FINAL_OFF &&
+          (max_iter <= 1 || c->final_sweep == MGRIT_FINAL_ALWAYS))) {
       // the chain of iteration 1 is launched first, gated on the chunks of the first sweep
       const int C_ = nchunks;
       const long long L = nc / C_;
