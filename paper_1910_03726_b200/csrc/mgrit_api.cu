@@ -2369,12 +2369,17 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
         if (k >= max_iter || c->final_sweep == MGRIT_FINAL_ALWAYS) last = true;
         else if (k >= 2 && h[k - 1] < h[k - 2]) last = h[k - 1] * (h[k - 1] / h[k - 2]) < tol;
       }
-      const bool ovl = nchunks > 1 || (vchunks > 1 && !last);
+      // short sweeps (cfg2: 26 us) are not worth chunking for the last iteration
+      const bool ovl = (nchunks > 1 && !(last && sweep_est_ms < 0.1)) || (vchunks > 1 && !last);
       if (ovl && vchunks > 1) {
         st = vcycle_overlapped(k < max_iter);      // level-1 interpolation || fine sweep || next level-1 sweep
       } else if (ovl) {
         // chain || the sweep chunks that measure ||r^(k)|| (check-sweep chunks if predicted last)
         st = overlapped_iteration(k < max_iter, last);
+      } else if (spec_inflight) {  // the correction is already running (speculative chain)
+        st = wait_chain(spec_par, nchunks);
+        spec_inflight = false;
+        if (!st && fcf) std::swap(c->ucur, c->unext);
       } else {
         st = v_join();
         if (!st) st = coarse_correction(c, rm(fcf ? c->unext : c->ucur, 0, 1));
