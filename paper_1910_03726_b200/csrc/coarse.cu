@@ -1016,6 +1016,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
       const int row = min(N, 4 * t + 4);
       const int need = min(a.wait_chunks, row / a.wait_every + 1);
       if (need > gate_done) {
+        mg_jitter(10);
         if (q == 0) {
           // The producing sweeps run concurrently on other SMs.  If kernels are being
           // serialised (a profiler's kernel replay, CUDA_LAUNCH_BLOCKING=1) they never run
@@ -1067,6 +1068,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT + 160, 1)
       // the issuing lanes' bulk groups have completed (not only read); release at system
       // scope for the stream-ordered wait
       if (a.progress && (4 * (t + 1)) % a.prog_every == 0) {
+        mg_jitter(9);
         bulk_wait_all();
         __syncwarp();
         if (q == 0) {

@@ -23,7 +23,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CASES = ["tiles_vcycle", "cluster_tb", "cluster_ca", "cluster_plain", "seq_periodic",
          "whole_rows", "sdirk", "rk_coarse_ideal", "rk_coarse_redisc", "cfg2", "cfg4",
-         "cfg3_ca", "cfg5_fullwidth", "two_level_16384"]
+         "cfg3_ca", "cfg5_fullwidth", "two_level_16384", "cfg3", "inflow_two_level",
+         "cfg4_overlap16"]
 RUNS = 3
 
 

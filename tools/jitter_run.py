@@ -23,6 +23,11 @@ EXTRA = {
     "cfg3_ca": (W.CFG3, {"coarse_kernel": (1,)}),
     "cfg5_fullwidth": (W.CFG5.scaled(16384, 1024, levels=4), {}),
     "two_level_16384": (W.CFG5.scaled(16384, 2048, levels=2, psi_widths=(9,)), {}),
+    # overlapped iteration: chunked first / last sweeps without (cfg3) and with
+    # a speculative chain (cfg2, cfg4 above; the truncated cluster chain of the inflow rows)
+    "cfg3": (W.CFG3, {}),
+    "inflow_two_level": (W.INFLOW_ERK3.scaled(1024, 4096), {}),
+    "cfg4_overlap16": (W.CFG4, {"overlap": (16, 1)}),
 }
 
 
