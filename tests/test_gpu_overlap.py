@@ -38,6 +38,8 @@ def _setup(B, order, tab, c, nx, nt, m, nu, relax, seed, options):
     (3, "erk3_ssp", 0.85, 4096, 4096, 4, 9, "F"),          # Parareal
     (3, "erk3_ssp", 0.85, 16384, 4096, 4, 9, "FCF"),       # halo-tile TMA sweep, 1024-point slices
     (3, "sdirk3", 4.0, 4096, 4096, 4, 31, "FCF"),          # cfg4 scheme
+    (3, "erk3_kutta", 0.85, 1024, 4000, 4, 9, "FCF"),      # nc = 1000: chunk counts that do not divide
+    (3, "erk3_ssp", 0.85, 2048, 6144, 4, 9, "F"),          # nc = 1536, Parareal
 ])
 @pytest.mark.parametrize("final", ["off", "predict"])
 def test_overlap_bitwise_equals_serial(order, tab, c, nx, nt, m, nu, relax, final):
