@@ -8,19 +8,26 @@ import numpy as np
 from . import binding, psi as psimod
 
 
-def psi_inputs(w, device: bool = False) -> List[Dict]:
+def psi_inputs(w, device: bool = False, nonlinear: bool = False) -> List[Dict]:
     """Coarse operators of a workload as library inputs (LSQ fit): host numpy
-    (default) or on the GPU (mgrit_psi_fit, device=True)."""
+    (default) or on the GPU (mgrit_psi_fit, device=True); nonlinear=True (two-level, explicit
+    schemes, device only) refines the linear fit by the nonlinear least squares of PAPER.md
+    Appendix B (mgrit_psi_fit_nl)."""
     if w.psi_kind == "ideal":
         return [{"kind": "ideal"}]
     if w.psi_kind == "redisc":
         return [{"kind": "redisc", "cfl": w.redisc_cfl}]
+    if nonlinear and not (device and w.levels == 2):
+        raise ValueError("the nonlinear fit is two-level and runs on the device")
     if device:
         out = binding.psi_fit_device(w.order, w.tableau, w.cfl, w.nx, w.m, w.levels,
                                      w.psi_widths, w.psi_eta)
         for lvl, p in enumerate(out):
             if p["imag"] > psimod.IMAG_TOL:
                 raise psimod.PsiRejected(f"level {lvl + 2}: imaginary component {p['imag']:.2e}")
+        if nonlinear:
+            out = [binding.psi_fit_nl_device(w.order, w.tableau, w.cfl, w.nx, w.m, w.nt,
+                                             out[0]["offsets"], out[0]["coeffs"])]
         return out
     return psimod.hierarchy(w.order, w.tableau, w.cfl, w.nx, w.m, w.levels,
                             w.psi_widths, w.psi_eta)

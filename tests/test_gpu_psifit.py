@@ -90,3 +90,20 @@ def test_paper_nonlinear_table_through_the_library(m, nu, kref):
     s.set_guess(U)
     r = s.solve(1e-10, 60)
     assert r["converged"] and r["iterations"] == kref, r["iterations"]
+
+
+def test_cfg2_with_nonlinear_psi_converges_no_slower():
+    """P:1032: 'no significant difference between the convergence rates' -- cfg2 with the
+    nonlinear refinement of its 9-point Psi needs at most as many iterations (+-1)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1910_03726_b200 import problem
+    w = W.CFG2
+    ks = []
+    for nl in (False, True):
+        s = problem.make_solver(w, problem.psi_inputs(w, device=True, nonlinear=nl))
+        s.set_guess(problem.device_guess(w))
+        r = s.solve(w.tol, w.max_iter)
+        assert r["converged"]
+        ks.append(r["iterations"])
+    assert abs(ks[1] - ks[0]) <= 1, ks
