@@ -152,6 +152,7 @@ cudaError_t launch_psi_level_tma(SweepCfg cfg, const PsiSweepArgs &a, cudaStream
 // sequential over nsteps, whole periodic row, one CTA.
 struct RKCoarseArgs {
   int nx, nsteps, q;
+  int ring_b;        // > 0: g / v rows through a shared-memory block ring of ring_b steps (set by the launcher)
   RowMap g, v, out;
   RKCoeffs co;
   SdirkCoef sd;      // implicit schemes: the coarse step's factored stage solve

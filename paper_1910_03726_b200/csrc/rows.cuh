@@ -205,6 +205,81 @@ __global__ void __launch_bounds__(NT, 1) rk_coarse_kernel(const __grid_constant_
   double x[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) x[p] = 0.0;
+  // Short rows (ring_b > 0: nx <= 512, contiguous g and v rows): a step takes a few tens of
+  // nanoseconds, far less than a global load, so the rows come in blocks of ring_b steps by
+  // bulk copies into a double-buffered shared-memory ring (one mbarrier per buffer), one
+  // block ahead of the chain; a step then only reads shared memory.
+  if (a.ring_b > 0) {
+    const int B = a.ring_b, N = a.nsteps;
+    double *ring = wbuf + 16 * (NT / 32) + 8 * 32 + 2;
+    ring += (reinterpret_cast<uintptr_t>(ring) & 8) ? 1 : 0;            // 16-byte aligned
+    uint64_t *bar = reinterpret_cast<uint64_t *>(ring + 4 * (size_t)B * nx);
+    auto issue = [&](int blk) {  // thread 0: rows n0 .. n0+cnt-1 of g (and v) -> buffer blk & 1
+      const int n0 = 1 + blk * B;
+      if (n0 > N) return;
+      const int cnt = min(B, N - n0 + 1), buf = blk & 1;
+      const uint32_t bytes = (uint32_t)cnt * (uint32_t)nx * 8u;
+      mbar_expect_tx(&bar[buf], a.v.base ? 2u * bytes : bytes);
+      tma_load_1d(ring + (size_t)(2 * buf) * B * nx, a.g.base + (a.g.off + n0) * (long long)nx, bytes, &bar[buf]);
+      if (a.v.base)
+        tma_load_1d(ring + (size_t)(2 * buf + 1) * B * nx, a.v.base + (a.v.off + n0) * (long long)nx, bytes,
+                    &bar[buf]);
+    };
+    if (tid == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      issue(0);
+      issue(1);
+    }
+#pragma unroll 1
+    for (int blk = 0; 1 + blk * B <= N; ++blk) {
+      const int n0 = 1 + blk * B, cnt = min(B, N - n0 + 1), buf = blk & 1;
+      mbar_wait(&bar[buf], (uint32_t)((blk >> 1) & 1));
+      const double *gs = ring + (size_t)(2 * buf) * B * nx + tid * P;
+      const double *vs = gs + (size_t)B * nx;
+      // the next step's g and v values are read from shared memory before the current step's
+      // arithmetic (a lone warp issues in order: the load latency then hides behind the step)
+      double *o = const_cast<double *>(a.out.base) + (a.out.off + (long long)n0 * a.out.stride) * nx + tid * P;
+      const long long ostep = a.out.stride * (long long)nx;
+      double gn[P], vn[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        gn[p] = gs[p];
+        vn[p] = a.v.base ? vs[p] : 0.0;
+      }
+#pragma unroll 2
+      for (int d = 0; d < cnt; ++d) {
+        double gc[P], vc[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          gc[p] = gn[p];
+          vc[p] = vn[p];
+        }
+        if (d + 1 < cnt) {
+#pragma unroll
+          for (int p = 0; p < P; ++p) {
+            gn[p] = gs[(d + 1) * nx + p];
+            vn[p] = a.v.base ? vs[(d + 1) * nx + p] : 0.0;
+          }
+        }
+#pragma unroll 1
+        for (int r = 0; r < a.q; ++r) rk(x);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          x[p] = x[p] + gc[p];
+          o[p] = vc[p] + x[p];
+        }
+        o += ostep;
+      }
+      __syncthreads();                    // every thread has read buffer `buf`
+      if (tid == 0) issue(blk + 2);
+    }
+    return;
+  }
   // g_n and v_n do not depend on the chain: a register ring loads them D steps ahead, so
   // their latency (~1 us) overlaps D coarse steps (one-warp rows exchange by shuffles, no
   // barrier).  The ring is indexed at compile time: steps run in blocks of D.
@@ -243,12 +318,23 @@ __global__ void __launch_bounds__(NT, 1) rk_coarse_kernel(const __grid_constant_
 
 template <class SC, bool BND = false>
 static cudaError_t launch_rkc(SweepCfg c, const RKCoarseArgs &a, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (2 * c.nt_threads * (SC::NL + SC::NR) + 4 +
-                                        16 * (c.nt_threads / 32) + 8 * 32 + 2);
+  size_t smem = sizeof(double) * (2 * c.nt_threads * (SC::NL + SC::NR) + 4 +
+                                  16 * (c.nt_threads / 32) + 8 * 32 + 2);
+  // short contiguous rows: shared-memory block ring of ring_b steps (4 arrays of <= 2048 doubles)
+  RKCoarseArgs b = a;
+  b.ring_b = 0;
+  if (a.nx <= 512 && a.nx % 2 == 0 && a.g.stride == 1 && (!a.v.base || a.v.stride == 1) &&
+      a.nsteps >= 16) {
+    b.ring_b = std::min(32, 2048 / a.nx);
+    smem += sizeof(double) * (4 * (size_t)b.ring_b * a.nx + 2) + 2 * sizeof(uint64_t) + 16;
+  }
 #define MG_RKC(NT_, P_)                                                      \
   if (c.nt_threads == NT_ && c.p == P_) {                                    \
     if constexpr (!BND || P_ >= SC::NL + SC::NR + 1) {                       \
-      rk_coarse_kernel<SC, NT_, P_, BND><<<1, NT_, smem, s>>>(a);            \
+      if (smem > 48 * 1024)                                                  \
+        cudaFuncSetAttribute(rk_coarse_kernel<SC, NT_, P_, BND>,             \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      rk_coarse_kernel<SC, NT_, P_, BND><<<1, NT_, smem, s>>>(b);            \
       return cudaGetLastError();                                             \
     } else {                                                                 \
       return cudaErrorInvalidConfiguration;                                  \
