@@ -1,6 +1,7 @@
 /*
- * mgrit.h — C ABI of the B200 MGRIT/Parareal library (libmgrit.so) for the periodic
- * 1D constant-coefficient linear advection equation u_t + alpha u_x = 0.
+ * mgrit.h — C ABI of the B200 MGRIT/Parareal library (libmgrit.so) for the 1D
+ * constant-coefficient linear advection equation u_t + alpha u_x = 0, periodic or
+ * with inflow/outflow boundaries (mgrit_set_inflow).
  *
  * Paper: De Sterck, Falgout, Friedhoff, Krzysik, MacLachlan, "Optimizing MGRIT and
  * Parareal coarse-grid operators for linear advection", arXiv:1910.03726.
