@@ -5,7 +5,8 @@ imports only `oracle/` and `workloads/`: the oracle's MGRIT on the FULL space-ti
  at the graded sizes — cfg3 and cfg4 at 4096 x 16384 exactly as
 BASELINE.json states them, and the cfg5 recipe at 8192 x 65536 (six levels, coarsest
 nt = 64, the full time length of the throughput run; nx halved so the oracle fits in host
-memory, tools/make_goldens.py).  Each golden stores the oracle's Psi coefficients (the
+memory, tools/make_goldens.py), and the two inflow/outflow bench shapes (4096 x 16384
+two-level, 1024 x 4096 four-level; oracle/inflow.py, R20).  Each golden stores the oracle's Psi coefficients (the
 library consumes the same data), the residual history, K, 8 sampled C-rows after every
 iteration and 8 sampled rows of the final FULL solution.
 
@@ -50,7 +51,8 @@ def _workload(meta):
 def test_goldens_present():
     names = {os.path.basename(p) for p in GOLD}
     for n in ("fullsize_cfg3_full.npz", "fullsize_cfg4_full.npz",
-              "fullsize_cfg5_8192x65536.npz"):
+              "fullsize_cfg5_8192x65536.npz", "fullsize_inflow_erk3_full.npz",
+              "fullsize_inflow_erk3_ml_full.npz"):
         assert n in names, n
 
 
@@ -66,6 +68,10 @@ def compare_with_golden(path, options=None):
     assert bool(z["converged"]) and len(ho) == K + 1
     s = binding.MGRIT(w.nx, w.nt, w.m, w.alpha, w.cfl, w.order, w.tableau, w.levels, psi,
                       w.relax, options=options)
+    if meta.get("boundary", "periodic") == "inflow":   # inflow data: the derivative table (R20)
+        stages = s.coefficients()[1].shape[0]
+        dg = W.inflow_sin4_derivatives(np.arange(w.nt) * w.dt, w.order + stages)
+        s.set_inflow(torch.from_numpy(dg).cuda())
     s.set_cycle(meta["cycle"])
     g = problem.device_guess(w)
     s.set_guess(g)

@@ -28,6 +28,7 @@ sys.path.insert(0, ROOT)
 
 import workloads as W  # noqa: E402
 from oracle import discretization as D  # noqa: E402
+from oracle import inflow as I  # noqa: E402
 from oracle import mgrit as M  # noqa: E402
 from oracle import psi as OP  # noqa: E402
 
@@ -36,6 +37,9 @@ GOLDENS = {
     "cfg4_full": lambda: W.CFG4,
     "cfg5_8192x65536": lambda: W.CFG5.scaled(8192, 65536),
     "cfg5_fcycle_1024x16384": lambda: W.CFG5.scaled(1024, 16384, levels=5),
+    # inflow/outflow rows (PAPER.md 4.5; oracle/inflow.py): the bench shapes
+    "inflow_erk3_full": lambda: W.INFLOW_ERK3,
+    "inflow_erk3_ml_full": lambda: W.INFLOW_ERK3_ML,
 }
 CYCLE = {"cfg5_fcycle_1024x16384": "F"}
 N_CROWS = 8      # sampled C-rows stored per iteration (full width)
@@ -60,6 +64,14 @@ def run(name: str) -> str:
     fits = OP.fit_hierarchy(phi, w.nx, w.m, w.cfl, w.psi_widths[: w.levels - 1], w.psi_eta)
     assert all(f.accepted for f in fits)
     phis = [phi] + [D.StencilPhi(f.stencil, w.nx) for f in fits]
+    g0 = None
+    if getattr(w, "boundary", "periodic") == "inflow":
+        # the periodic problem's Psi truncated at the boundaries, the bounded fine propagator
+        # and its forcing rows from the inflow derivative table (R20)
+        ph = I.BoundedRKPhi(w.order, w.tableau, w.cfl, w.nx, w.alpha)
+        dgs = W.inflow_sin4_derivatives(np.arange(w.nt) * w.dt, ph.nq)
+        g0 = I.fine_rhs(ph, w.u0(), dgs)
+        phis = [ph] + [I.TruncatedStencilPhi(f.stencil, w.nx) for f in fits]
     nc = w.nt // w.m
     crow_idx, final_idx = sample_rows(nc, w.nt)
     crows = []
@@ -71,12 +83,13 @@ def run(name: str) -> str:
     U = w.guess()
     t0 = time.time()
     rep = M.solve(U, phis, w.m, w.dx, w.dt, w.relax, w.tol, w.max_iter, cycle=cycle,
-                  on_iter=on_iter)
+                  on_iter=on_iter, g0=g0)
     secs = time.time() - t0
     meta = dict(name=name, workload=w.name, nx=w.nx, nt=w.nt, m=w.m, levels=w.levels,
                 order=w.order, tableau=w.tableau, cfl=w.cfl, relax=w.relax, cycle=cycle,
                 tol=w.tol, max_iter=w.max_iter, u0_kind=w.u0_kind, u0_seed=w.u0_seed,
                 guess_seed=w.guess_seed, guess_lo=w.guess_lo, oracle_seconds=round(secs, 1),
+                boundary=getattr(w, "boundary", "periodic"),
                 generator="tools/make_goldens.py (oracle/ + workloads/ only)")
     out = dict(meta=np.array(json.dumps(meta)), history=np.array(rep.history),
                iterations=np.array(rep.iterations), converged=np.array(rep.converged),
