@@ -307,6 +307,16 @@ typedef enum {
 int mgrit_set_option(mgrit_ctx *ctx, int option, const int *values, int n);
 
 /*
+ * mgrit_overlap_plan — the chunking the overlapped two-level iteration (MGRIT_OPT_OVERLAP)
+ * uses for a coarse chain of nc steps when `want` chunks are asked for (host-only, no GPU):
+ * *chunks = C (0: serial), and for i < C the fine intervals [j0[i], j1[i]) of sweep chunk i
+ * (j0, j1 nullable; room for `want` entries).  Chain chunk i covers the steps iL+1..(i+1)L,
+ * L = nc/C; sweep chunk i is shifted by one interval so that it reads C-rows <= (i+1)L and
+ * overwrites coarse right-hand-side rows <= (i+1)L only.  Errors: EINVAL.
+ */
+int mgrit_overlap_plan(long long nc, int want, int *chunks, long long *j0, long long *j1);
+
+/*
  * ---- Time-parallel MGRIT over several GPUs (the paper parallelises time
  * only, with contiguous blocks of time per processor) ----
  *

@@ -74,6 +74,8 @@ _SIGS = [
     ("mgrit_set_cycle", C.c_int, [C.c_void_p, C.c_int]),
     ("mgrit_set_final_sweep", C.c_int, [C.c_void_p, C.c_int]),
     ("mgrit_set_option", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.c_int]),
+    ("mgrit_overlap_plan", C.c_int, [C.c_longlong, C.c_int, C.POINTER(C.c_int),
+                                     C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     ("mgrit_get_crows", C.c_int, [C.c_void_p, C.c_void_p]),
     ("mgrit_fill_guess", C.c_int, [C.c_void_p, C.c_longlong, C.c_longlong, C.c_int,
                                    C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
@@ -200,6 +202,18 @@ def psi_fit_nl_device(order: int, tableau: str, cfl: float, nx: int, m: int, nt:
     return {"kind": "stencil", "offsets": list(offsets), "coeffs": [cof[a] for a in range(n)],
             "objective": obj.value, "iterations": its.value,
             "history": [hist[i] for i in range(its.value + 1)]}
+
+
+def overlap_plan(nc: int, want: int):
+    """mgrit_overlap_plan: (C, [(j0, j1), ...]) of the overlapped two-level iteration (host-only)."""
+    ch = C.c_int()
+    n = max(1, want)
+    j0 = (C.c_longlong * n)()
+    j1 = (C.c_longlong * n)()
+    st = lib().mgrit_overlap_plan(nc, want, C.byref(ch), j0, j1)
+    if st:
+        raise MgritError(st, "mgrit_overlap_plan")
+    return ch.value, [(j0[i], j1[i]) for i in range(ch.value)]
 
 
 def fill_guess(dst, seed: int, lo: float = -1.0, u0=None, row0: int = 0, stream=None):

@@ -842,6 +842,23 @@ int reduce_norm(mgrit_ctx *c, long long n, double *norm2_host) {
 // V-cycle's coarsest level): trapezoid tiles, one launch, no inter-CTA communication.
 // Long chains (two-level): the row split over a thread-block cluster (DSMEM halos), else
 // one periodic CTA.
+// ---- chunking of the overlapped two-level iteration --------------------
+// Number of chunks actually used for a chain of nc steps when `want` are asked for: the
+// largest C <= want with nc % C == 0, chunk length L = nc/C a multiple of 4 (the chain
+// publishes per half of 4 steps) and L >= 32; 0 if there is none above 1.
+int overlap_chunks(long long nc, int want) {
+  while (want > 1 && (nc % want || (nc / want) % 4 || nc / want < 32)) --want;
+  return want > 1 ? want : 0;
+}
+// Sweep chunk i of C (chunk length L = nc/C): the fine intervals [j0, j1).  Shifted by one
+// interval against the chain's chunks so that it reads only C-rows <= (i+1)L (corrected by
+// chain chunk i) and overwrites only coarse right-hand-side rows <= (i+1)L (consumed by it).
+void overlap_sweep_chunk(long long nc, int C, int i, long long *j0, long long *j1) {
+  const long long L = nc / C;
+  *j0 = i == 0 ? 0 : i * L - 1;
+  *j1 = i + 1 < C ? (i + 1) * L - 1 : nc;
+}
+
 struct CoarsePlan {
   enum Kind { NONE, TILES, CLUSTER, CLUSTER_CA, SEQ, TILES_SEG } kind = NONE;
   SweepCfg cfg = {0, 0};
@@ -1851,6 +1868,14 @@ int mgrit_set_option(mgrit_ctx *c, int option, const int *values, int n) {
   return MGRIT_OK;
 }
 
+int mgrit_overlap_plan(long long nc, int want, int *chunks, long long *j0, long long *j1) {
+  if (nc < 1 || want < 0 || !chunks) return MGRIT_EINVAL;
+  const int C = overlap_chunks(nc, want);
+  *chunks = C;
+  for (int i = 0; i < C && j0 && j1; ++i) overlap_sweep_chunk(nc, C, i, &j0[i], &j1[i]);
+  return MGRIT_OK;
+}
+
 int mgrit_set_cycle(mgrit_ctx *c, int cycle) {
   if (!c) return MGRIT_EINVAL;
   if (cycle != MGRIT_CYCLE_V && cycle != MGRIT_CYCLE_F) return fail(c, MGRIT_EINVAL, "cycle must be V or F");
@@ -2026,7 +2051,7 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     const bool sp = spec_default && fcf;
     int want = opt(c, MGRIT_OPT_OVERLAP) ? c->opt_v[MGRIT_OPT_OVERLAP][0]
                                          : (nc >= 2048 ? (sp ? 8 : 16) : (nc >= 1024 ? (sp ? 4 : 8) : 0));
-    while (want > 1 && (nc % want || (nc / want) % 4 || nc / want < 32)) --want;
+    want = overlap_chunks(nc, want);
     if (chain && want > 1) nchunks = want;
     if (nchunks && !c->wait_value_fn) {   // stream-ordered memory operations (driver entry points)
       cudaDriverEntryPointQueryResult qr;
@@ -2136,8 +2161,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
     for (int i = 0; i < C_; ++i) {
       s2 = wait_chain(par, i + 1);
       if (s2) return s2;
-      const long long j0 = i == 0 ? 0 : i * L - 1;
-      const long long j1 = i + 1 < C_ ? (i + 1) * L - 1 : nc;
+      long long j0, j1;
+      overlap_sweep_chunk(nc, C_, i, &j0, &j1);
       const int reserve = i + 1 < C_ ? (spec ? 32 : 16) : (spec ? 16 : 0);
       s2 = final ? check_sweep(j0, j1 - j0, reserve) : do_sweep(false, true, j0, j1 - j0, reserve);
       if (s2) return s2;
@@ -2345,8 +2370,8 @@ int mgrit_solve(mgrit_ctx *c, double tol, int max_iter, double *out_dev, int *it
       spec_inflight = true;
       spec_par = p2;
       for (int i = 0; i < C_; ++i) {
-        const long long j0 = i == 0 ? 0 : i * L - 1;
-        const long long j1 = i + 1 < C_ ? (i + 1) * L - 1 : nc;
+        long long j0, j1;
+        overlap_sweep_chunk(nc, C_, i, &j0, &j1);
         st = do_sweep(true, false, j0, j1 - j0, 16);
         if (st) return st;
         const int wr = ((mem_fn_t)c->write_value_fn)(user, (unsigned long long)(uintptr_t)(c->prog + 2),
