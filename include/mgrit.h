@@ -269,14 +269,20 @@ int mgrit_set_final_sweep(mgrit_ctx *ctx, int mode);
  *                                                the intervals already corrected follows
  *                                                beside it, released by stream-ordered memory
  *                                                waits (bitwise the serial iteration); 0 or
- *                                                1: serial; default 16 (chains >= 2048
- *                                                steps) / 8 (>= 1024, or speculative).
+ *                                                1: serial; default 16 / 8 chunks for chains
+ *                                                of >= 2048 / >= 1024 steps, halved with a
+ *                                                speculative chain (mgrit_overlap_plan).
  *                                                Optional second value: 1 / 0 = speculative
  *                                                chain on / off (FCF: the chain of iteration
  *                                                k+1 is launched behind the sweep chunks of
  *                                                iteration k, gated on a flag the stream
  *                                                writes after each chunk; default: on when
- *                                                the chain is estimated >= 1.5x the sweep)
+ *                                                the chain is estimated >= 1.5x the sweep).
+ *                                                The speculative chain needs concurrent
+ *                                                kernels: under tools that serialise them
+ *                                                (profiler kernel replay, launch blocking)
+ *                                                use C, 0 -- its gate otherwise gives up
+ *                                                after 10 s with a launch failure
  *   MGRIT_OPT_VOVERLAP       C[, n[, spec]]      V-cycle host-loop solves (halo-tile kernels):
  *                                                the HBM-bound level-1 interpolation in C
  *                                                chunks on a high-priority stream, the
