@@ -40,3 +40,29 @@ def test_chunks_are_hazard_free(nc, want):
 def test_plan_rejects_bad_arguments():
     with pytest.raises(B.MgritError):
         B.overlap_plan(0, 8)
+
+
+def test_psi_fit_nl_argument_checks_without_a_gpu():
+    """mgrit_psi_fit_nl validates its arguments before it touches the device (include/mgrit.h):
+    EINVAL for sizes / a non-contiguous pattern / null pointers, ENOMEM for a short workspace,
+    EUNSUPPORTED for SDIRK tableaux (Appendix B is explicit-only)."""
+    import ctypes as C
+    L = B.lib()
+    offs = (C.c_int * 3)(-2, -1, 0)
+    gap = (C.c_int * 3)(-3, -1, 0)
+    cof = (C.c_double * 3)(0.1, 0.8, 0.1)
+    its, obj = C.c_int(), C.c_double()
+    need = L.mgrit_psi_fit_nl_workspace_bytes(256)
+    assert need > 0 and L.mgrit_psi_fit_nl_workspace_bytes(1) == 0
+    fake = C.c_void_p(0x1000)      # never dereferenced on these paths
+
+    def call(nx=256, tab=B.TABLEAU["erk1"], order=1, m=4, nt=1024, nnz=3, o=offs, ws=fake, nb=need):
+        return L.mgrit_psi_fit_nl(nx, order, tab, 0.85, m, nt, nnz, o, cof, 30, C.byref(its),
+                                  C.byref(obj), None, ws, nb, None)
+
+    assert call(nx=4) == -1                      # EINVAL: nx too small
+    assert call(nt=1023) == -1                   # nt not a multiple of m
+    assert call(o=gap) == -1                     # pattern not contiguous
+    assert call(ws=None) == -1                   # null workspace
+    assert call(nb=need - 1) == -2               # ENOMEM
+    assert call(tab=B.TABLEAU["sdirk1"]) == -5   # EUNSUPPORTED
